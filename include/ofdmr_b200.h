@@ -1,0 +1,152 @@
+/*
+ * ofdmr_b200.h — C-ABI drop-in boundary for the OFDM radar receiver hot path
+ * (arXiv 2209.03883 reference `ofdmradar`).
+ *
+ * The reference exposes the receiver as C++ free functions with value semantics
+ * (namespace ofdmradar).  This header replaces them with batched, stream-ordered
+ * entry points on caller-owned DEVICE pointers (frames contiguous, each frame a
+ * row-major N x M grid of complex64 {float re, im}; rows = subcarrier k,
+ * cols = OFDM symbol l, include/ofdmradar/grid.hpp:14-18), plus one host-buffer
+ * entry point (ofdmr_pipeline_host) that performs the H2D/D2H copies itself.
+ * Each function names the reference interface it replaces.
+ *
+ * Errors: every function returns OFDMR_OK (0), OFDMR_ERR_CONFIG (2, mirrors
+ * ofdmradar::ConfigError, include/ofdmradar/errors.hpp:9-12) or OFDMR_ERR_CUDA (10).
+ * ofdmr_last_error() returns a thread-local message for the last failure.  A zero
+ * X cell (spectral_division's ConfigError, src/estimation.cpp:17) is reported per
+ * frame through the device `status` array (bit 0) — stream-ordered calls cannot
+ * throw; the synchronous host entry point returns OFDMR_ERR_CONFIG for it.
+ *
+ * Sizes: N, M, N', M' must be powers of two in [16, 4096] (B200 design limit; the
+ * reference also accepts other sizes through FFTW), N' >= N, M' >= M
+ * (periodogram.cpp:43, ConfigError otherwise), max_targets <= 64.
+ *
+ * Threading: one context per host thread or stream (the reference functions are
+ * reentrant; this context owns scratch buffers).
+ */
+#ifndef OFDMR_B200_H
+#define OFDMR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OFDMR_OK 0
+#define OFDMR_ERR_CONFIG 2
+#define OFDMR_ERR_CUDA 10
+
+#define OFDMR_WINDOW_RECT 0     /* WindowKind::Rectangular, waveform.hpp:16 */
+#define OFDMR_WINDOW_HAMMING 1  /* WindowKind::Hamming */
+#define OFDMR_EST_LS 0          /* EstimatorKind::Ls and ::ZcpLs (divide by the precoded x_tx), pipeline.cpp:49-53 */
+#define OFDMR_EST_DFT_CE 1      /* EstimatorKind::DftCe, pipeline.cpp:54-55 */
+
+/* Receiver configuration: the subset of WaveformConfig (waveform.hpp:20-41),
+ * EstimatorSettings and DetectorSettings (config.hpp:25-37) the hot path reads. */
+typedef struct ofdmr_config {
+    int32_t n_subcarriers; /* N */
+    int32_t n_symbols;     /* M */
+    int32_t n_prime;       /* N' (delay bins) */
+    int32_t m_prime;       /* M' (Doppler bins) */
+    int32_t window;        /* OFDMR_WINDOW_* */
+    int32_t estimator;     /* OFDMR_EST_* */
+    int32_t n_cp;          /* DFT-CE truncation length L (waveform.n_cp, pipeline.cpp:55) */
+    int32_t max_targets;   /* K_max (detector.max_targets) */
+    double pfa;            /* waveform.pfa */
+    int32_t chunk_frames;  /* frames per internal launch chunk (0 = default) */
+    int32_t device;        /* CUDA device ordinal */
+} ofdmr_config;
+
+/* Fixed-size detection record (Detection, periodogram.hpp:12-18, without the
+ * host-side physics fields which ofdmr_bins_to_physics computes in fp64). */
+typedef struct ofdmr_context ofdmr_context;
+
+/* --- context ------------------------------------------------------------ */
+int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out);
+void ofdmr_destroy(ofdmr_context* ctx);
+/* Subsequent calls enqueue on this cudaStream_t (NULL = legacy default stream). */
+int ofdmr_set_stream(ofdmr_context* ctx, void* cuda_stream);
+const char* ofdmr_last_error(void);
+/* Number of kernel launches enqueued by this context since creation. */
+int64_t ofdmr_launch_count(const ofdmr_context* ctx);
+
+/* Per-stage CUDA-event timing for profiling runs: when on, every kernel launch of the
+ * pipeline / periodogram schedules is bracketed by events.  ofdmr_get_profile syncs the
+ * context stream and returns (then resets) the summed milliseconds and launch counts of
+ * stage 0 (column pass), 1 (row pass + detection), 2 (top-K merge). */
+int ofdmr_set_profiling(ofdmr_context* ctx, int32_t on);
+int ofdmr_get_profile(ofdmr_context* ctx, double* ms3, int64_t* launches3);
+
+/* --- host-side helpers (fp64, bit-identical formulas) -------------------- */
+/* make_window, periodogram.cpp:25-37 (wk: n doubles, wl: m doubles). */
+int ofdmr_make_window(int32_t kind, int32_t n, int32_t m, double* wk, double* wl);
+/* Window2d::power_factor, periodogram.cpp:11-16. */
+double ofdmr_window_power_factor(int32_t kind, int32_t n, int32_t m);
+/* detection_threshold, periodogram.cpp:77-81. */
+int ofdmr_detection_threshold(double sigma2, double pfa, double power_factor, double* eta);
+/* bins_to_physics, periodogram.cpp:138-144 (Ts = (1 + n_cp/N)/df, waveform.hpp:31-35). */
+void ofdmr_bins_to_physics(int64_t delay_bin, int64_t doppler_bin, int32_t n_subcarriers, int32_t n_cp,
+                           int32_t n_prime, int32_t m_prime, double df_hz, double fc_hz, double* range_m,
+                           double* velocity_mps);
+
+/* --- batched device entry points (stream-ordered) ----------------------- */
+/* spectral_division, estimation.cpp:10-21: h = y / x; status[f] bit0 = zero X cell. */
+int ofdmr_spectral_division(ofdmr_context* ctx, const void* y, const void* x, void* h, int32_t* status,
+                            int64_t frames);
+/* dft_ce, estimation.cpp:23-39 (L = cfg.n_cp). */
+int ofdmr_dft_ce(ofdmr_context* ctx, const void* h, void* h_out, int64_t frames);
+/* estimate_channel, pipeline.cpp:47-58 (LS / ZCP-LS / DFT-CE per cfg.estimator). */
+int ofdmr_estimate_channel(ofdmr_context* ctx, const void* y, const void* x_tx, void* h, int32_t* status,
+                           int64_t frames);
+/* periodogram, periodogram.cpp:39-75: p = N' x M' fp32 per frame, Doppler fft-shifted. */
+int ofdmr_periodogram(ofdmr_context* ctx, const void* h, float* p, int64_t frames);
+/* detection_threshold + threshold_mask + extract_peaks, periodogram.cpp:77-136, on a
+ * device map p; sigma2_h[f] is the per-frame post-division noise power.  Records are
+ * [frame][max_targets]; counts[f] valid entries, ordered by (power desc, index asc).
+ * k_per_frame may be NULL (= max_targets). */
+int ofdmr_detect(ofdmr_context* ctx, const float* p, const double* sigma2_h, const int32_t* k_per_frame,
+                 int32_t* delay_bin, int32_t* doppler_bin, float* peak_power, int32_t* counts, int64_t frames);
+/* threshold_mask + extract_peaks, periodogram.cpp:83-136, with the mask given by its
+ * per-frame threshold eta[f] (mask = p >= eta). Same record layout as ofdmr_detect. */
+int ofdmr_extract_peaks(ofdmr_context* ctx, const float* p, const double* eta, const int32_t* k_per_frame,
+                        int32_t* delay_bin, int32_t* doppler_bin, float* peak_power, int32_t* counts,
+                        int64_t frames);
+/* Receiver half of run_pipeline, pipeline.cpp:72-96: y, x_tx -> estimate_channel ->
+ * division_noise_power(sigma2) -> periodogram -> threshold -> extract_peaks.
+ * Optional outputs (NULL to skip): sigma2_h_out [frames], p_out [frames][N'][M'],
+ * status [frames]. */
+int ofdmr_pipeline(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
+                   const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
+                   int32_t* counts, double* sigma2_h_out, float* p_out, int32_t* status, int64_t frames);
+/* Same on HOST buffers (pinned recommended): copies inside, double-buffered, synchronous.
+ * Returns OFDMR_ERR_CONFIG if any frame had a zero X cell. */
+int ofdmr_pipeline_host(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
+                        const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
+                        int32_t* counts, int64_t frames);
+
+/* --- FPS-SFT (sft.cpp:185-490) ------------------------------------------ */
+/* SftConfig, sft.hpp:14-33. */
+typedef struct ofdmr_sft_config {
+    int32_t i_max;
+    double detect_threshold; /* 0 = derive from sigma2/pfa + relative floor */
+    double pfa;
+    int32_t decimation;
+    double frac_tol;
+    double amp_tol;
+    int32_t max_entries;     /* entries kept per frame (<= 64) */
+} ofdmr_sft_config;
+
+/* sft_iterate over a batch of N x M c64 grids h (device).  seeds[f] = SftConfig.seed,
+ * sigma2[f] = SftConfig.sigma2 (host arrays).  Outputs (device, [frame][max_entries]):
+ * k, l, amplitude (complex double re/im interleaved), n_entries, and per-frame stats
+ * (iterations, samples_used, converged, residual_energy; device). */
+int ofdmr_sft(ofdmr_context* ctx, const void* h, int32_t n, int32_t m, const ofdmr_sft_config* cfg,
+              const uint64_t* seeds, const double* sigma2, int32_t* k_out, int32_t* l_out, double* amp_out,
+              int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged,
+              double* residual, int64_t frames);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OFDMR_B200_H */

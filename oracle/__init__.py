@@ -1,0 +1,285 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+Python bindings for
+  * oracle/liboracle.so        — the plain-C fp64 restatement (oracle/oracle.c), and
+  * oracle/_ref/libofdmref.so  — the reference's own sources + substitute FFT (built
+                                 by oracle/Makefile where /root/reference exists).
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this package, and only as the checker / timed CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "liboracle.so"
+REF_SO = HERE / "_ref" / "libofdmref.so"
+
+vp = C.c_void_p
+
+
+class RxConfig(C.Structure):
+    _fields_ = [("n", C.c_int32), ("m", C.c_int32), ("n_prime", C.c_int32), ("m_prime", C.c_int32),
+                ("estimator", C.c_int32), ("n_cp", C.c_int32), ("window", C.c_int32), ("pfa", C.c_double)]
+
+
+class SftConfig(C.Structure):
+    _fields_ = [("i_max", C.c_int64), ("detect_threshold", C.c_double), ("seed", C.c_uint64),
+                ("sigma2", C.c_double), ("pfa", C.c_double), ("decimation", C.c_int64),
+                ("frac_tol", C.c_double), ("amp_tol", C.c_double)]
+
+
+class SftResult(C.Structure):
+    _fields_ = [("n_entries", C.c_int64), ("residual_energy", C.c_double), ("converged", C.c_int32),
+                ("iterations", C.c_int64), ("samples_used", C.c_int64)]
+
+
+_orc = None
+_ref = None
+
+
+def orc() -> C.CDLL:
+    global _orc
+    if _orc is None:
+        if not ORACLE_SO.exists():
+            raise ImportError(f"{ORACLE_SO} missing: run `make -f oracle/Makefile`")
+        _orc = C.CDLL(str(ORACLE_SO))
+        _orc.orc_detection_threshold.restype = C.c_int
+        _orc.orc_division_noise_power.restype = C.c_double
+        _orc.orc_division_noise_power.argtypes = [C.c_double, vp, C.c_size_t]
+        _orc.orc_power_factor.restype = C.c_double
+        _orc.orc_power_factor.argtypes = [vp, C.c_size_t, vp, C.c_size_t]
+        _orc.orc_extract_peaks.restype = C.c_long
+        _orc.orc_extract_peaks.argtypes = [vp, C.c_size_t, C.c_size_t, vp, C.c_size_t, vp, vp, vp]
+        _orc.orc_estimate_noise_power.restype = C.c_double
+        _orc.orc_estimate_noise_power.argtypes = [vp, C.c_size_t, C.c_double]
+        _orc.orc_derive_seed.restype = C.c_uint64
+        _orc.orc_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        _orc.orc_slope_admissible.argtypes = [C.c_long, C.c_long, C.c_size_t, C.c_size_t]
+        _orc.orc_detections_from_spectrum.restype = C.c_long
+        _orc.orc_detections_from_spectrum.argtypes = [vp, vp, vp, vp, C.c_long, C.c_size_t, C.c_size_t, C.c_double,
+                                                      C.c_double, C.c_long, vp, vp, vp]
+        _orc.orc_rng_u64.argtypes = [C.c_uint64, C.c_long, vp]
+        _orc.orc_receive_batch.argtypes = [C.POINTER(RxConfig), vp, vp, vp, C.c_long, vp, C.c_int32, vp, vp, vp, vp,
+                                           vp, vp, C.c_int]
+        _orc.orc_receive_frame.argtypes = [C.POINTER(RxConfig), vp, vp, C.c_double, C.c_int32, vp, vp, vp, vp, vp,
+                                           vp, vp]
+        _orc.orc_sft_iterate.argtypes = [vp, C.c_size_t, C.c_size_t, C.POINTER(SftConfig), C.c_long, vp, vp, vp, vp,
+                                         C.POINTER(SftResult)]
+        _orc.orc_fft.argtypes = [vp, C.c_size_t, C.c_int]
+        sz = C.c_size_t
+        _orc.orc_spectral_division.argtypes = [vp, vp, vp, sz, sz]
+        _orc.orc_dft_ce.argtypes = [vp, vp, sz, sz, sz]
+        _orc.orc_make_window.argtypes = [C.c_int, sz, sz, vp, vp]
+        _orc.orc_periodogram.argtypes = [vp, sz, sz, vp, vp, sz, sz, vp]
+        _orc.orc_detection_threshold.argtypes = [C.c_double, C.c_double, C.c_double, vp]
+    return _orc
+
+
+def ref_available() -> bool:
+    return REF_SO.exists()
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not REF_SO.exists():
+            raise ImportError(f"{REF_SO} missing (built from /root/reference by `make -f oracle/Makefile ref`)")
+        _ref = C.CDLL(str(REF_SO))
+        i64, d = C.c_int64, C.c_double
+        _ref.ref_receive_frame.argtypes = [i64, i64, i64, i64, C.c_int, i64, C.c_int, d, vp, vp, d, i64, vp, vp, vp,
+                                           vp, vp, vp, vp]
+        _ref.ref_receive_batch.argtypes = [i64, i64, i64, i64, C.c_int, i64, C.c_int, d, vp, vp, vp, i64, vp, i64, vp,
+                                           vp, vp, vp, C.c_int]
+        _ref.ref_periodogram.argtypes = [vp, i64, i64, C.c_int, i64, i64, vp]
+        _ref.ref_dft_ce.argtypes = [vp, vp, i64, i64, i64]
+        _ref.ref_spectral_division.argtypes = [vp, vp, vp, i64, i64]
+        _ref.ref_extract_peaks.restype = C.c_long
+        _ref.ref_extract_peaks.argtypes = [vp, i64, i64, d, i64, vp, vp, vp]
+        _ref.ref_window_power_factor.restype = d
+        _ref.ref_window_power_factor.argtypes = [C.c_int, i64, i64]
+        _ref.ref_detection_threshold.argtypes = [d, d, d, vp]
+        _ref.ref_bins_to_physics.argtypes = [C.c_long, C.c_long, i64, i64, i64, i64, d, d, i64, vp, vp]
+        _ref.ref_sft_iterate.argtypes = [vp, i64, i64, i64, d, C.c_uint64, d, d, i64, d, d, i64, vp, vp, vp, vp, vp,
+                                         vp, vp, vp, vp]
+        _ref.ref_sft_batch_c64.argtypes = [vp, i64, i64, i64, i64, vp, vp, d, i64, i64, vp, vp, vp, vp, vp, C.c_int]
+        _ref.ref_make_frame_pair.argtypes = [i64, i64, d, d, i64, C.c_int, vp, vp, i64, d, C.c_uint64, vp, vp, vp]
+        _ref.ref_rng_u64.argtypes = [C.c_uint64, i64, vp]
+    return _ref
+
+
+def _p(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ------------------------------------------------------------------ restatement --
+
+def fft(x: np.ndarray, inverse: bool = False) -> np.ndarray:
+    a = np.ascontiguousarray(x, np.complex128).copy()
+    orc().orc_fft(_p(a), a.size, 1 if inverse else -1)
+    return a
+
+
+def spectral_division(y: np.ndarray, x: np.ndarray) -> np.ndarray:
+    y = np.ascontiguousarray(y, np.complex128)
+    x = np.ascontiguousarray(x, np.complex128)
+    h = np.empty_like(y)
+    rc = orc().orc_spectral_division(_p(y), _p(x), _p(h), C.c_size_t(y.shape[0]), C.c_size_t(y.shape[1]))
+    if rc:
+        raise ValueError("spectral_division: zero cell in X")
+    return h
+
+
+def dft_ce(h: np.ndarray, n_cp: int) -> np.ndarray:
+    h = np.ascontiguousarray(h, np.complex128)
+    out = np.empty_like(h)
+    rc = orc().orc_dft_ce(_p(h), _p(out), C.c_size_t(h.shape[0]), C.c_size_t(h.shape[1]), C.c_size_t(n_cp))
+    if rc:
+        raise ValueError("dft_ce: truncation length exceeds N")
+    return out
+
+
+def make_window(kind: int, n: int, m: int):
+    wk = np.empty(n)
+    wl = np.empty(m)
+    orc().orc_make_window(C.c_int(kind), C.c_size_t(n), C.c_size_t(m), _p(wk), _p(wl))
+    return wk, wl
+
+
+def power_factor(kind: int, n: int, m: int) -> float:
+    wk, wl = make_window(kind, n, m)
+    return orc().orc_power_factor(_p(wk), n, _p(wl), m)
+
+
+def periodogram(h: np.ndarray, kind: int, n_prime: int, m_prime: int) -> np.ndarray:
+    h = np.ascontiguousarray(h, np.complex128)
+    n, m = h.shape
+    wk, wl = make_window(kind, n, m)
+    p = np.empty((n_prime, m_prime))
+    rc = orc().orc_periodogram(_p(h), C.c_size_t(n), C.c_size_t(m), _p(wk), _p(wl), C.c_size_t(n_prime),
+                               C.c_size_t(m_prime), _p(p))
+    if rc:
+        raise ValueError("periodogram: N' >= N and M' >= M required")
+    return p
+
+
+def detection_threshold(sigma2: float, pfa: float, pf: float) -> float:
+    eta = C.c_double()
+    rc = orc().orc_detection_threshold(C.c_double(sigma2), C.c_double(pfa), C.c_double(pf), C.byref(eta))
+    if rc:
+        raise ValueError("threshold: bad arguments")
+    return eta.value
+
+
+def extract_peaks(p: np.ndarray, eta: float, max_targets: int):
+    p = np.ascontiguousarray(p, np.float64)
+    mask = (p >= eta).astype(np.uint8)
+    d = np.zeros(max_targets, np.int64)
+    v = np.zeros(max_targets, np.int64)
+    w = np.zeros(max_targets, np.float64)
+    n = orc().orc_extract_peaks(_p(p), p.shape[0], p.shape[1], _p(mask), max_targets, _p(d), _p(v), _p(w))
+    return [(int(d[i]), int(v[i]), float(w[i])) for i in range(n)]
+
+
+def division_noise_power(sigma2: float, x: np.ndarray) -> float:
+    x = np.ascontiguousarray(x, np.complex128)
+    return orc().orc_division_noise_power(sigma2, _p(x), x.size)
+
+
+def estimate_noise_power(p: np.ndarray, pf: float) -> float:
+    p = np.ascontiguousarray(p, np.float64)
+    return orc().orc_estimate_noise_power(_p(p), p.size, pf)
+
+
+def rx_config(n, m, n_prime, m_prime, estimator, n_cp, window, pfa) -> RxConfig:
+    c = RxConfig()
+    c.n, c.m, c.n_prime, c.m_prime = n, m, n_prime, m_prime
+    c.estimator, c.n_cp, c.window, c.pfa = estimator, n_cp, window, pfa
+    return c
+
+
+def receive_frame(cfg: RxConfig, y: np.ndarray, x: np.ndarray, sigma2: float, max_targets: int,
+                  want_map: bool = False):
+    """run_pipeline's receiver half on one c64 frame (upcast to fp64)."""
+    y = np.ascontiguousarray(y, np.complex64)
+    x = np.ascontiguousarray(x, np.complex64)
+    d = np.zeros(max(max_targets, 1), np.int64)
+    v = np.zeros(max(max_targets, 1), np.int64)
+    w = np.zeros(max(max_targets, 1), np.float64)
+    cnt = C.c_long()
+    s2h = C.c_double()
+    eta = C.c_double()
+    pmap = np.empty((cfg.n_prime, cfg.m_prime)) if want_map else None
+    rc = orc().orc_receive_frame(C.byref(cfg), _p(y), _p(x), sigma2, max_targets, _p(d), _p(v), _p(w), C.byref(cnt),
+                                 C.byref(s2h), C.byref(eta), _p(pmap) if pmap is not None else None)
+    if rc:
+        raise ValueError("oracle receive_frame: config error")
+    dets = [(int(d[i]), int(v[i]), float(w[i])) for i in range(cnt.value)]
+    return dets, s2h.value, eta.value, pmap
+
+
+def receive_batch(cfg: RxConfig, y: np.ndarray, x: np.ndarray, sigma2: np.ndarray, k_max: int,
+                  k_per_frame: np.ndarray | None = None, threads: int | None = None):
+    F = y.shape[0]
+    threads = threads or os.cpu_count() or 1
+    d = np.zeros((F, k_max), np.int64)
+    v = np.zeros((F, k_max), np.int64)
+    w = np.zeros((F, k_max), np.float64)
+    cnt = np.zeros(F, np.int64)
+    s2h = np.zeros(F)
+    eta = np.zeros(F)
+    kp = None if k_per_frame is None else np.ascontiguousarray(k_per_frame, np.int32)
+    rc = orc().orc_receive_batch(C.byref(cfg), _p(y), _p(x), _p(np.ascontiguousarray(sigma2, np.float64)), F,
+                                 _p(kp) if kp is not None else None, k_max, _p(d), _p(v), _p(w), _p(cnt), _p(s2h),
+                                 _p(eta), threads)
+    if rc:
+        raise ValueError("oracle receive_batch: config error")
+    return d, v, w, cnt, s2h, eta
+
+
+def sft_iterate(h: np.ndarray, seed: int, sigma2: float = 0.0, i_max: int = 10, detect_threshold: float = 0.0,
+                pfa: float = 1e-2, decimation: int = 8, frac_tol: float = 0.25, amp_tol: float = 0.35,
+                max_entries: int = 256):
+    h = np.ascontiguousarray(h, np.complex128)
+    c = SftConfig(i_max, detect_threshold, seed, sigma2, pfa, decimation, frac_tol, amp_tol)
+    k = np.zeros(max_entries, np.int64)
+    l = np.zeros(max_entries, np.int64)
+    ar = np.zeros(max_entries)
+    ai = np.zeros(max_entries)
+    res = SftResult()
+    rc = orc().orc_sft_iterate(_p(h), h.shape[0], h.shape[1], C.byref(c), max_entries, _p(k), _p(l), _p(ar), _p(ai),
+                               C.byref(res))
+    if rc:
+        raise ValueError("sft_iterate: empty grid")
+    n = min(res.n_entries, max_entries)
+    ents = [(int(k[i]), int(l[i]), complex(ar[i], ai[i])) for i in range(n)]
+    return dict(entries=ents, residual=res.residual_energy, converged=bool(res.converged),
+                iterations=int(res.iterations), samples_used=int(res.samples_used), n_entries=int(res.n_entries))
+
+
+def detections_from_spectrum(entries, n: int, m: int, sigma2: float, pfa: float, max_targets: int):
+    ne = len(entries)
+    k = np.array([e[0] for e in entries] + [0], np.int64)
+    l = np.array([e[1] for e in entries] + [0], np.int64)
+    ar = np.array([e[2].real for e in entries] + [0.0])
+    ai = np.array([e[2].imag for e in entries] + [0.0])
+    d = np.zeros(max(max_targets, 1), np.int64)
+    v = np.zeros(max(max_targets, 1), np.int64)
+    w = np.zeros(max(max_targets, 1))
+    cnt = orc().orc_detections_from_spectrum(_p(k), _p(l), _p(ar), _p(ai), ne, n, m, sigma2, pfa, max_targets, _p(d),
+                                             _p(v), _p(w))
+    return [(int(d[i]), int(v[i]), float(w[i])) for i in range(cnt)]
+
+
+def rng_u64(seed: int, count: int) -> np.ndarray:
+    out = np.empty(count, np.uint64)
+    orc().orc_rng_u64(seed, count, _p(out))
+    return out
+
+
+def derive_seed(base: int, stream: int) -> int:
+    return int(orc().orc_derive_seed(base, stream))

@@ -1,0 +1,689 @@
+// C-ABI host layer (include/ofdmr_b200.h): context, argument checking with the
+// reference's error semantics, chunked stream-ordered launch schedules, and the
+// host-buffer (H2D/D2H inside) pipeline entry point.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ofdmr_b200.h"
+#include "radar_kernels.cuh"
+#include "sft_kernels.cuh"
+
+namespace ofdmr {
+cudaError_t launch_colpass(const ColArgs& a, int n, int np, int frames, cudaStream_t st);
+cudaError_t launch_rowpass(const RowArgs& a, int mp, int frames, cudaStream_t st);
+cudaError_t launch_merge(const MergeArgs& a, int frames, cudaStream_t st);
+int colpass_tile_cols(int np);
+int rowpass_rows(int mp, int np);
+size_t rowpass_smem(int mp, int rows);
+}  // namespace ofdmr
+
+using namespace ofdmr;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(OFDMR_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define OFDMR_CUDA(call)                                 \
+    do {                                                 \
+        cudaError_t _e = (call);                         \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+bool pow2_in(int v, int lo, int hi) { return v >= lo && v <= hi && (v & (v - 1)) == 0; }
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+}  // namespace
+
+struct ofdmr_context {
+    ofdmr_config cfg{};
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    float2* tw = nullptr;        // 4096-entry e^{-j2pi t/4096}
+    float* wk = nullptr;         // Hamming windows (fp32) or null for rectangular
+    float* wl = nullptr;
+    float2* gbuf = nullptr;      // k-pass intermediate for one chunk
+    double* partial = nullptr;   // per (frame, tile) 1/|x|^2 partials for one chunk
+    unsigned long long* cand = nullptr;  // per (frame, block) top-K keys for one chunk
+    int32_t* status_scratch = nullptr;
+    int64_t chunk = 0;
+    int ntiles = 0;              // M / C of the colpass
+    int rows_per_block = 0;
+    int nblk = 0;
+    int g_rows = 0;              // rows of G (N' or L with the shortcut)
+    bool shortcut = false;
+    double log_pfa = 0.0, pf = 1.0, inv_count = 0.0;
+    float scale = 0.f;
+    int64_t launches = 0;
+    // host-buffer pipeline staging (lazily allocated)
+    void* dev_y[2] = {nullptr, nullptr};
+    void* dev_x[2] = {nullptr, nullptr};
+    double* dev_s2[2] = {nullptr, nullptr};
+    int32_t* dev_k[2] = {nullptr, nullptr};
+    int32_t* dev_d[2] = {nullptr, nullptr};
+    int32_t* dev_dp[2] = {nullptr, nullptr};
+    float* dev_pw[2] = {nullptr, nullptr};
+    int32_t* dev_cnt[2] = {nullptr, nullptr};
+    int32_t* dev_st[2] = {nullptr, nullptr};
+    int32_t* host_st = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};
+    // FPS-SFT scratch
+    SftScratch sft{};
+    // optional per-stage event timing (bench roofline): stage 0 colpass, 1 rowpass, 2 merge
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof;
+    std::vector<cudaEvent_t> ev_pool;
+};
+
+namespace {
+
+cudaEvent_t pool_event(ofdmr_context* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one kernel launch with events when profiling is on.
+struct StageTimer {
+    ofdmr_context* c;
+    int stage;
+    cudaEvent_t a = nullptr;
+    StageTimer(ofdmr_context* ctx, int st) : c(ctx), stage(st) {
+        if (c->profiling) {
+            a = pool_event(c);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~StageTimer() {
+        if (c->profiling) {
+            cudaEvent_t b = pool_event(c);
+            cudaEventRecord(b, c->stream);
+            c->prof.push_back({stage, {a, b}});
+        }
+    }
+};
+
+int check_cfg(const ofdmr_config* c) {
+    if (!c) return fail(OFDMR_ERR_CONFIG, "ofdmr_create: null config");
+    if (!pow2_in(c->n_subcarriers, 16, 4096) || !pow2_in(c->n_symbols, 16, 4096))
+        return fail(OFDMR_ERR_CONFIG, "N and M must be powers of two in [16, 4096]");
+    if (c->n_prime < c->n_subcarriers || c->m_prime < c->n_symbols)
+        return fail(OFDMR_ERR_CONFIG, "periodogram: N' >= N and M' >= M required");
+    if (!pow2_in(c->n_prime, 16, 4096) || !pow2_in(c->m_prime, 16, 4096))
+        return fail(OFDMR_ERR_CONFIG, "N' and M' must be powers of two in [16, 4096]");
+    if (c->n_prime > 4 * c->n_subcarriers) return fail(OFDMR_ERR_CONFIG, "N' <= 4 N supported");
+    if (c->window != OFDMR_WINDOW_RECT && c->window != OFDMR_WINDOW_HAMMING)
+        return fail(OFDMR_ERR_CONFIG, "window must be rectangular or hamming");
+    if (c->estimator != OFDMR_EST_LS && c->estimator != OFDMR_EST_DFT_CE)
+        return fail(OFDMR_ERR_CONFIG, "estimator must be LS or DFT-CE");
+    if (c->estimator == OFDMR_EST_DFT_CE && (c->n_cp < 0 || c->n_cp > c->n_subcarriers))
+        return fail(OFDMR_ERR_CONFIG, "dft_ce: truncation length exceeds N");
+    if (c->max_targets < 1 || c->max_targets > kMaxK) return fail(OFDMR_ERR_CONFIG, "max_targets must be in [1, 64]");
+    if (!(c->pfa > 0.0 && c->pfa <= 1.0)) return fail(OFDMR_ERR_CONFIG, "threshold: pfa must lie in (0,1]");
+    return OFDMR_OK;
+}
+
+void make_window_d(int kind, int n, int m, double* wk, double* wl) {
+    for (int k = 0; k < n; ++k) wk[k] = 1.0;
+    for (int l = 0; l < m; ++l) wl[l] = 1.0;
+    if (kind == OFDMR_WINDOW_HAMMING) {
+        for (int k = 0; k < n; ++k) wk[k] = 0.54 - 0.46 * std::cos(kTwoPi * double(k) / double(n - 1));
+        for (int l = 0; l < m; ++l) wl[l] = 0.54 - 0.46 * std::cos(kTwoPi * double(l) / double(m - 1));
+    }
+}
+
+double power_factor_d(int kind, int n, int m) {
+    std::vector<double> wk(n), wl(m);
+    make_window_d(kind, n, m, wk.data(), wl.data());
+    double sk = 0.0, sl = 0.0;
+    for (double v : wk) sk += v * v;
+    for (double v : wl) sl += v * v;
+    return sk * sl / (double(n) * double(m));
+}
+
+size_t cells(const ofdmr_context* c) { return size_t(c->cfg.n_subcarriers) * size_t(c->cfg.n_symbols); }
+
+ColArgs base_col(ofdmr_context* c) {
+    ColArgs a{};
+    a.tw = c->tw;
+    a.m = c->cfg.n_symbols;
+    a.ntiles = c->ntiles;
+    return a;
+}
+
+int launch_col(ofdmr_context* c, const ColArgs& a, int np, int64_t frames) {
+    StageTimer t(c, 0);
+    const cudaError_t e = launch_colpass(a, c->cfg.n_subcarriers, np, int(frames), c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "colpass");
+    ++c->launches;
+    return OFDMR_OK;
+}
+
+// k-pass -> row-pass (+detect) -> merge over one chunk of frames.
+int run_pipeline_chunk(ofdmr_context* c, const float2* y, const float2* x, const double* sigma2,
+                       const int32_t* kpf, int32_t* d, int32_t* dp, float* pw, int32_t* cnt, double* s2h_out,
+                       float* p_out, int32_t* status, int64_t nf) {
+    const ofdmr_config& g = c->cfg;
+    ColArgs a = base_col(c);
+    a.y = y;
+    a.x = x;
+    a.g_out = c->gbuf;
+    if (g.window == OFDMR_WINDOW_HAMMING) {
+        a.wk = c->wk;
+        a.wl = c->wl;
+    }
+    a.inv_partial = c->partial;
+    a.status = status;
+    a.ce_taps = g.estimator == OFDMR_EST_DFT_CE ? g.n_cp : 0;
+    a.shortcut = c->shortcut ? 1 : 0;
+    a.g_rows = c->g_rows;
+    int rc = launch_col(c, a, g.n_prime, nf);
+    if (rc) return rc;
+
+    RowArgs r{};
+    r.g = c->gbuf;
+    r.p_out = p_out;
+    r.inv_partial = c->partial;
+    r.ntiles = c->ntiles;
+    r.sigma2 = sigma2;
+    r.log_pfa = c->log_pfa;
+    r.power_factor = c->pf;
+    r.inv_count = c->inv_count;
+    r.scale = c->scale;
+    r.tw = c->tw;
+    r.n_prime = g.n_prime;
+    r.g_rows = c->g_rows;
+    r.m = g.n_symbols;
+    r.rows_per_block = c->rows_per_block;
+    r.kmax = g.max_targets;
+    r.cand = c->cand;
+    r.detect = 1;
+    cudaError_t e;
+    {
+        StageTimer t(c, 1);
+        e = launch_rowpass(r, g.m_prime, int(nf), c->stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "rowpass");
+    ++c->launches;
+
+    MergeArgs mg{};
+    mg.cand = c->cand;
+    mg.nblk = c->nblk;
+    mg.kmax = g.max_targets;
+    mg.k_per_frame = kpf;
+    mg.m_prime = g.m_prime;
+    mg.det_delay = d;
+    mg.det_doppler = dp;
+    mg.det_power = pw;
+    mg.counts = cnt;
+    mg.inv_partial = c->partial;
+    mg.ntiles = c->ntiles;
+    mg.sigma2 = sigma2;
+    mg.log_pfa = c->log_pfa;
+    mg.power_factor = c->pf;
+    mg.inv_count = c->inv_count;
+    mg.s2h_out = s2h_out;
+    {
+        StageTimer t(c, 2);
+        e = launch_merge(mg, int(nf), c->stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "merge");
+    ++c->launches;
+    return OFDMR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ofdmr_last_error(void) { return g_last_error.c_str(); }
+
+int ofdmr_make_window(int32_t kind, int32_t n, int32_t m, double* wk, double* wl) {
+    if (n <= 0 || m <= 0) return fail(OFDMR_ERR_CONFIG, "make_window: empty");
+    make_window_d(kind, n, m, wk, wl);
+    return OFDMR_OK;
+}
+
+double ofdmr_window_power_factor(int32_t kind, int32_t n, int32_t m) { return power_factor_d(kind, n, m); }
+
+int ofdmr_detection_threshold(double sigma2, double pfa, double power_factor, double* eta) {
+    if (sigma2 < 0.0) return fail(OFDMR_ERR_CONFIG, "threshold: sigma2 must be >= 0");
+    if (!(pfa > 0.0 && pfa <= 1.0)) return fail(OFDMR_ERR_CONFIG, "threshold: pfa must lie in (0,1]");
+    *eta = -sigma2 * std::log(pfa) * power_factor;
+    return OFDMR_OK;
+}
+
+void ofdmr_bins_to_physics(int64_t delay_bin, int64_t doppler_bin, int32_t n_subcarriers, int32_t n_cp,
+                           int32_t n_prime, int32_t m_prime, double df_hz, double fc_hz, double* range_m,
+                           double* velocity_mps) {
+    const double c = 3.0e8;
+    const double t_useful = 1.0 / df_hz;
+    const double ts = t_useful + double(n_cp) * (t_useful / double(n_subcarriers));
+    *range_m = c * double(delay_bin) / (2.0 * double(n_prime) * df_hz);
+    *velocity_mps = c * double(doppler_bin) / (2.0 * fc_hz * double(m_prime) * ts);
+}
+
+int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
+    if (!out) return fail(OFDMR_ERR_CONFIG, "ofdmr_create: null out");
+    *out = nullptr;
+    int rc = check_cfg(cfg);
+    if (rc) return rc;
+    int ndev = 0;
+    OFDMR_CUDA(cudaGetDeviceCount(&ndev));
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(OFDMR_ERR_CONFIG, "device ordinal out of range");
+    OFDMR_CUDA(cudaSetDevice(cfg->device));
+    auto* c = new ofdmr_context();
+    c->cfg = *cfg;
+    c->device = cfg->device;
+    const int n = cfg->n_subcarriers, m = cfg->n_symbols, np = cfg->n_prime, mp = cfg->m_prime;
+    c->shortcut = cfg->estimator == OFDMR_EST_DFT_CE && cfg->window == OFDMR_WINDOW_RECT && np == n;
+    c->g_rows = c->shortcut ? cfg->n_cp : np;
+    if (c->shortcut && c->g_rows == 0) c->g_rows = 1;  // L = 0: all-zero estimate, keep one zero row
+    c->ntiles = m / colpass_tile_cols(np);
+    c->rows_per_block = rowpass_rows(mp, np);
+    c->nblk = (np + c->rows_per_block - 1) / c->rows_per_block;
+    c->log_pfa = std::log(cfg->pfa);
+    c->pf = power_factor_d(cfg->window, n, m);
+    c->inv_count = 1.0 / double(size_t(n) * size_t(m));
+    c->scale = float(1.0 / (double(n) * double(m)));
+    const size_t gframe = size_t(c->g_rows) * size_t(m) * sizeof(float2);
+    int64_t chunk = cfg->chunk_frames;
+    if (chunk <= 0) {
+        chunk = int64_t((48ull << 20) / gframe);  // keep the intermediate L2-resident
+        if (chunk < 1) chunk = 1;
+        if (chunk > 256) chunk = 256;
+    }
+    c->chunk = chunk;
+
+    std::vector<float2> tw(kTwLenHost);
+    for (int t = 0; t < kTwLenHost; ++t) {
+        const double a = -kTwoPi * double(t) / double(kTwLenHost);
+        tw[t] = make_float2(float(std::cos(a)), float(std::sin(a)));
+    }
+    cudaError_t e = cudaMalloc(&c->tw, sizeof(float2) * kTwLenHost);
+    if (e == cudaSuccess) e = cudaMemcpy(c->tw, tw.data(), sizeof(float2) * kTwLenHost, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && cfg->window == OFDMR_WINDOW_HAMMING) {
+        std::vector<double> wk(n), wl(m);
+        make_window_d(cfg->window, n, m, wk.data(), wl.data());
+        std::vector<float> fk(wk.begin(), wk.end()), fl(wl.begin(), wl.end());
+        e = cudaMalloc(&c->wk, sizeof(float) * n);
+        if (e == cudaSuccess) e = cudaMalloc(&c->wl, sizeof(float) * m);
+        if (e == cudaSuccess) e = cudaMemcpy(c->wk, fk.data(), sizeof(float) * n, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(c->wl, fl.data(), sizeof(float) * m, cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&c->gbuf, gframe * size_t(chunk));
+    if (e == cudaSuccess) e = cudaMalloc(&c->partial, sizeof(double) * size_t(c->ntiles) * size_t(chunk));
+    if (e == cudaSuccess)
+        e = cudaMalloc(&c->cand, sizeof(unsigned long long) * size_t(c->nblk) * cfg->max_targets * size_t(chunk));
+    if (e == cudaSuccess) e = cudaMalloc(&c->status_scratch, sizeof(int32_t) * size_t(chunk));
+    if (e != cudaSuccess) {
+        ofdmr_destroy(c);
+        return cuda_fail(e, "ofdmr_create: allocation");
+    }
+    *out = c;
+    return OFDMR_OK;
+}
+
+void ofdmr_destroy(ofdmr_context* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaFree(c->tw);
+    cudaFree(c->wk);
+    cudaFree(c->wl);
+    cudaFree(c->gbuf);
+    cudaFree(c->partial);
+    cudaFree(c->cand);
+    cudaFree(c->status_scratch);
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(c->dev_y[i]);
+        cudaFree(c->dev_x[i]);
+        cudaFree(c->dev_s2[i]);
+        cudaFree(c->dev_k[i]);
+        cudaFree(c->dev_d[i]);
+        cudaFree(c->dev_dp[i]);
+        cudaFree(c->dev_pw[i]);
+        cudaFree(c->dev_cnt[i]);
+        cudaFree(c->dev_st[i]);
+        if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+        if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+    }
+    if (c->host_st) cudaFreeHost(c->host_st);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    sft_free(c->sft);
+    for (auto& p : c->prof) {
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    delete c;
+}
+
+int ofdmr_set_stream(ofdmr_context* c, void* s) {
+    if (!c) return fail(OFDMR_ERR_CONFIG, "null context");
+    c->stream = static_cast<cudaStream_t>(s);
+    return OFDMR_OK;
+}
+
+int64_t ofdmr_launch_count(const ofdmr_context* c) { return c ? c->launches : 0; }
+
+int ofdmr_set_profiling(ofdmr_context* c, int32_t on) {
+    if (!c) return fail(OFDMR_ERR_CONFIG, "null context");
+    c->profiling = on != 0;
+    return OFDMR_OK;
+}
+
+int ofdmr_get_profile(ofdmr_context* c, double* ms, int64_t* launches) {
+    if (!c || !ms || !launches) return fail(OFDMR_ERR_CONFIG, "get_profile: null argument");
+    for (int i = 0; i < 3; ++i) {
+        ms[i] = 0.0;
+        launches[i] = 0;
+    }
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    OFDMR_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& p : c->prof) {
+        float t = 0.f;
+        OFDMR_CUDA(cudaEventElapsedTime(&t, p.second.first, p.second.second));
+        ms[p.first] += t;
+        launches[p.first] += 1;
+        c->ev_pool.push_back(p.second.first);
+        c->ev_pool.push_back(p.second.second);
+    }
+    c->prof.clear();
+    return OFDMR_OK;
+}
+
+int ofdmr_spectral_division(ofdmr_context* c, const void* y, const void* x, void* h, int32_t* status,
+                            int64_t frames) {
+    if (!c || !y || !x || !h || !status) return fail(OFDMR_ERR_CONFIG, "spectral_division: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
+    const size_t fc = cells(c);
+    for (int64_t f0 = 0; f0 < frames; f0 += 65535) {
+        const int64_t nf = std::min<int64_t>(65535, frames - f0);
+        ColArgs a = base_col(c);
+        a.y = static_cast<const float2*>(y) + fc * f0;
+        a.x = static_cast<const float2*>(x) + fc * f0;
+        a.h_out = static_cast<float2*>(h) + fc * f0;
+        a.status = status + f0;
+        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf);
+        if (rc) return rc;
+    }
+    return OFDMR_OK;
+}
+
+int ofdmr_dft_ce(ofdmr_context* c, const void* h, void* h_out, int64_t frames) {
+    if (!c || !h || !h_out) return fail(OFDMR_ERR_CONFIG, "dft_ce: null argument");
+    if (c->cfg.n_cp > c->cfg.n_subcarriers) return fail(OFDMR_ERR_CONFIG, "dft_ce: truncation length exceeds N");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const size_t fc = cells(c);
+    for (int64_t f0 = 0; f0 < frames; f0 += 65535) {
+        const int64_t nf = std::min<int64_t>(65535, frames - f0);
+        ColArgs a = base_col(c);
+        a.h = static_cast<const float2*>(h) + fc * f0;
+        a.h_out = static_cast<float2*>(h_out) + fc * f0;
+        a.hout_after_ce = 1;
+        a.ce_taps = c->cfg.n_cp;
+        if (a.ce_taps == 0) {  // everything truncated: H' = 0
+            OFDMR_CUDA(cudaMemsetAsync(a.h_out, 0, sizeof(float2) * fc * size_t(nf), c->stream));
+            continue;
+        }
+        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf);
+        if (rc) return rc;
+    }
+    return OFDMR_OK;
+}
+
+int ofdmr_estimate_channel(ofdmr_context* c, const void* y, const void* x, void* h, int32_t* status,
+                           int64_t frames) {
+    if (!c || !y || !x || !h || !status) return fail(OFDMR_ERR_CONFIG, "estimate_channel: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    if (c->cfg.estimator != OFDMR_EST_DFT_CE || c->cfg.n_cp == 0) {
+        int rc = ofdmr_spectral_division(c, y, x, h, status, frames);
+        if (rc || c->cfg.estimator != OFDMR_EST_DFT_CE) return rc;
+        return ofdmr_dft_ce(c, h, h, frames);
+    }
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
+    const size_t fc = cells(c);
+    for (int64_t f0 = 0; f0 < frames; f0 += 65535) {
+        const int64_t nf = std::min<int64_t>(65535, frames - f0);
+        ColArgs a = base_col(c);
+        a.y = static_cast<const float2*>(y) + fc * f0;
+        a.x = static_cast<const float2*>(x) + fc * f0;
+        a.h_out = static_cast<float2*>(h) + fc * f0;
+        a.hout_after_ce = 1;
+        a.ce_taps = c->cfg.n_cp;
+        a.status = status + f0;
+        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf);
+        if (rc) return rc;
+    }
+    return OFDMR_OK;
+}
+
+int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames) {
+    if (!c || !h || !p) return fail(OFDMR_ERR_CONFIG, "periodogram: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const ofdmr_config& g = c->cfg;
+    const size_t fc = cells(c);
+    const size_t pframe = size_t(g.n_prime) * size_t(g.m_prime);
+    // the general (non-shortcut) G layout is always N' rows; the chunk buffer holds g_rows rows
+    const int64_t chunk = c->shortcut ? std::max<int64_t>(1, c->chunk * c->g_rows / g.n_prime) : c->chunk;
+    for (int64_t f0 = 0; f0 < frames; f0 += chunk) {
+        const int64_t nf = std::min<int64_t>(chunk, frames - f0);
+        ColArgs a = base_col(c);
+        a.h = static_cast<const float2*>(h) + fc * f0;
+        a.g_out = c->gbuf;
+        a.g_rows = g.n_prime;
+        if (g.window == OFDMR_WINDOW_HAMMING) {
+            a.wk = c->wk;
+            a.wl = c->wl;
+        }
+        int rc = launch_col(c, a, g.n_prime, nf);
+        if (rc) return rc;
+        RowArgs r{};
+        r.g = c->gbuf;
+        r.p_out = p + pframe * f0;
+        r.scale = c->scale;
+        r.tw = c->tw;
+        r.n_prime = g.n_prime;
+        r.g_rows = g.n_prime;
+        r.m = g.n_symbols;
+        r.rows_per_block = c->rows_per_block;
+        r.kmax = g.max_targets;
+        r.detect = 0;
+        cudaError_t e;
+        {
+            StageTimer t(c, 1);
+            e = launch_rowpass(r, g.m_prime, int(nf), c->stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "rowpass");
+        ++c->launches;
+    }
+    return OFDMR_OK;
+}
+
+static int detect_impl(ofdmr_context* c, const float* p, const double* sigma2_h, const double* eta, const int32_t* kpf,
+                       int32_t* d, int32_t* dp, float* pw, int32_t* cnt, int64_t frames) {
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const ofdmr_config& g = c->cfg;
+    const size_t pframe = size_t(g.n_prime) * size_t(g.m_prime);
+    const int K = g.max_targets;
+    // cand buffer is sized for c->chunk frames of this context's N'
+    for (int64_t f0 = 0; f0 < frames; f0 += c->chunk) {
+        const int64_t nf = std::min<int64_t>(c->chunk, frames - f0);
+        RowArgs r{};
+        r.p_in = p + pframe * f0;
+        r.sigma2 = sigma2_h ? sigma2_h + f0 : nullptr;
+        r.eta_in = eta ? eta + f0 : nullptr;
+        r.log_pfa = c->log_pfa;
+        r.power_factor = c->pf;
+        r.tw = c->tw;
+        r.n_prime = g.n_prime;
+        r.g_rows = g.n_prime;
+        r.m = g.n_symbols;
+        r.rows_per_block = c->rows_per_block;
+        r.kmax = K;
+        r.cand = c->cand;
+        r.detect = 1;
+        cudaError_t e = launch_rowpass(r, g.m_prime, int(nf), c->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "rowpass(detect)");
+        ++c->launches;
+        MergeArgs mg{};
+        mg.cand = c->cand;
+        mg.nblk = c->nblk;
+        mg.kmax = K;
+        mg.k_per_frame = kpf ? kpf + f0 : nullptr;
+        mg.m_prime = g.m_prime;
+        mg.det_delay = d + size_t(K) * f0;
+        mg.det_doppler = dp + size_t(K) * f0;
+        mg.det_power = pw + size_t(K) * f0;
+        mg.counts = cnt + f0;
+        mg.sigma2 = sigma2_h ? sigma2_h + f0 : nullptr;
+        e = launch_merge(mg, int(nf), c->stream);
+        if (e != cudaSuccess) return cuda_fail(e, "merge");
+        ++c->launches;
+    }
+    return OFDMR_OK;
+}
+
+int ofdmr_detect(ofdmr_context* c, const float* p, const double* sigma2_h, const int32_t* kpf, int32_t* d,
+                 int32_t* dp, float* pw, int32_t* cnt, int64_t frames) {
+    if (!c || !p || !sigma2_h || !d || !dp || !pw || !cnt) return fail(OFDMR_ERR_CONFIG, "detect: null argument");
+    return detect_impl(c, p, sigma2_h, nullptr, kpf, d, dp, pw, cnt, frames);
+}
+
+int ofdmr_extract_peaks(ofdmr_context* c, const float* p, const double* eta, const int32_t* kpf, int32_t* d,
+                        int32_t* dp, float* pw, int32_t* cnt, int64_t frames) {
+    if (!c || !p || !eta || !d || !dp || !pw || !cnt) return fail(OFDMR_ERR_CONFIG, "extract_peaks: null argument");
+    return detect_impl(c, p, nullptr, eta, kpf, d, dp, pw, cnt, frames);
+}
+
+int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double* sigma2, const int32_t* kpf,
+                   int32_t* d, int32_t* dp, float* pw, int32_t* cnt, double* s2h_out, float* p_out,
+                   int32_t* status, int64_t frames) {
+    if (!c || !y || !x || !sigma2 || !d || !dp || !pw || !cnt) return fail(OFDMR_ERR_CONFIG, "pipeline: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const ofdmr_config& g = c->cfg;
+    const size_t fc = cells(c);
+    const size_t pframe = size_t(g.n_prime) * size_t(g.m_prime);
+    const int K = g.max_targets;
+    if (status) OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
+    for (int64_t f0 = 0; f0 < frames; f0 += c->chunk) {
+        const int64_t nf = std::min<int64_t>(c->chunk, frames - f0);
+        int32_t* st = status ? status + f0 : c->status_scratch;
+        if (!status) OFDMR_CUDA(cudaMemsetAsync(st, 0, sizeof(int32_t) * size_t(nf), c->stream));
+        const int rc = run_pipeline_chunk(
+            c, static_cast<const float2*>(y) + fc * f0, static_cast<const float2*>(x) + fc * f0, sigma2 + f0,
+            kpf ? kpf + f0 : nullptr, d + size_t(K) * f0, dp + size_t(K) * f0, pw + size_t(K) * f0, cnt + f0,
+            s2h_out ? s2h_out + f0 : nullptr, p_out ? p_out + pframe * f0 : nullptr, st, nf);
+        if (rc) return rc;
+    }
+    return OFDMR_OK;
+}
+
+int ofdmr_pipeline_host(ofdmr_context* c, const void* y, const void* x, const double* sigma2, const int32_t* kpf,
+                        int32_t* d, int32_t* dp, float* pw, int32_t* cnt, int64_t frames) {
+    if (!c || !y || !x || !sigma2 || !d || !dp || !pw || !cnt)
+        return fail(OFDMR_ERR_CONFIG, "pipeline_host: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const int64_t ch = c->chunk;
+    const size_t fc = cells(c);
+    const size_t fbytes = fc * sizeof(float2);
+    const int K = c->cfg.max_targets;
+    if (!c->dev_y[0]) {
+        for (int i = 0; i < 2; ++i) {
+            OFDMR_CUDA(cudaMalloc(&c->dev_y[i], fbytes * size_t(ch)));
+            OFDMR_CUDA(cudaMalloc(&c->dev_x[i], fbytes * size_t(ch)));
+            OFDMR_CUDA(cudaMalloc(&c->dev_s2[i], sizeof(double) * size_t(ch)));
+            OFDMR_CUDA(cudaMalloc(&c->dev_k[i], sizeof(int32_t) * size_t(ch)));
+            OFDMR_CUDA(cudaMalloc(&c->dev_d[i], sizeof(int32_t) * size_t(ch) * K));
+            OFDMR_CUDA(cudaMalloc(&c->dev_dp[i], sizeof(int32_t) * size_t(ch) * K));
+            OFDMR_CUDA(cudaMalloc(&c->dev_pw[i], sizeof(float) * size_t(ch) * K));
+            OFDMR_CUDA(cudaMalloc(&c->dev_cnt[i], sizeof(int32_t) * size_t(ch)));
+            OFDMR_CUDA(cudaMalloc(&c->dev_st[i], sizeof(int32_t) * size_t(ch)));
+            OFDMR_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+            OFDMR_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+        }
+        OFDMR_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        OFDMR_CUDA(cudaMallocHost(&c->host_st, sizeof(int32_t) * size_t(ch)));
+    }
+    bool zero_cell = false;
+    int64_t idx = 0;
+    for (int64_t f0 = 0; f0 < frames; f0 += ch, ++idx) {
+        const int b = int(idx & 1);
+        const int64_t nf = std::min<int64_t>(ch, frames - f0);
+        // copy stream: wait until chunk idx-2 released buffer b, then stage inputs
+        OFDMR_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_done[b], 0));
+        OFDMR_CUDA(cudaMemcpyAsync(c->dev_y[b], static_cast<const char*>(y) + fbytes * f0, fbytes * nf,
+                                   cudaMemcpyHostToDevice, c->copy_stream));
+        OFDMR_CUDA(cudaMemcpyAsync(c->dev_x[b], static_cast<const char*>(x) + fbytes * f0, fbytes * nf,
+                                   cudaMemcpyHostToDevice, c->copy_stream));
+        OFDMR_CUDA(cudaMemcpyAsync(c->dev_s2[b], sigma2 + f0, sizeof(double) * nf, cudaMemcpyHostToDevice,
+                                   c->copy_stream));
+        if (kpf)
+            OFDMR_CUDA(cudaMemcpyAsync(c->dev_k[b], kpf + f0, sizeof(int32_t) * nf, cudaMemcpyHostToDevice,
+                                       c->copy_stream));
+        OFDMR_CUDA(cudaEventRecord(c->ev_copied[b], c->copy_stream));
+        OFDMR_CUDA(cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
+        int rc = ofdmr_pipeline(c, c->dev_y[b], c->dev_x[b], c->dev_s2[b], kpf ? c->dev_k[b] : nullptr, c->dev_d[b],
+                                c->dev_dp[b], c->dev_pw[b], c->dev_cnt[b], nullptr, nullptr, c->dev_st[b], nf);
+        if (rc) return rc;
+        OFDMR_CUDA(cudaMemcpyAsync(d + size_t(K) * f0, c->dev_d[b], sizeof(int32_t) * K * nf, cudaMemcpyDeviceToHost,
+                                   c->stream));
+        OFDMR_CUDA(cudaMemcpyAsync(dp + size_t(K) * f0, c->dev_dp[b], sizeof(int32_t) * K * nf,
+                                   cudaMemcpyDeviceToHost, c->stream));
+        OFDMR_CUDA(cudaMemcpyAsync(pw + size_t(K) * f0, c->dev_pw[b], sizeof(float) * K * nf, cudaMemcpyDeviceToHost,
+                                   c->stream));
+        OFDMR_CUDA(cudaMemcpyAsync(cnt + f0, c->dev_cnt[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, c->stream));
+        OFDMR_CUDA(cudaMemcpyAsync(c->host_st, c->dev_st[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, c->stream));
+        OFDMR_CUDA(cudaEventRecord(c->ev_done[b], c->stream));
+        OFDMR_CUDA(cudaStreamSynchronize(c->stream));  // host_st is single-buffered
+        for (int64_t i = 0; i < nf; ++i) zero_cell |= (c->host_st[i] & 1) != 0;
+    }
+    OFDMR_CUDA(cudaStreamSynchronize(c->stream));
+    if (zero_cell) return fail(OFDMR_ERR_CONFIG, "spectral_division: zero cell in X");
+    return OFDMR_OK;
+}
+
+int ofdmr_sft(ofdmr_context* c, const void* h, int32_t n, int32_t m, const ofdmr_sft_config* cfg,
+              const uint64_t* seeds, const double* sigma2, int32_t* k_out, int32_t* l_out, double* amp_out,
+              int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged, double* residual,
+              int64_t frames) {
+    if (!c || !h || !cfg || !seeds || !sigma2 || !k_out || !l_out || !amp_out || !n_entries)
+        return fail(OFDMR_ERR_CONFIG, "sft: null argument");
+    if (n <= 0 || m <= 0) return fail(OFDMR_ERR_CONFIG, "sft_iterate: empty grid");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    std::string err;
+    const int rc = sft_run(c->sft, c->stream, static_cast<const float2*>(h), n, m, *cfg, seeds, sigma2, k_out, l_out,
+                           amp_out, n_entries, iterations, samples_used, converged, residual, frames, &c->launches, err);
+    if (rc) return fail(rc, err);
+    return OFDMR_OK;
+}
+
+}  // extern "C"

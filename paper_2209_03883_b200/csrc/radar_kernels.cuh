@@ -1,0 +1,83 @@
+// Receiver hot-path kernels (sm_100a): subcarrier-axis column pass, symbol-axis row
+// pass with fused |.|^2 / fftshift / strict-3x3-local-max detection, and the per-frame
+// top-K merge.  Host launch code lives in capi.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ofdmr {
+
+constexpr int kNT = 256;      // threads per CTA for the FFT passes
+constexpr int kTwLenHost = 4096;  // twiddle table length (fft_smem.cuh kTwLen)
+constexpr int kMaxK = 64;     // max detections per frame (reference default max_targets, config.hpp:33)
+
+// Column (subcarrier / delay axis) pass over tiles of C adjacent columns of one frame.
+struct ColArgs {
+    const float2* y;        // LS inputs: received frame Y (N x M per frame) ...
+    const float2* x;        // ... and transmitted (possibly ZC-precoded) x_tx; or null
+    const float2* h;        // channel-estimate input when y == null
+    float2* h_out;          // optional: H (hout_after_ce = 0) or H' after DFT-CE (= 1)
+    float2* g_out;          // optional: k-pass output G (g_rows x M per frame)
+    const float* wk;        // subcarrier window (N), null = rectangular
+    const float* wl;        // symbol window (M), null = rectangular
+    double* inv_partial;    // per (frame, tile) sum of 1/|x|^2, deterministic; or null
+    int* status;            // per frame: bit0 = zero X cell (estimation.cpp:17)
+    const float2* tw;       // 4096-entry twiddle table
+    int m;                  // columns M
+    int ce_taps;            // DFT-CE truncation L (0 = no DFT-CE)
+    int hout_after_ce;
+    int shortcut;           // rect window, N' = N, DFT-CE: G = IFFT_N(H) rows < L
+    int g_rows;             // rows of G written per frame
+    int ntiles;             // M / C
+};
+
+// Row (symbol / Doppler axis) pass over blocks of R rows of one frame (+ 1 halo row
+// each side) with the detection fused in.
+struct RowArgs {
+    const float2* g;        // G (g_rows x m per frame), or null when p_in is given
+    const float* p_in;      // P (n_prime x m_prime) for the detect-only entry point
+    float* p_out;           // optional periodogram map out (n_prime x m_prime, fft-shifted)
+    const double* inv_partial;  // per (frame, tile) 1/|x|^2 partials, or null
+    int ntiles;
+    const double* sigma2;   // per frame: noise sigma^2 (with partials) or sigma_h^2 (without)
+    const double* eta_in;   // per frame threshold given directly (extract_peaks on a mask), or null
+    double log_pfa;         // log(pfa) computed on the host (periodogram.cpp:80)
+    double power_factor;    // window power factor (periodogram.cpp:11-16)
+    double inv_count;       // 1 / (N M) for division_noise_power (pipeline.cpp:22)
+    float scale;            // 1 / (N M) periodogram scale (periodogram.cpp:65)
+    const float2* tw;
+    int n_prime;            // rows of P
+    int g_rows;             // rows of G that are non-zero (rows >= g_rows are exactly 0)
+    int m;                  // input row length (M); zero-padded to m_prime
+    int rows_per_block;     // R
+    int kmax;               // candidates kept per block
+    unsigned long long* cand;  // [frame][nblk][kmax] packed keys
+    int detect;             // 0 = map only
+};
+
+struct MergeArgs {
+    const unsigned long long* cand;
+    int nblk;
+    int kmax;
+    const int32_t* k_per_frame;  // null -> kmax
+    int m_prime;
+    int32_t* det_delay;
+    int32_t* det_doppler;
+    float* det_power;
+    int32_t* counts;
+    const double* inv_partial;
+    int ntiles;
+    const double* sigma2;
+    double log_pfa, power_factor, inv_count;
+    double* s2h_out;        // optional per-frame sigma_h^2
+    double* eta_out;        // optional per-frame threshold
+};
+
+// Packed detection key: larger key = larger power, ties -> smaller row-major index
+// (extract_peaks ordering, periodogram.cpp:98-102).  P >= 0 so the float bit pattern
+// orders like the value.
+__device__ __forceinline__ unsigned long long make_key(float p, uint32_t idx) {
+    return (static_cast<unsigned long long>(__float_as_uint(p)) << 32) | (0xFFFFFFFFu - idx);
+}
+
+}  // namespace ofdmr

@@ -1,0 +1,155 @@
+"""Regenerate the golden fixtures in tests/golden/ from the REFERENCE'S OWN SOURCES.
+
+Runs only where /root/reference exists (this container): it drives
+oracle/_ref/libofdmref.so (reference src/*.cpp + substitute FFT, built by
+`make -f oracle/Makefile ref`) on seeded inputs and stores inputs + outputs as small
+.npz files.  The GPU box never reads /root/reference; tests load these fixtures.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import ctypes as C
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+
+import oracle as O  # noqa: E402
+from paper_2209_03883_b200 import _native, gen  # noqa: E402
+from paper_2209_03883_b200.configs import RadarConfig  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+TWO_PI = 6.283185307179586476925286766559
+
+
+def p(a):
+    return a.ctypes.data
+
+
+def periodogram_fixtures(R):
+    rng = np.random.default_rng(2209)
+    cases = [(16, 8, 16, 8, 0), (64, 32, 128, 64, 1), (48, 20, 48, 40, 1), (37, 11, 74, 11, 0), (128, 64, 128, 64, 1)]
+    for i, (n, m, np_, mp, w) in enumerate(cases):
+        h = rng.normal(size=(n, m)) + 1j * rng.normal(size=(n, m))
+        h = np.ascontiguousarray(h)
+        out = np.empty((np_, mp))
+        assert R.ref_periodogram(p(h), n, m, w, np_, mp, p(out)) == 0
+        np.savez_compressed(OUT / f"periodogram_{i}.npz", kind="periodogram", h=h, window=w, n_prime=np_,
+                            m_prime=mp, p=out)
+
+
+def dft_ce_fixture(R):
+    rng = np.random.default_rng(3883)
+    n, m, L = 64, 24, 16
+    h = np.ascontiguousarray(rng.normal(size=(n, m)) + 1j * rng.normal(size=(n, m)))
+    out = np.empty_like(h)
+    assert R.ref_dft_ce(p(h), p(out), n, m, L) == 0
+    np.savez_compressed(OUT / "dft_ce_0.npz", kind="dft_ce", h=h, n_cp=L, out=out)
+
+
+def receive_fixtures(R):
+    # small grids through the reference receiver half of run_pipeline (pipeline.cpp:72-96)
+    cases = [
+        ("receive_ls_rect", RadarConfig("g0", 128, 32, 128, 32, 32, 4, 0, 0, 3, 4, 3, 3, 10.0, 10.0, range_hi=60.0)),
+        ("receive_dftce_hamming_pad", RadarConfig("g1", 128, 32, 256, 64, 16, 16, 1, 1, 4, 4, 2, 5, -5.0, 15.0,
+                                                  range_hi=60.0)),
+    ]
+    for name, cfg in cases:
+        fb = gen.frames(cfg, 0, cfg.frames, threads=1)
+        F, K = cfg.frames, cfg.max_targets
+        d = np.zeros((F, K), np.int64)
+        v = np.zeros((F, K), np.int64)
+        w = np.zeros((F, K))
+        cnt = np.zeros(F, np.int64)
+        s2h = np.zeros(F)
+        for f in range(F):
+            c = C.c_long()
+            s = C.c_double()
+            e = C.c_double()
+            dd = np.zeros(K, np.int64)
+            vv = np.zeros(K, np.int64)
+            ww = np.zeros(K)
+            rc = R.ref_receive_frame(cfg.n, cfg.m, cfg.n_prime, cfg.m_prime, cfg.estimator, cfg.n_cp, cfg.window,
+                                     cfg.pfa, p(fb.y[f]), p(fb.x[f]), float(fb.sigma2[f]), K, p(dd), p(vv), p(ww),
+                                     C.byref(c), C.byref(s), C.byref(e), None)
+            assert rc == 0
+            d[f], v[f], w[f], cnt[f], s2h[f] = dd, vv, ww, c.value, s.value
+        cfgv = np.array([cfg.n, cfg.m, cfg.n_prime, cfg.m_prime, cfg.estimator, cfg.n_cp, cfg.window], np.int64)
+        np.savez_compressed(OUT / f"{name}.npz", kind="receive", cfg=cfgv, pfa=cfg.pfa, k=K, y=fb.y, x=fb.x,
+                            sigma2=fb.sigma2, delay=d, doppler=v, power=w, count=cnt, s2h=s2h)
+
+
+def sft_fixture(R):
+    rng = np.random.default_rng(4455)
+    n, m, F = 64, 48, 4
+    hs, seeds, s2s = [], [], []
+    for f in range(F):
+        truth = []
+        uk, ul = set(), set()
+        while len(truth) < 5:
+            k, l = int(rng.integers(n)), int(rng.integers(m))
+            if k in uk or l in ul:
+                continue
+            uk.add(k)
+            ul.add(l)
+            truth.append((k, l, (0.5 + 1.5 * rng.random()) * np.exp(1j * TWO_PI * rng.random())))
+        a = np.arange(n)[:, None]
+        b = np.arange(m)[None, :]
+        h = sum(A * np.exp(1j * TWO_PI * (a * k / n + b * l / m)) for k, l, A in truth)
+        s2 = 0.01 * f
+        h = h + np.sqrt(s2 / 2) * (rng.normal(size=(n, m)) + 1j * rng.normal(size=(n, m)))
+        hs.append(np.ascontiguousarray(h))
+        seeds.append(1000 + f)
+        s2s.append(s2)
+    ME = 64
+    out = {k: [] for k in ("ek", "el", "ea_re", "ea_im", "n_entries", "residual", "converged", "iterations",
+                           "samples_used")}
+    for f in range(F):
+        ek = np.zeros(ME, np.int64)
+        el = np.zeros(ME, np.int64)
+        ar = np.zeros(ME)
+        ai = np.zeros(ME)
+        ne = C.c_int64()
+        res = C.c_double()
+        conv = C.c_int32()
+        its = C.c_int64()
+        su = C.c_int64()
+        rc = R.ref_sft_iterate(p(hs[f]), n, m, 8, 0.0, seeds[f], s2s[f], 1e-2, 8, 0.25, 0.35, ME, p(ek), p(el), p(ar),
+                               p(ai), C.byref(ne), C.byref(res), C.byref(conv), C.byref(its), C.byref(su))
+        assert rc == 0
+        for k, v in (("ek", ek), ("el", el), ("ea_re", ar), ("ea_im", ai), ("n_entries", ne.value),
+                     ("residual", res.value), ("converged", conv.value), ("iterations", its.value),
+                     ("samples_used", su.value)):
+            out[k].append(v)
+    np.savez_compressed(OUT / "sft_64x48.npz", kind="sft", h=np.stack(hs), seed=np.array(seeds, np.uint64),
+                        sigma2=np.array(s2s), i_max=8, **{k: np.array(v) for k, v in out.items()})
+
+
+def frame_fixture(R):
+    # generator pin: reference make_random_frame + apply_channel (validity-checked targets)
+    n, m, ncp = 128, 32, 32
+    df = 491.5e6 / 1024
+    ranges = np.array([10.0, 25.5, 33.3])
+    vels = np.array([3.0, -5.5, 7.25])
+    y = np.empty((n, m), np.complex128)
+    x = np.empty((n, m), np.complex128)
+    s2 = C.c_double()
+    rc = R.ref_make_frame_pair(n, m, df, 77e9, ncp, 16, p(ranges), p(vels), 3, 5.0, 4242, p(y), p(x), C.byref(s2))
+    assert rc == 0, rc
+    np.savez_compressed(OUT / "frame_gen_0.npz", kind="frame", n=n, m=m, n_cp=ncp, df=df, qam=16, ranges=ranges,
+                        vels=vels, snr_db=5.0, seed=4242, y=y, x=x, sigma2=s2.value)
+
+
+if __name__ == "__main__":
+    R = O.ref()
+    periodogram_fixtures(R)
+    dft_ce_fixture(R)
+    receive_fixtures(R)
+    sft_fixture(R)
+    frame_fixture(R)
+    for f in sorted(OUT.glob("*.npz")):
+        print(f.name, f.stat().st_size)

@@ -1,0 +1,224 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded c64 inputs.  Bars (BASELINE north_star / SURVEY.md §8d):
+  * detection bins + order bit-exact (fp32-unresolvable oracle near-ties counted apart),
+  * peak powers within 1e-4 relative, whole maps within 1e-4 of the frame maximum,
+  * FPS-SFT (k, l) sets bit-exact, amplitudes within 1e-4, iterations / convergence equal.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2209_03883_b200 import configs, gen
+from paper_2209_03883_b200.receiver import ConfigError, Receiver
+from tests.parity import classify, powers_close
+
+pytestmark = pytest.mark.gpu
+TWO_PI = 6.283185307179586476925286766559
+MAP_TOL = 1e-4
+
+
+def _rc(cfg):
+    return O.rx_config(cfg.n, cfg.m, cfg.n_prime, cfg.m_prime, cfg.estimator, cfg.n_cp, cfg.window, cfg.pfa)
+
+
+def _pipeline_parity(cfg, frames, first=0, check_map=False):
+    fb = gen.frames(cfg, first, frames)
+    kf = fb.n_targets if cfg.per_frame_k else None
+    with Receiver.from_config(cfg) as rx:
+        dets, pmap = rx.pipeline(fb.y, fb.x, fb.sigma2, k_per_frame=kf, want_map=True)
+        torch.cuda.synchronize()
+        pmap = pmap.cpu().numpy()
+        s2h = dets.sigma2_h.cpu().numpy()
+    rc = _rc(cfg)
+    stats = {"ok": 0, "tie": 0, "fail": 0}
+    for f in range(frames):
+        k = int(kf[f]) if kf is not None else cfg.max_targets
+        ref, ref_s2h, eta, ref_map = O.receive_frame(rc, fb.y[f], fb.x[f], float(fb.sigma2[f]), k, want_map=True)
+        assert abs(s2h[f] - ref_s2h) <= 1e-6 * ref_s2h
+        err = np.abs(pmap[f] - ref_map).max() / ref_map.max()
+        assert err <= MAP_TOL, (cfg.name, f, err)
+        got = dets.frame(f)
+        verdict = classify(got, ref, ref_map, eta, k)
+        stats[verdict] += 1
+        assert verdict != "fail", (cfg.name, f, got, ref)
+        assert powers_close(got, ref), (got, ref)
+    assert stats["tie"] <= max(1, frames // 100), stats
+    return stats
+
+
+def test_spectral_division_and_zero_cell(cuda):
+    cfg = configs.CFG0
+    fb = gen.frames(cfg, 0, 2)
+    with Receiver.from_config(cfg) as rx:
+        h = rx.spectral_division(fb.y, fb.x).cpu().numpy()
+        for f in range(2):
+            ref = O.spectral_division(fb.y[f], fb.x[f])
+            assert np.abs(h[f] - ref).max() <= 1e-6 * np.abs(ref).max()
+        x = fb.x.copy()
+        x[1, 5, 7] = 0
+        with pytest.raises(ConfigError):
+            rx.spectral_division(fb.y, x)
+
+
+@pytest.mark.parametrize("n,m,L", [(1024, 256, 128), (2048, 512, 256), (64, 16, 16), (256, 64, 0), (128, 32, 128)])
+def test_dft_ce_matches_oracle(cuda, n, m, L):
+    rng = np.random.default_rng(n + L)
+    h = (rng.normal(size=(3, n, m)) + 1j * rng.normal(size=(3, n, m))).astype(np.complex64)
+    with Receiver(n, m, estimator="dft-ce", n_cp=L) as rx:
+        out = rx.dft_ce(h).cpu().numpy()
+    for f in range(3):
+        ref = O.dft_ce(h[f].astype(np.complex128), L)
+        scale = max(np.abs(ref).max(), 1e-30)
+        assert np.abs(out[f] - ref).max() <= 1e-5 * scale if L else np.abs(out[f]).max() == 0
+
+
+@pytest.mark.parametrize("n,m,np_,mp,window", [
+    (1024, 256, 1024, 256, 0), (1024, 256, 1024, 256, 1), (64, 32, 128, 64, 1), (16, 16, 64, 16, 0),
+    (128, 64, 512, 128, 1), (2048, 512, 4096, 2048, 1), (1024, 1024, 1024, 1024, 0), (256, 4096, 256, 4096, 0),
+])
+def test_periodogram_matches_oracle(cuda, n, m, np_, mp, window):
+    F = 2
+    h = np.stack([gen.noise_grid(n, m, 1.0, 77 + f) for f in range(F)]).astype(np.complex64)
+    h[0] += 3.0 * np.exp(1j * TWO_PI * (-np.arange(n)[:, None] * 5 / n + np.arange(m)[None, :] * 3 / m))
+    with Receiver(n, m, np_, mp, window=window) as rx:
+        p = rx.periodogram(h).cpu().numpy()
+    for f in range(F):
+        ref = O.periodogram(h[f].astype(np.complex128), window, np_, mp)
+        assert np.abs(p[f] - ref).max() / ref.max() <= MAP_TOL
+
+
+def test_reference_unit_analogues(cuda):
+    # DC peak (test_periodogram.cpp:58-67), analytic target (:90-104), two targets (:152-178)
+    with Receiver(16, 16, 16, 16, window=0, max_targets=8) as rx:
+        p = rx.periodogram(np.ones((16, 16), np.complex64)).cpu().numpy()
+        r, c = np.unravel_index(np.argmax(p), p.shape)
+        assert r == 0 and c - 8 == 0
+    n, m = 64, 32
+    k = np.arange(n)[:, None]
+    l = np.arange(m)[None, :]
+    t1 = np.exp(1j * TWO_PI * (-k * 10 / n + l * 5 / m))
+    t2 = np.exp(1j * TWO_PI * (-k * 30 / n + l * (-8) / m))
+    with Receiver(n, m, window=0, max_targets=8) as rx:
+        p = rx.periodogram((t1 + 0.7 * t2).astype(np.complex64))
+        d = rx.extract_peaks(p, 1.0).frame(0)
+        assert [(a, b) for a, b, _ in d] == [(10, 5), (30, -8)]
+        p1 = rx.periodogram(np.exp(1j * TWO_PI * (-k * 21 / n + l * 9 / m)).astype(np.complex64)).cpu().numpy()
+        r, c = np.unravel_index(np.argmax(p1), p1.shape)
+        assert r == 21 and c - m // 2 == 9
+
+
+def test_detect_on_shared_map_is_exact(cuda):
+    # extract_peaks on the SAME fp32 map: GPU selection must equal the oracle's exactly
+    cfg = configs.CFG1
+    fb = gen.frames(cfg, 0, 4)
+    rc = _rc(cfg)
+    maps, etas, refs = [], [], []
+    for f in range(4):
+        _, s2h, eta, pm = O.receive_frame(rc, fb.y[f], fb.x[f], float(fb.sigma2[f]), 3, want_map=True)
+        pm32 = pm.astype(np.float32)
+        maps.append(pm32)
+        etas.append(eta)
+        refs.append(O.extract_peaks(pm32.astype(np.float64), eta, 16))
+    with Receiver.from_config(cfg.replace(max_targets=16)) as rx:
+        d = rx.extract_peaks(np.stack(maps), np.array(etas))
+        for f in range(4):
+            got = d.frame(f)
+            assert [(a, b) for a, b, _ in got] == [(a, b) for a, b, _ in refs[f]]
+            assert all(float(np.float32(w)) == pytest.approx(wr, rel=1e-7) for (_, _, w), (_, _, wr) in zip(got, refs[f]))
+
+
+def test_pipeline_cfg0(cuda):
+    _pipeline_parity(configs.CFG0, 1)
+
+
+def test_pipeline_cfg1(cuda):
+    _pipeline_parity(configs.CFG1, 16)
+
+
+def test_pipeline_cfg1_rect_shortcut(cuda):
+    # rectangular window + N' = N takes the exact DFT-CE collapse (G has only L rows)
+    _pipeline_parity(configs.CFG1.replace(window=0), 8)
+
+
+def test_pipeline_cfg4_subset(cuda):
+    _pipeline_parity(configs.CFG4, 64, first=1000)
+
+
+def test_pipeline_cfg2_zc_precoded(cuda):
+    _pipeline_parity(configs.CFG2, 2)
+
+
+def test_pipeline_host_equals_device_and_deterministic(cuda):
+    cfg = configs.CFG4
+    fb = gen.frames(cfg, 0, 40)
+    with Receiver.from_config(cfg, chunk_frames=16) as rx:
+        d1, _ = rx.pipeline(fb.y, fb.x, fb.sigma2, k_per_frame=fb.n_targets)
+        d2, _ = rx.pipeline(fb.y, fb.x, fb.sigma2, k_per_frame=fb.n_targets)
+        hd, hv, hp, hc = rx.pipeline_host(fb.y, fb.x, fb.sigma2, fb.n_targets)
+    for a, b in ((d1.delay_bin, d2.delay_bin), (d1.doppler_bin, d2.doppler_bin), (d1.peak_power, d2.peak_power)):
+        assert torch.equal(a, b)
+    assert (d1.delay_bin.cpu().numpy() == hd).all() and (d1.doppler_bin.cpu().numpy() == hv).all()
+    assert (d1.peak_power.cpu().numpy() == hp).all() and (d1.counts.cpu().numpy() == hc).all()
+
+
+def test_pipeline_zero_cell_raises(cuda):
+    cfg = configs.CFG0
+    fb = gen.frames(cfg, 0, 1)
+    x = fb.x.copy()
+    x[0, 100, 3] = 0
+    with Receiver.from_config(cfg) as rx:
+        with pytest.raises(ConfigError):
+            rx.pipeline(fb.y, x, fb.sigma2)
+        with pytest.raises(ConfigError):
+            rx.pipeline_host(fb.y, x, fb.sigma2)
+
+
+def test_sft_cfg3_subset_matches_oracle(cuda):
+    c3 = configs.CFG3
+    F = 8
+    h, s2, tk, tl = gen.sparse_frames(c3.n, c3.m, c3.targets, c3.snr_db, c3.base_seed, 0, F)
+    seeds = np.array([gen.derive_seed(c3.base_seed + f, 0x736674) for f in range(F)], np.uint64)
+    with Receiver(16, 16) as rx:
+        out = rx.sft(h, seeds, s2, i_max=c3.i_max, pfa=c3.pfa, decimation=c3.decimation)
+        torch.cuda.synchronize()
+    k = out["k"].cpu().numpy()
+    l = out["l"].cpu().numpy()
+    amp = out["amp"].cpu().numpy()
+    ne = out["n_entries"].cpu().numpy()
+    for f in range(F):
+        ref = O.sft_iterate(h[f].astype(np.complex128), int(seeds[f]), float(s2[f]), i_max=c3.i_max,
+                            pfa=c3.pfa, decimation=c3.decimation)
+        assert int(ne[f]) == ref["n_entries"]
+        got = [(int(k[f, i]), int(l[f, i])) for i in range(int(ne[f]))]
+        assert got == [(a, b) for a, b, _ in ref["entries"]]
+        ga = amp[f, : int(ne[f]), 0] + 1j * amp[f, : int(ne[f]), 1]
+        ra = np.array([a for _, _, a in ref["entries"]])
+        assert np.abs(ga - ra).max(initial=0) <= 1e-4 * np.abs(ra).max(initial=1)
+        assert int(out["iterations"][f]) == ref["iterations"]
+        assert int(out["samples_used"][f]) == ref["samples_used"]
+        assert bool(out["converged"][f]) == ref["converged"]
+
+
+def test_sft_small_grids_match_oracle(cuda):
+    rng = np.random.default_rng(5)
+    F, n, m = 16, 64, 32
+    hs = []
+    for f in range(F):
+        a = np.arange(n)[:, None]
+        b = np.arange(m)[None, :]
+        h = sum((0.5 + rng.random()) * np.exp(1j * TWO_PI * (a * rng.integers(n) / n + b * rng.integers(m) / m + rng.random()))
+                for _ in range(4))
+        h = h + 0.05 * (rng.normal(size=(n, m)) + 1j * rng.normal(size=(n, m)))
+        hs.append(h)
+    h = np.stack(hs).astype(np.complex64)
+    seeds = np.arange(F, dtype=np.uint64) + 11
+    s2 = np.full(F, 0.005)
+    with Receiver(16, 16) as rx:
+        out = rx.sft(h, seeds, s2, i_max=10)
+    for f in range(F):
+        ref = O.sft_iterate(h[f].astype(np.complex128), int(seeds[f]), 0.005, i_max=10)
+        ne = int(out["n_entries"][f])
+        assert ne == ref["n_entries"]
+        got = [(int(out["k"][f, i]), int(out["l"][f, i])) for i in range(ne)]
+        assert got == [(a, b) for a, b, _ in ref["entries"]]
