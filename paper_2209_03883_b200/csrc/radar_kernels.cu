@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kNT) rowpass_kernel(RowArgs a) {
     constexpr int VS = pad_len(MP);
     const int R = a.rows_per_block;
     float2* cbuf = reinterpret_cast<float2*>(smem_raw);                   // RB x VS complex
-    float* ptile = reinterpret_cast<float*>(cbuf + RB * VS);              // (R + 2) x MP
+    float* ptile = reinterpret_cast<float*>(cbuf + ((RB * VS + 1) & ~1));  // (R + 2) x MP, 16-B aligned
     unsigned long long* list = reinterpret_cast<unsigned long long*>(ptile + (size_t)(R + 2) * MP);
     __shared__ int s_cnt;
     __shared__ unsigned long long s_best[kNT / 32];
@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(kNT) rowpass_kernel(RowArgs a) {
             }
             __syncthreads();
         }
+        __syncthreads();  // the last chunk may have been a zero-fill without a barrier
     }
 
     // ---- 2. map store (interior rows)
@@ -341,11 +342,16 @@ __global__ void __launch_bounds__(kNT) merge_kernel(MergeArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
         int n = 0;
-        for (int i = 0; i < kf; ++i) {
-            const unsigned long long key = s_top[i];
-            if (key == 0) break;
-            const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
+        for (int i = 0; i < a.kmax; ++i) {
+            const unsigned long long key = i < kf ? s_top[i] : 0ull;
             const size_t o = (size_t)f * a.kmax + i;
+            if (key == 0) {  // unused slots are cleared so outputs are fully defined
+                a.det_delay[o] = 0;
+                a.det_doppler[o] = 0;
+                a.det_power[o] = 0.f;
+                continue;
+            }
+            const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
             a.det_delay[o] = (int32_t)(idx / a.m_prime);
             a.det_doppler[o] = (int32_t)(idx % a.m_prime) - a.m_prime / 2;
             a.det_power[o] = __uint_as_float((uint32_t)(key >> 32));
@@ -417,7 +423,7 @@ size_t rowpass_smem(int mp, int rows) {
     const int rb = mp >= 4096 ? 1 : mp >= 2048 ? 2 : mp >= 1024 ? 4 : 8;
     // strict 3x3 maxima are never 8-adjacent: at most ceil(R/2) * (M'/2) per block
     const size_t cap = (size_t)((rows + 1) / 2) * (size_t)(mp / 2) + 16;
-    return (size_t)rb * pad_len(mp) * sizeof(float2) + (size_t)(rows + 2) * mp * sizeof(float) +
+    return (size_t)((rb * pad_len(mp) + 1) & ~1) * sizeof(float2) + (size_t)(rows + 2) * mp * sizeof(float) +
            cap * sizeof(unsigned long long);
 }
 
