@@ -45,6 +45,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "ofdmr_b200.h"]
     units = {
         "radar_kernels": [],
+        "fast_kernels": [],
         "capi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions
         "sft_kernels": ["-fmad=false"],

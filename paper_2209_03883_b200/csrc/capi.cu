@@ -18,6 +18,20 @@ cudaError_t launch_merge(const MergeArgs& a, int frames, cudaStream_t st);
 int colpass_tile_cols(int np);
 int rowpass_rows(int mp, int np);
 size_t rowpass_smem(int mp, int rows);
+struct FastRowArgs {
+    RowArgs r;
+    const float2* tw256_t;
+    int* frame_done;
+    const int32_t* k_per_frame;
+    int32_t* det_delay;
+    int32_t* det_doppler;
+    float* det_power;
+    int32_t* counts;
+    double* s2h_out;
+};
+cudaError_t launch_colpass_fast(const ColArgs& a, bool ls, bool win, const float2* tw_t, int frames, cudaStream_t st);
+cudaError_t launch_rowpass_fast(const FastRowArgs& a, int frames, cudaStream_t st);
+int fast_rows_per_block();
 }  // namespace ofdmr
 
 using namespace ofdmr;
@@ -54,9 +68,26 @@ struct ofdmr_context {
     float2* tw = nullptr;        // 4096-entry e^{-j2pi t/4096}
     float* wk = nullptr;         // Hamming windows (fp32) or null for rectangular
     float* wl = nullptr;
-    float2* gbuf = nullptr;      // k-pass intermediate for one chunk
-    double* partial = nullptr;   // per (frame, tile) 1/|x|^2 partials for one chunk
-    unsigned long long* cand = nullptr;  // per (frame, block) top-K keys for one chunk
+    // two scheduling slots (slot 0 = the caller's stream, slot 1 = an internal stream);
+    // consecutive chunks alternate so one chunk's row pass overlaps the next chunk's
+    // column pass; each slot owns its L2-resident intermediate and scratch.
+    struct Slot {
+        cudaStream_t stream = nullptr;
+        float2* gbuf = nullptr;      // k-pass intermediate for one chunk
+        double* partial = nullptr;   // per (frame, tile) 1/|x|^2 partials
+        unsigned long long* cand = nullptr;  // per (frame, block) top-K keys
+        int* frame_done = nullptr;   // fast path: per-frame finished-block counters
+        int32_t* status_scratch = nullptr;
+    } slot[2];
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool fast = false;           // N = N' = 1024, M = M' = 256 specialised kernels
+    float2* tw1024_t = nullptr;  // [t1*32 + j] = W_1024^{j t1}
+    float2* tw256_t = nullptr;   // [t1*16 + j] = W_256^{j t1}
+    // slot-0 aliases used by the single-stream entry points
+    float2* gbuf = nullptr;
+    double* partial = nullptr;
+    unsigned long long* cand = nullptr;
     int32_t* status_scratch = nullptr;
     int64_t chunk = 0;
     int ntiles = 0;              // M / C of the colpass
@@ -106,17 +137,19 @@ cudaEvent_t pool_event(ofdmr_context* c) {
 struct StageTimer {
     ofdmr_context* c;
     int stage;
+    cudaStream_t s;
     cudaEvent_t a = nullptr;
-    StageTimer(ofdmr_context* ctx, int st) : c(ctx), stage(st) {
+    StageTimer(ofdmr_context* ctx, int st, cudaStream_t stream) : c(ctx), stage(st), s(stream) {
         if (c->profiling) {
             a = pool_event(c);
-            cudaEventRecord(a, c->stream);
+            cudaEventRecord(a, s);
         }
     }
+    StageTimer(ofdmr_context* ctx, int st) : StageTimer(ctx, st, ctx->stream) {}
     ~StageTimer() {
         if (c->profiling) {
             cudaEvent_t b = pool_event(c);
-            cudaEventRecord(b, c->stream);
+            cudaEventRecord(b, s);
             c->prof.push_back({stage, {a, b}});
         }
     }
@@ -170,39 +203,100 @@ ColArgs base_col(ofdmr_context* c) {
     return a;
 }
 
-int launch_col(ofdmr_context* c, const ColArgs& a, int np, int64_t frames) {
-    StageTimer t(c, 0);
-    const cudaError_t e = launch_colpass(a, c->cfg.n_subcarriers, np, int(frames), c->stream);
+int launch_col(ofdmr_context* c, const ColArgs& a, int np, int64_t frames, cudaStream_t st) {
+    StageTimer t(c, 0, st);
+    const cudaError_t e = launch_colpass(a, c->cfg.n_subcarriers, np, int(frames), st);
     if (e != cudaSuccess) return cuda_fail(e, "colpass");
     ++c->launches;
     return OFDMR_OK;
 }
 
-// k-pass -> row-pass (+detect) -> merge over one chunk of frames.
-int run_pipeline_chunk(ofdmr_context* c, const float2* y, const float2* x, const double* sigma2,
-                       const int32_t* kpf, int32_t* d, int32_t* dp, float* pw, int32_t* cnt, double* s2h_out,
-                       float* p_out, int32_t* status, int64_t nf) {
+int run_pipeline_chunk_fast(ofdmr_context* c, int si, const float2* y, const float2* x, const double* sigma2,
+                            const int32_t* kpf, int32_t* d, int32_t* dp, float* pw, int32_t* cnt, double* s2h_out,
+                            float* p_out, int32_t* status, int64_t nf) {
     const ofdmr_config& g = c->cfg;
+    auto& s = c->slot[si];
     ColArgs a = base_col(c);
     a.y = y;
     a.x = x;
-    a.g_out = c->gbuf;
-    if (g.window == OFDMR_WINDOW_HAMMING) {
+    a.g_out = s.gbuf;
+    const bool win = g.window == OFDMR_WINDOW_HAMMING;
+    if (win) {
         a.wk = c->wk;
         a.wl = c->wl;
     }
-    a.inv_partial = c->partial;
+    a.inv_partial = s.partial;
     a.status = status;
     a.ce_taps = g.estimator == OFDMR_EST_DFT_CE ? g.n_cp : 0;
     a.shortcut = c->shortcut ? 1 : 0;
     a.g_rows = c->g_rows;
-    int rc = launch_col(c, a, g.n_prime, nf);
+    cudaError_t e;
+    {
+        StageTimer t(c, 0, s.stream);
+        e = launch_colpass_fast(a, true, win, c->tw1024_t, int(nf), s.stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "colpass_fast");
+    ++c->launches;
+    FastRowArgs r{};
+    r.r.g = s.gbuf;
+    r.r.p_out = p_out;
+    r.r.inv_partial = s.partial;
+    r.r.ntiles = c->ntiles;
+    r.r.sigma2 = sigma2;
+    r.r.log_pfa = c->log_pfa;
+    r.r.power_factor = c->pf;
+    r.r.inv_count = c->inv_count;
+    r.r.scale = c->scale;
+    r.r.n_prime = g.n_prime;
+    r.r.g_rows = c->g_rows;
+    r.r.m = g.n_symbols;
+    r.r.kmax = g.max_targets;
+    r.r.cand = s.cand;
+    r.r.detect = 1;
+    r.tw256_t = c->tw256_t;
+    r.frame_done = s.frame_done;
+    r.k_per_frame = kpf;
+    r.det_delay = d;
+    r.det_doppler = dp;
+    r.det_power = pw;
+    r.counts = cnt;
+    r.s2h_out = s2h_out;
+    {
+        StageTimer t(c, 1, s.stream);
+        e = launch_rowpass_fast(r, int(nf), s.stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "rowpass_fast");
+    ++c->launches;
+    return OFDMR_OK;
+}
+
+// k-pass -> row-pass (+detect) -> merge over one chunk of frames.
+int run_pipeline_chunk(ofdmr_context* c, int si, const float2* y, const float2* x, const double* sigma2,
+                       const int32_t* kpf, int32_t* d, int32_t* dp, float* pw, int32_t* cnt, double* s2h_out,
+                       float* p_out, int32_t* status, int64_t nf) {
+    if (c->fast) return run_pipeline_chunk_fast(c, si, y, x, sigma2, kpf, d, dp, pw, cnt, s2h_out, p_out, status, nf);
+    const ofdmr_config& g = c->cfg;
+    auto& s = c->slot[si];
+    ColArgs a = base_col(c);
+    a.y = y;
+    a.x = x;
+    a.g_out = s.gbuf;
+    if (g.window == OFDMR_WINDOW_HAMMING) {
+        a.wk = c->wk;
+        a.wl = c->wl;
+    }
+    a.inv_partial = s.partial;
+    a.status = status;
+    a.ce_taps = g.estimator == OFDMR_EST_DFT_CE ? g.n_cp : 0;
+    a.shortcut = c->shortcut ? 1 : 0;
+    a.g_rows = c->g_rows;
+    int rc = launch_col(c, a, g.n_prime, nf, s.stream);
     if (rc) return rc;
 
     RowArgs r{};
-    r.g = c->gbuf;
+    r.g = s.gbuf;
     r.p_out = p_out;
-    r.inv_partial = c->partial;
+    r.inv_partial = s.partial;
     r.ntiles = c->ntiles;
     r.sigma2 = sigma2;
     r.log_pfa = c->log_pfa;
@@ -215,18 +309,18 @@ int run_pipeline_chunk(ofdmr_context* c, const float2* y, const float2* x, const
     r.m = g.n_symbols;
     r.rows_per_block = c->rows_per_block;
     r.kmax = g.max_targets;
-    r.cand = c->cand;
+    r.cand = s.cand;
     r.detect = 1;
     cudaError_t e;
     {
-        StageTimer t(c, 1);
-        e = launch_rowpass(r, g.m_prime, int(nf), c->stream);
+        StageTimer t(c, 1, s.stream);
+        e = launch_rowpass(r, g.m_prime, int(nf), s.stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "rowpass");
     ++c->launches;
 
     MergeArgs mg{};
-    mg.cand = c->cand;
+    mg.cand = s.cand;
     mg.nblk = c->nblk;
     mg.kmax = g.max_targets;
     mg.k_per_frame = kpf;
@@ -235,7 +329,7 @@ int run_pipeline_chunk(ofdmr_context* c, const float2* y, const float2* x, const
     mg.det_doppler = dp;
     mg.det_power = pw;
     mg.counts = cnt;
-    mg.inv_partial = c->partial;
+    mg.inv_partial = s.partial;
     mg.ntiles = c->ntiles;
     mg.sigma2 = sigma2;
     mg.log_pfa = c->log_pfa;
@@ -243,8 +337,8 @@ int run_pipeline_chunk(ofdmr_context* c, const float2* y, const float2* x, const
     mg.inv_count = c->inv_count;
     mg.s2h_out = s2h_out;
     {
-        StageTimer t(c, 2);
-        e = launch_merge(mg, int(nf), c->stream);
+        StageTimer t(c, 2, s.stream);
+        e = launch_merge(mg, int(nf), s.stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "merge");
     ++c->launches;
@@ -305,10 +399,16 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
     c->pf = power_factor_d(cfg->window, n, m);
     c->inv_count = 1.0 / double(size_t(n) * size_t(m));
     c->scale = float(1.0 / (double(n) * double(m)));
+    c->fast = n == 1024 && np == 1024 && m == 256 && mp == 256;
+    if (c->fast) {
+        c->rows_per_block = fast_rows_per_block();
+        c->nblk = (np + c->rows_per_block - 1) / c->rows_per_block;
+    }
     const size_t gframe = size_t(c->g_rows) * size_t(m) * sizeof(float2);
     int64_t chunk = cfg->chunk_frames;
     if (chunk <= 0) {
-        chunk = int64_t((48ull << 20) / gframe);  // keep the intermediate L2-resident
+        // two chunks in flight; keep both intermediates L2-resident (126 MB L2)
+        chunk = int64_t((32ull << 20) / gframe);
         if (chunk < 1) chunk = 1;
         if (chunk > 256) chunk = 256;
     }
@@ -330,11 +430,42 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         if (e == cudaSuccess) e = cudaMemcpy(c->wk, fk.data(), sizeof(float) * n, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->wl, fl.data(), sizeof(float) * m, cudaMemcpyHostToDevice);
     }
-    if (e == cudaSuccess) e = cudaMalloc(&c->gbuf, gframe * size_t(chunk));
-    if (e == cudaSuccess) e = cudaMalloc(&c->partial, sizeof(double) * size_t(c->ntiles) * size_t(chunk));
-    if (e == cudaSuccess)
-        e = cudaMalloc(&c->cand, sizeof(unsigned long long) * size_t(c->nblk) * cfg->max_targets * size_t(chunk));
-    if (e == cudaSuccess) e = cudaMalloc(&c->status_scratch, sizeof(int32_t) * size_t(chunk));
+    // the periodogram entry point always needs the full N' rows
+    const size_t gbytes = std::max(gframe, size_t(np) * size_t(m) * sizeof(float2)) * size_t(chunk);
+    for (int si = 0; si < 2 && e == cudaSuccess; ++si) {
+        auto& s = c->slot[si];
+        e = cudaMalloc(&s.gbuf, gbytes);
+        if (e == cudaSuccess) e = cudaMalloc(&s.partial, sizeof(double) * size_t(c->ntiles) * size_t(chunk));
+        if (e == cudaSuccess)
+            e = cudaMalloc(&s.cand, sizeof(unsigned long long) * size_t(c->nblk) * cfg->max_targets * size_t(chunk));
+        if (e == cudaSuccess) e = cudaMalloc(&s.frame_done, sizeof(int) * size_t(chunk));
+        if (e == cudaSuccess) e = cudaMemset(s.frame_done, 0, sizeof(int) * size_t(chunk));
+        if (e == cudaSuccess) e = cudaMalloc(&s.status_scratch, sizeof(int32_t) * size_t(chunk));
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+    if (e == cudaSuccess && c->fast) {
+        std::vector<float2> t1024(1024), t256(256);
+        for (int t1 = 0; t1 < 32; ++t1)
+            for (int j = 0; j < 32; ++j) {
+                const double a = -kTwoPi * double(t1 * j) / 1024.0;
+                t1024[t1 * 32 + j] = make_float2(float(std::cos(a)), float(std::sin(a)));
+            }
+        for (int t1 = 0; t1 < 16; ++t1)
+            for (int j = 0; j < 16; ++j) {
+                const double a = -kTwoPi * double(t1 * j) / 256.0;
+                t256[t1 * 16 + j] = make_float2(float(std::cos(a)), float(std::sin(a)));
+            }
+        e = cudaMalloc(&c->tw1024_t, sizeof(float2) * 1024);
+        if (e == cudaSuccess) e = cudaMalloc(&c->tw256_t, sizeof(float2) * 256);
+        if (e == cudaSuccess) e = cudaMemcpy(c->tw1024_t, t1024.data(), sizeof(float2) * 1024, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(c->tw256_t, t256.data(), sizeof(float2) * 256, cudaMemcpyHostToDevice);
+    }
+    c->gbuf = c->slot[0].gbuf;
+    c->partial = c->slot[0].partial;
+    c->cand = c->slot[0].cand;
+    c->status_scratch = c->slot[0].status_scratch;
     if (e != cudaSuccess) {
         ofdmr_destroy(c);
         return cuda_fail(e, "ofdmr_create: allocation");
@@ -349,10 +480,18 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->tw);
     cudaFree(c->wk);
     cudaFree(c->wl);
-    cudaFree(c->gbuf);
-    cudaFree(c->partial);
-    cudaFree(c->cand);
-    cudaFree(c->status_scratch);
+    for (auto& s : c->slot) {
+        cudaFree(s.gbuf);
+        cudaFree(s.partial);
+        cudaFree(s.cand);
+        cudaFree(s.frame_done);
+        cudaFree(s.status_scratch);
+    }
+    cudaFree(c->tw1024_t);
+    cudaFree(c->tw256_t);
+    if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (int i = 0; i < 2; ++i) {
         cudaFree(c->dev_y[i]);
         cudaFree(c->dev_x[i]);
@@ -425,7 +564,7 @@ int ofdmr_spectral_division(ofdmr_context* c, const void* y, const void* x, void
         a.x = static_cast<const float2*>(x) + fc * f0;
         a.h_out = static_cast<float2*>(h) + fc * f0;
         a.status = status + f0;
-        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf);
+        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf, c->stream);
         if (rc) return rc;
     }
     return OFDMR_OK;
@@ -448,7 +587,7 @@ int ofdmr_dft_ce(ofdmr_context* c, const void* h, void* h_out, int64_t frames) {
             OFDMR_CUDA(cudaMemsetAsync(a.h_out, 0, sizeof(float2) * fc * size_t(nf), c->stream));
             continue;
         }
-        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf);
+        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf, c->stream);
         if (rc) return rc;
     }
     return OFDMR_OK;
@@ -475,7 +614,7 @@ int ofdmr_estimate_channel(ofdmr_context* c, const void* y, const void* x, void*
         a.hout_after_ce = 1;
         a.ce_taps = c->cfg.n_cp;
         a.status = status + f0;
-        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf);
+        int rc = launch_col(c, a, c->cfg.n_subcarriers, nf, c->stream);
         if (rc) return rc;
     }
     return OFDMR_OK;
@@ -490,36 +629,78 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
     const size_t pframe = size_t(g.n_prime) * size_t(g.m_prime);
     // the general (non-shortcut) G layout is always N' rows; the chunk buffer holds g_rows rows
     const int64_t chunk = c->shortcut ? std::max<int64_t>(1, c->chunk * c->g_rows / g.n_prime) : c->chunk;
-    for (int64_t f0 = 0; f0 < frames; f0 += chunk) {
-        const int64_t nf = std::min<int64_t>(chunk, frames - f0);
+    (void)chunk;
+    const int64_t pchunk = c->chunk;  // slot buffers hold chunk x N' rows
+    const bool two = !c->profiling;
+    if (two) {
+        OFDMR_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+        OFDMR_CUDA(cudaStreamWaitEvent(c->aux_stream, c->ev_fork, 0));
+    }
+    c->slot[0].stream = c->stream;
+    c->slot[1].stream = c->aux_stream;
+    int64_t ci = 0;
+    for (int64_t f0 = 0; f0 < frames; f0 += pchunk, ++ci) {
+        const int64_t nf = std::min<int64_t>(pchunk, frames - f0);
+        auto& s = c->slot[two ? (ci & 1) : 0];
         ColArgs a = base_col(c);
         a.h = static_cast<const float2*>(h) + fc * f0;
-        a.g_out = c->gbuf;
+        a.g_out = s.gbuf;
         a.g_rows = g.n_prime;
-        if (g.window == OFDMR_WINDOW_HAMMING) {
+        const bool win = g.window == OFDMR_WINDOW_HAMMING;
+        if (win) {
             a.wk = c->wk;
             a.wl = c->wl;
         }
-        int rc = launch_col(c, a, g.n_prime, nf);
+        if (c->fast) {
+            cudaError_t e;
+            {
+                StageTimer t(c, 0, s.stream);
+                e = launch_colpass_fast(a, false, win, c->tw1024_t, int(nf), s.stream);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "colpass_fast");
+            ++c->launches;
+            FastRowArgs r{};
+            r.r.g = s.gbuf;
+            r.r.p_out = p + pframe * f0;
+            r.r.scale = c->scale;
+            r.r.n_prime = g.n_prime;
+            r.r.g_rows = g.n_prime;
+            r.r.m = g.n_symbols;
+            r.r.kmax = g.max_targets;
+            r.r.detect = 0;
+            r.tw256_t = c->tw256_t;
+            {
+                StageTimer t(c, 1, s.stream);
+                e = launch_rowpass_fast(r, int(nf), s.stream);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "rowpass_fast");
+            ++c->launches;
+            continue;
+        }
+        int rc = launch_col(c, a, g.n_prime, nf, s.stream);
         if (rc) return rc;
         RowArgs r{};
-        r.g = c->gbuf;
+        r.g = s.gbuf;
         r.p_out = p + pframe * f0;
         r.scale = c->scale;
         r.tw = c->tw;
         r.n_prime = g.n_prime;
         r.g_rows = g.n_prime;
         r.m = g.n_symbols;
-        r.rows_per_block = c->rows_per_block;
+        r.rows_per_block = rowpass_rows(g.m_prime, g.n_prime);
         r.kmax = g.max_targets;
         r.detect = 0;
         cudaError_t e;
         {
-            StageTimer t(c, 1);
-            e = launch_rowpass(r, g.m_prime, int(nf), c->stream);
+            StageTimer t(c, 1, s.stream);
+            e = launch_rowpass(r, g.m_prime, int(nf), s.stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "rowpass");
         ++c->launches;
+    }
+    if (two) {
+        OFDMR_CUDA(cudaEventRecord(c->ev_join, c->aux_stream));
+        OFDMR_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     }
     return OFDMR_OK;
 }
@@ -592,15 +773,28 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
     const size_t pframe = size_t(g.n_prime) * size_t(g.m_prime);
     const int K = g.max_targets;
     if (status) OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
-    for (int64_t f0 = 0; f0 < frames; f0 += c->chunk) {
+    const bool two = !c->profiling && frames > c->chunk;
+    if (two) {
+        OFDMR_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+        OFDMR_CUDA(cudaStreamWaitEvent(c->aux_stream, c->ev_fork, 0));
+    }
+    c->slot[0].stream = c->stream;
+    c->slot[1].stream = c->aux_stream;
+    int64_t ci = 0;
+    for (int64_t f0 = 0; f0 < frames; f0 += c->chunk, ++ci) {
         const int64_t nf = std::min<int64_t>(c->chunk, frames - f0);
-        int32_t* st = status ? status + f0 : c->status_scratch;
-        if (!status) OFDMR_CUDA(cudaMemsetAsync(st, 0, sizeof(int32_t) * size_t(nf), c->stream));
+        const int si = two ? int(ci & 1) : 0;
+        int32_t* st = status ? status + f0 : c->slot[si].status_scratch;
+        if (!status) OFDMR_CUDA(cudaMemsetAsync(st, 0, sizeof(int32_t) * size_t(nf), c->slot[si].stream));
         const int rc = run_pipeline_chunk(
-            c, static_cast<const float2*>(y) + fc * f0, static_cast<const float2*>(x) + fc * f0, sigma2 + f0,
+            c, si, static_cast<const float2*>(y) + fc * f0, static_cast<const float2*>(x) + fc * f0, sigma2 + f0,
             kpf ? kpf + f0 : nullptr, d + size_t(K) * f0, dp + size_t(K) * f0, pw + size_t(K) * f0, cnt + f0,
             s2h_out ? s2h_out + f0 : nullptr, p_out ? p_out + pframe * f0 : nullptr, st, nf);
         if (rc) return rc;
+    }
+    if (two) {
+        OFDMR_CUDA(cudaEventRecord(c->ev_join, c->aux_stream));
+        OFDMR_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     }
     return OFDMR_OK;
 }

@@ -1,0 +1,379 @@
+// Fast path for the hot shapes N = N' = 1024, M = M' = 256 (cfg0 / cfg1 / cfg4 and the
+// batched 2-D periodogram).  Same math and outputs as the generic kernels in
+// radar_kernels.cu; see DESIGN.md "Kernels" for the roofline analysis.
+//
+//   colpass1024_fast<MODE>: CTA = 8 adjacent columns (OFDM symbols) x 1024 subcarriers
+//     of one frame; one warp per column with the column in registers (warp_fft.cuh).
+//     LS divide + sum 1/|x|^2 (estimation.cpp:10-21, pipeline.cpp:18-23) on the tile
+//     load; DFT-CE (estimation.cpp:23-39) as IFFT -> truncate -> input-pruned FFT; the
+//     separable window (periodogram.cpp:52-56); the delay IFFT (periodogram.cpp:60).
+//     With a rectangular window and N' = N the DFT-CE + delay IFFT collapse exactly to
+//     the first L rows of IFFT_N(H) (MODE & kShortcut).
+//   rowpass256_fast: CTA = 30 rows of P (+1 halo row each side); half-warp FFT_256 per
+//     row (periodogram.cpp:57), |.|^2/(NM) + fftshift (:63-73), optional map store,
+//     strict wrapped 3x3 local maxima >= eta (:77-136), per-block top-K, and the per-frame
+//     top-K merge done by the last block of each frame (no separate merge launch).
+#include "radar_kernels.cuh"
+#include "warp_fft.cuh"
+
+namespace ofdmr {
+
+constexpr int kFastC = 8;            // columns per colpass CTA (one warp each)
+constexpr int kColVS = 1057;         // pad_len(1024)
+constexpr int kRowR = 30;            // P rows per rowpass CTA (+2 halo = 32 = 2 rounds of 16)
+constexpr int kListCap = 512;        // candidate list in smem; exact fallback scan beyond it
+
+enum : int { kLS = 1, kCE = 2, kPrune = 4, kWin = 8, kShortcut = 16 };
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) colpass1024_fast(ColArgs a, const float2* __restrict__ tw_t) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* tw = reinterpret_cast<float2*>(smem_raw);   // 1024: tw[t1*32 + j] = W^{j t1}
+    float2* tile = tw + 1024;                            // 8 x kColVS
+    __shared__ double red[8];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int f = blockIdx.y, tile_idx = blockIdx.x, c0 = tile_idx * kFastC;
+    const int m = a.m;
+    const size_t fbase = (size_t)f * 1024 * m;
+
+    for (int i = tid; i < 1024; i += 256) tw[i] = tw_t[i];
+
+    double inv_acc = 0.0;
+    int zero_cell = 0;
+#pragma unroll 4
+    for (int idx = tid; idx < 1024 * (kFastC / 2); idx += 256) {
+        const int k = idx >> 2;
+        const int c = (idx & 3) * 2;
+        const size_t off = fbase + (size_t)k * m + c0 + c;
+        float2 h0, h1;
+        if constexpr (MODE & kLS) {
+            const float4 yv = __ldcs(reinterpret_cast<const float4*>(a.y + off));
+            const float4 xv = __ldcs(reinterpret_cast<const float4*>(a.x + off));
+            const float n0 = fmaf(xv.x, xv.x, xv.y * xv.y);
+            const float n1 = fmaf(xv.z, xv.z, xv.w * xv.w);
+            float i0 = 0.f, i1 = 0.f;
+            if (n0 == 0.f) zero_cell = 1; else i0 = 1.0f / n0;
+            if (n1 == 0.f) zero_cell = 1; else i1 = 1.0f / n1;
+            inv_acc += (double)i0 + (double)i1;
+            h0 = make_float2(fmaf(yv.x, xv.x, yv.y * xv.y) * i0, fmaf(yv.y, xv.x, -yv.x * xv.y) * i0);
+            h1 = make_float2(fmaf(yv.z, xv.z, yv.w * xv.w) * i1, fmaf(yv.w, xv.z, -yv.z * xv.w) * i1);
+        } else {
+            const float4 hv = __ldcs(reinterpret_cast<const float4*>(a.h + off));
+            h0 = make_float2(hv.x, hv.y);
+            h1 = make_float2(hv.z, hv.w);
+        }
+        const int p = k + (k >> 5);
+        tile[c * kColVS + p] = h0;
+        tile[(c + 1) * kColVS + p] = h1;
+    }
+    if constexpr (MODE & kLS) {
+        if (zero_cell) atomicOr(a.status + f, 1);
+        if (a.inv_partial != nullptr) {
+            double v = inv_acc;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[w] = v;
+        }
+    }
+    __syncthreads();
+    if constexpr (MODE & kLS) {
+        if (a.inv_partial != nullptr && tid == 0) {
+            double s = 0.0;
+            for (int i = 0; i < 8; ++i) s += red[i];
+            a.inv_partial[(size_t)f * a.ntiles + tile_idx] = s;
+        }
+    }
+
+    // ---- per-warp column chain, registers only between transforms
+    float2* col = tile + w * kColVS;
+    float2 v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = col[lane + 33 * i];
+    const float wl = (MODE & kWin) ? a.wl[c0 + w] : 1.0f;
+    int out_rows = 1024;
+    if constexpr (MODE & kCE) {
+        warp_fft1024<true, 32>(v, col, tw);  // IFFT_N: lane t1 holds taps t1 + 32 t2
+        const int L = a.ce_taps;
+        if constexpr (MODE & kShortcut) {
+#pragma unroll
+            for (int t2 = 0; t2 < 32; ++t2)
+                if (lane + 32 * t2 < L) col[lane + 33 * t2] = v[t2];
+            out_rows = L;
+        } else {
+            constexpr float inv_n = 1.0f / 1024.0f;
+#pragma unroll
+            for (int t2 = 0; t2 < 32; ++t2) v[t2] = (lane + 32 * t2 < L) ? cscale(v[t2], inv_n) : make_float2(0.f, 0.f);
+            if constexpr (MODE & kPrune) warp_fft1024<false, 4>(v, col, tw);   // L <= 128: taps in v[0..3]
+            else warp_fft1024<false, 32>(v, col, tw);
+            if constexpr (MODE & kWin) {
+#pragma unroll
+                for (int t2 = 0; t2 < 32; ++t2) v[t2] = cscale(v[t2], __ldg(a.wk + lane + 32 * t2) * wl);
+            }
+            warp_fft1024<true, 32>(v, col, tw);  // delay IFFT_N'
+#pragma unroll
+            for (int t2 = 0; t2 < 32; ++t2) col[lane + 33 * t2] = v[t2];
+        }
+    } else {
+        if constexpr (MODE & kWin) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = cscale(v[i], __ldg(a.wk + lane + 32 * i) * wl);
+        }
+        warp_fft1024<true, 32>(v, col, tw);
+#pragma unroll
+        for (int t2 = 0; t2 < 32; ++t2) col[lane + 33 * t2] = v[t2];
+    }
+    __syncthreads();
+
+    // ---- coalesced row-segment store of G (out_rows x 8 columns); G stays in L2
+    float2* g = a.g_out + (size_t)f * a.g_rows * m;
+#pragma unroll 4
+    for (int idx = tid; idx < out_rows * (kFastC / 2); idx += 256) {
+        const int k = idx >> 2;
+        const int c = (idx & 3) * 2;
+        const int p = k + (k >> 5);
+        const float2 v0 = tile[c * kColVS + p];
+        const float2 v1 = tile[(c + 1) * kColVS + p];
+        *reinterpret_cast<float4*>(g + (size_t)k * m + c0 + c) = make_float4(v0.x, v0.y, v1.x, v1.y);
+    }
+}
+
+struct FastRowArgs {
+    RowArgs r;
+    const float2* tw256_t;      // tw[t1*16 + j] = W_256^{j t1}
+    // fused merge (per frame, by the last row block to finish)
+    int* frame_done;            // per-frame block counters (zeroed; reset by the merging block)
+    const int32_t* k_per_frame;
+    int32_t* det_delay;
+    int32_t* det_doppler;
+    float* det_power;
+    int32_t* counts;
+    double* s2h_out;
+};
+
+// Strict wrapped 3x3 local max >= eta at tile row tr (1..nrows), column c; key or 0.
+__device__ __forceinline__ unsigned long long qualify256(const float* pt, int tr, int c, double eta, int r0) {
+    const float v = pt[tr * 256 + c];
+    if (!((double)v >= eta)) return 0ull;
+    const int cl = (c - 1) & 255, cr = (c + 1) & 255;
+    const float* up = pt + (tr - 1) * 256;
+    const float* mid = pt + tr * 256;
+    const float* dn = pt + (tr + 1) * 256;
+    if (up[cl] >= v || up[c] >= v || up[cr] >= v || mid[cl] >= v || mid[cr] >= v || dn[cl] >= v || dn[c] >= v ||
+        dn[cr] >= v)
+        return 0ull;
+    return make_key(v, (uint32_t)((r0 + tr - 1) * 256 + c));
+}
+
+constexpr size_t kRowSmem = sizeof(float) * (kRowR + 2) * 256 + sizeof(float2) * (256 + 16 * 16 * 17) +
+                            sizeof(unsigned long long) * kListCap;
+
+__global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
+    const RowArgs& a = e.r;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* ptile = reinterpret_cast<float*>(smem_raw);                       // (R + 2) x 256
+    float2* tw = reinterpret_cast<float2*>(ptile + (kRowR + 2) * 256);      // 256
+    float2* tbufs = tw + 256;                                                // 16 x (16 x 17)
+    unsigned long long* list = reinterpret_cast<unsigned long long*>(tbufs + 16 * 16 * 17);
+    __shared__ unsigned long long s_top[kMaxK];
+    __shared__ unsigned long long s_best[8];
+    __shared__ int s_idx[8];
+    __shared__ int s_cnt, s_last;
+
+    const int tid = threadIdx.x;
+    const int f = blockIdx.y, rb = blockIdx.x;
+    const int np = 1024, m = 256;
+    const int r0 = rb * kRowR;
+    const int nrows = min(kRowR, np - r0);
+    const int TR = nrows + 2;
+    const int hw = tid >> 4, j = tid & 15;
+
+    tw[tid] = e.tw256_t[tid];
+    __syncthreads();
+
+    const float2* gf = a.g + (size_t)f * a.g_rows * m;
+    for (int t0 = 0; t0 < TR; t0 += 16) {
+        const int tr = t0 + hw;
+        if (tr < TR) {
+            const int gr = (r0 - 1 + tr + np) & (np - 1);
+            float* prow = ptile + tr * 256;
+            if (gr < a.g_rows) {
+                float2 v[16];
+                const float2* src = gf + (size_t)gr * m;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = __ldcs(src + j + 16 * i);
+                halfwarp_fft256<false>(v, tbufs + hw * 16 * 17, tw);
+#pragma unroll
+                for (int t2 = 0; t2 < 16; ++t2) prow[(j + 16 * t2 + 128) & 255] = cnorm(v[t2]) * a.scale;
+            } else {
+#pragma unroll
+                for (int t2 = 0; t2 < 16; ++t2) prow[j + 16 * t2] = 0.f;
+            }
+        }
+    }
+    __syncthreads();
+
+    if (a.p_out != nullptr) {
+        float* po = a.p_out + (size_t)f * np * 256 + (size_t)r0 * 256;
+        for (int idx = tid; idx < nrows * 64; idx += 256) {
+            const int r = idx >> 6, q = idx & 63;
+            __stcs(reinterpret_cast<float4*>(po + (size_t)r * 256) + q,
+                   reinterpret_cast<const float4*>(ptile + (r + 1) * 256)[q]);
+        }
+    }
+    if (!a.detect) return;
+
+    double eta;
+    if (a.eta_in != nullptr) {
+        eta = a.eta_in[f];
+    } else {
+        double s2h = a.sigma2[f];
+        if (a.inv_partial != nullptr) {
+            if (s2h <= 0.0) {
+                s2h = 0.0;
+            } else {
+                double acc = 0.0;
+                for (int t = 0; t < a.ntiles; ++t) acc += a.inv_partial[(size_t)f * a.ntiles + t];
+                s2h = s2h * acc * a.inv_count;
+            }
+        }
+        eta = -s2h * a.log_pfa * a.power_factor;
+    }
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    for (int idx = tid; idx < nrows * 256; idx += 256) {
+        const unsigned long long key = qualify256(ptile, (idx >> 8) + 1, idx & 255, eta, r0);
+        if (key) {
+            const int slot = atomicAdd(&s_cnt, 1);
+            if (slot < kListCap) list[slot] = key;
+        }
+    }
+    __syncthreads();
+    const int cnt = s_cnt;
+    const int K = a.kmax;
+    if (cnt <= kListCap) {
+        block_topk_smem(list, cnt, K, s_top, s_best, s_idx);
+    } else {
+        // exact fallback: K rounds of "largest qualifying key below the previous one"
+        unsigned long long prev = ~0ull;
+        for (int round = 0; round < K; ++round) {
+            unsigned long long best = 0;
+            for (int idx = tid; idx < nrows * 256; idx += 256) {
+                const unsigned long long key = qualify256(ptile, (idx >> 8) + 1, idx & 255, eta, r0);
+                if (key < prev && key > best) best = key;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+                best = ob > best ? ob : best;
+            }
+            if ((tid & 31) == 0) s_best[tid >> 5] = best;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long b = 0;
+                for (int i = 0; i < 8; ++i) b = s_best[i] > b ? s_best[i] : b;
+                s_top[round] = b;
+            }
+            __syncthreads();
+            prev = s_top[round];
+            __syncthreads();
+            if (prev == 0) {
+                for (int r = round + 1 + tid; r < K; r += 256) s_top[r] = 0;
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    unsigned long long* out = a.cand + ((size_t)f * gridDim.x + rb) * K;
+    for (int i = tid; i < K; i += 256) out[i] = s_top[i];
+
+    // ---- last block of this frame merges all blocks' candidates
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const int prev = atomicAdd(e.frame_done + f, 1);
+        s_last = prev == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    unsigned long long* all = a.cand + (size_t)f * gridDim.x * K;
+    const int total = gridDim.x * K;
+    const int kf = e.k_per_frame ? min(e.k_per_frame[f], K) : K;
+    block_topk_global(all, total, kf, s_top, s_best, s_idx);
+    __syncthreads();
+    if (tid < K) {
+        const unsigned long long key = tid < kf ? s_top[tid] : 0ull;
+        const size_t o = (size_t)f * K + tid;
+        if (key == 0) {
+            e.det_delay[o] = 0;
+            e.det_doppler[o] = 0;
+            e.det_power[o] = 0.f;
+        } else {
+            const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
+            e.det_delay[o] = (int32_t)(idx >> 8);
+            e.det_doppler[o] = (int32_t)(idx & 255) - 128;
+            e.det_power[o] = __uint_as_float((uint32_t)(key >> 32));
+        }
+    }
+    if (tid == 0) {
+        int n = 0;
+        for (int i = 0; i < kf; ++i) n += s_top[i] != 0;
+        e.counts[f] = n;
+        e.frame_done[f] = 0;  // ready for the next launch
+        if (e.s2h_out != nullptr) {
+            double s2h = a.sigma2[f];
+            if (a.inv_partial != nullptr) {
+                if (s2h <= 0.0) {
+                    s2h = 0.0;
+                } else {
+                    double acc = 0.0;
+                    for (int t = 0; t < a.ntiles; ++t) acc += a.inv_partial[(size_t)f * a.ntiles + t];
+                    s2h = s2h * acc * a.inv_count;
+                }
+            }
+            e.s2h_out[f] = s2h;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ launch ------
+
+template <int MODE>
+cudaError_t launch_col_fast_t(const ColArgs& a, const float2* tw_t, int frames, cudaStream_t st) {
+    const size_t smem = (1024 + kFastC * kColVS) * sizeof(float2);
+    auto kern = colpass1024_fast<MODE>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid(a.m / kFastC, frames);
+    kern<<<grid, 256, smem, st>>>(a, tw_t);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_colpass_fast(const ColArgs& a, bool ls, bool win, const float2* tw_t, int frames,
+                                cudaStream_t st) {
+    const bool ce = a.ce_taps > 0;
+    const bool prune = ce && a.ce_taps <= 128;
+    if (!ce) {
+        if (ls) return win ? launch_col_fast_t<kLS | kWin>(a, tw_t, frames, st) : launch_col_fast_t<kLS>(a, tw_t, frames, st);
+        return win ? launch_col_fast_t<kWin>(a, tw_t, frames, st) : launch_col_fast_t<0>(a, tw_t, frames, st);
+    }
+    if (!ls) return cudaErrorInvalidValue;  // pipeline CE always starts from (Y, X)
+    if (a.shortcut) return launch_col_fast_t<kLS | kCE | kShortcut>(a, tw_t, frames, st);
+    if (win) {
+        return prune ? launch_col_fast_t<kLS | kCE | kPrune | kWin>(a, tw_t, frames, st)
+                     : launch_col_fast_t<kLS | kCE | kWin>(a, tw_t, frames, st);
+    }
+    return prune ? launch_col_fast_t<kLS | kCE | kPrune>(a, tw_t, frames, st)
+                 : launch_col_fast_t<kLS | kCE>(a, tw_t, frames, st);
+}
+
+cudaError_t launch_rowpass_fast(const FastRowArgs& a, int frames, cudaStream_t st) {
+    cudaError_t err = cudaFuncSetAttribute(rowpass256_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem);
+    if (err != cudaSuccess) return err;
+    dim3 grid((1024 + kRowR - 1) / kRowR, frames);
+    rowpass256_fast<<<grid, 256, kRowSmem, st>>>(a);
+    return cudaGetLastError();
+}
+
+int fast_rows_per_block() { return kRowR; }
+
+}  // namespace ofdmr

@@ -80,4 +80,54 @@ __device__ __forceinline__ unsigned long long make_key(float p, uint32_t idx) {
     return (static_cast<unsigned long long>(__float_as_uint(p)) << 32) | (0xFFFFFFFFu - idx);
 }
 
+// Block-wide top-K selection over a shared-memory key list (keys unique, 0 = empty).
+// Writes up to K keys in descending order to out[0..K) (zero-filled).  NT threads.
+template <int NT>
+__device__ __forceinline__ void block_topk(unsigned long long* list, int cnt, int K, unsigned long long* out,
+                           unsigned long long* s_best, int* s_idx) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int round = 0; round < K; ++round) {
+        unsigned long long best = 0;
+        int bi = -1;
+        for (int i = threadIdx.x; i < cnt; i += NT) {
+            const unsigned long long v = list[i];
+            if (v > best) { best = v; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best) { best = ob; bi = oi; }
+        }
+        if (lane == 0) { s_best[w] = best; s_idx[w] = bi; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long b = 0;
+            int id = -1;
+            for (int i = 0; i < NT / 32; ++i)
+                if (s_best[i] > b) { b = s_best[i]; id = s_idx[i]; }
+            out[round] = b;
+            if (id >= 0) list[id] = 0;
+            s_best[0] = b;
+        }
+        __syncthreads();
+        const bool done = s_best[0] == 0;
+        __syncthreads();
+        if (done) {
+            for (int r = round + 1 + threadIdx.x; r < K; r += NT) out[r] = 0;
+            break;
+        }
+    }
+}
+
+__device__ __forceinline__ void block_topk_smem(unsigned long long* list, int cnt, int K, unsigned long long* out,
+                                                unsigned long long* s_best, int* s_idx) {
+    block_topk<256>(list, cnt, K, out, s_best, s_idx);
+}
+// Same over a global-memory scratch list (entries are consumed in place).
+__device__ __forceinline__ void block_topk_global(unsigned long long* list, int cnt, int K, unsigned long long* out,
+                                                  unsigned long long* s_best, int* s_idx) {
+    block_topk<256>(list, cnt, K, out, s_best, s_idx);
+}
+
 }  // namespace ofdmr
