@@ -192,22 +192,30 @@ __global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
 
     const float2* gf = a.g + (size_t)f * a.g_rows * m;
     for (int t0 = 0; t0 < TR; t0 += 16) {
+        // a warp's two half-warps must stay converged (the half-warp FFT uses __syncwarp):
+        // rows past the tile or at/after g_rows (exactly zero) load zeros, stores are predicated
         const int tr = t0 + hw;
-        if (tr < TR) {
-            const int gr = (r0 - 1 + tr + np) & (np - 1);
-            float* prow = ptile + tr * 256;
-            if (gr < a.g_rows) {
-                float2 v[16];
-                const float2* src = gf + (size_t)gr * m;
+        const bool in_tile = tr < TR;
+        const int gr = (r0 - 1 + tr + np) & (np - 1);
+        const bool nonzero = in_tile && gr < a.g_rows;
+        const int wtr = t0 + (hw & ~1);                      // first tile row of this warp
+        const bool warp_active = wtr < TR;
+        const bool warp_any = warp_active && ((((r0 - 1 + wtr + np) & (np - 1)) < a.g_rows) ||
+                                              (wtr + 1 < TR && ((r0 + wtr + np) & (np - 1)) < a.g_rows));
+        float* prow = ptile + tr * 256;
+        if (warp_any) {
+            float2 v[16];
+            const float2* src = gf + (size_t)(nonzero ? gr : 0) * m;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = __ldcs(src + j + 16 * i);
-                halfwarp_fft256<false>(v, tbufs + hw * 16 * 17, tw);
+            for (int i = 0; i < 16; ++i) v[i] = nonzero ? __ldcs(src + j + 16 * i) : make_float2(0.f, 0.f);
+            halfwarp_fft256<false>(v, tbufs + hw * 16 * 17, tw);
+            if (in_tile) {
 #pragma unroll
                 for (int t2 = 0; t2 < 16; ++t2) prow[(j + 16 * t2 + 128) & 255] = cnorm(v[t2]) * a.scale;
-            } else {
-#pragma unroll
-                for (int t2 = 0; t2 < 16; ++t2) prow[j + 16 * t2] = 0.f;
             }
+        } else if (in_tile) {
+#pragma unroll
+            for (int t2 = 0; t2 < 16; ++t2) prow[j + 16 * t2] = 0.f;
         }
     }
     __syncthreads();
