@@ -38,33 +38,48 @@ __global__ void __launch_bounds__(256, 2) colpass1024_fast(ColArgs a, const floa
 
     for (int i = tid; i < 1024; i += 256) tw[i] = tw_t[i];
 
+    // Tile load: 16 float4 per thread per array, issued in two batches of 8 so that
+    // 8 (H) or 16 (Y and X) independent 16-B loads per thread are in flight.
     double inv_acc = 0.0;
     int zero_cell = 0;
-#pragma unroll 4
-    for (int idx = tid; idx < 1024 * (kFastC / 2); idx += 256) {
-        const int k = idx >> 2;
-        const int c = (idx & 3) * 2;
-        const size_t off = fbase + (size_t)k * m + c0 + c;
-        float2 h0, h1;
-        if constexpr (MODE & kLS) {
-            const float4 yv = __ldcs(reinterpret_cast<const float4*>(a.y + off));
-            const float4 xv = __ldcs(reinterpret_cast<const float4*>(a.x + off));
-            const float n0 = fmaf(xv.x, xv.x, xv.y * xv.y);
-            const float n1 = fmaf(xv.z, xv.z, xv.w * xv.w);
-            float i0 = 0.f, i1 = 0.f;
-            if (n0 == 0.f) zero_cell = 1; else i0 = 1.0f / n0;
-            if (n1 == 0.f) zero_cell = 1; else i1 = 1.0f / n1;
-            inv_acc += (double)i0 + (double)i1;
-            h0 = make_float2(fmaf(yv.x, xv.x, yv.y * xv.y) * i0, fmaf(yv.y, xv.x, -yv.x * xv.y) * i0);
-            h1 = make_float2(fmaf(yv.z, xv.z, yv.w * xv.w) * i1, fmaf(yv.w, xv.z, -yv.z * xv.w) * i1);
-        } else {
-            const float4 hv = __ldcs(reinterpret_cast<const float4*>(a.h + off));
-            h0 = make_float2(hv.x, hv.y);
-            h1 = make_float2(hv.z, hv.w);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        float4 yv[8], xv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int idx = tid + (half * 8 + q) * 256;
+            const size_t off = fbase + (size_t)(idx >> 2) * m + c0 + (idx & 3) * 2;
+            if constexpr (MODE & kLS) {
+                yv[q] = __ldcs(reinterpret_cast<const float4*>(a.y + off));
+                xv[q] = __ldcs(reinterpret_cast<const float4*>(a.x + off));
+            } else {
+                yv[q] = __ldcs(reinterpret_cast<const float4*>(a.h + off));
+            }
         }
-        const int p = k + (k >> 5);
-        tile[c * kColVS + p] = h0;
-        tile[(c + 1) * kColVS + p] = h1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int idx = tid + (half * 8 + q) * 256;
+            const int k = idx >> 2;
+            const int c = (idx & 3) * 2;
+            float2 h0, h1;
+            if constexpr (MODE & kLS) {
+                const float n0 = fmaf(xv[q].x, xv[q].x, xv[q].y * xv[q].y);
+                const float n1 = fmaf(xv[q].z, xv[q].z, xv[q].w * xv[q].w);
+                float i0 = 0.f, i1 = 0.f;
+                if (n0 == 0.f) zero_cell = 1; else i0 = 1.0f / n0;
+                if (n1 == 0.f) zero_cell = 1; else i1 = 1.0f / n1;
+                inv_acc += (double)i0 + (double)i1;
+                const float4 y4 = yv[q], x4 = xv[q];
+                h0 = make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
+                h1 = make_float2(fmaf(y4.z, x4.z, y4.w * x4.w) * i1, fmaf(y4.w, x4.z, -y4.z * x4.w) * i1);
+            } else {
+                h0 = make_float2(yv[q].x, yv[q].y);
+                h1 = make_float2(yv[q].z, yv[q].w);
+            }
+            const int p = k + (k >> 5);
+            tile[c * kColVS + p] = h0;
+            tile[(c + 1) * kColVS + p] = h1;
+        }
     }
     if constexpr (MODE & kLS) {
         if (zero_cell) atomicOr(a.status + f, 1);
