@@ -286,11 +286,14 @@ def main():
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-        "kernel": "pipeline step: colpass (LS+DFT-CE+window+IFFT_N) + rowpass (FFT_M'+|.|^2+detect) + merge, "
-                  "chunked so the k-pass intermediate stays in L2",
+        "kernel": ("fused_ce1024 (persistent, one frame per CTA: LS + IFFT/truncate -> L x M taps -> row FFT -> "
+                   "pruned FFT x w_k -> IFFT -> |.|^2 -> 3x3 top-K)" if stage_n[1] == 0 else
+                   "pipeline step: colpass + rowpass + merge, chunked so the intermediate stays in L2"),
         "algorithmic_bytes_per_frame": alg_bytes_frame, "frames_per_launch_chunk": int(rx.cfg.chunk_frames) or None,
-        "stage_ms": {"colpass": stage_ms[0], "rowpass": stage_ms[1], "merge": stage_ms[2]},
-        "stage_launches": {"colpass": int(stage_n[0]), "rowpass": int(stage_n[1]), "merge": int(stage_n[2])},
+        "stage_ms": ({"fused_ce": stage_ms[0]} if stage_n[1] == 0 else
+                     {"colpass": stage_ms[0], "rowpass": stage_ms[1], "merge": stage_ms[2]}),
+        "stage_launches": ({"fused_ce": int(stage_n[0])} if stage_n[1] == 0 else
+                           {"colpass": int(stage_n[0]), "rowpass": int(stage_n[1]), "merge": int(stage_n[2])}),
         "step_ms_events": ms,
     }
 

@@ -9,7 +9,9 @@ import ctypes as C
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libofdmr_b200.so"
+import os
+
+LIB_PATH = Path(os.environ["OFDMR_LIB"]) if os.environ.get("OFDMR_LIB") else PKG / "libofdmr_b200.so"
 GEN_PATH = PKG / "libofdmr_gen.so"
 
 vp = C.c_void_p

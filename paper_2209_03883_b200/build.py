@@ -46,6 +46,8 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
     units = {
         "radar_kernels": [],
         "fast_kernels": [],
+        "fused_ce": [],
+        "fused_ws": [],
         "capi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions
         "sft_kernels": ["-fmad=false"],

@@ -3,6 +3,7 @@
 // host-buffer (H2D/D2H inside) pipeline entry point.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -32,6 +33,32 @@ struct FastRowArgs {
 cudaError_t launch_colpass_fast(const ColArgs& a, bool ls, bool win, const float2* tw_t, int frames, cudaStream_t st);
 cudaError_t launch_rowpass_fast(const FastRowArgs& a, int frames, cudaStream_t st);
 int fast_rows_per_block();
+struct FusedArgs {
+    const float2* y;
+    const float2* x;
+    const double* sigma2;
+    const int32_t* k_per_frame;
+    int32_t* det_delay;
+    int32_t* det_doppler;
+    float* det_power;
+    int32_t* counts;
+    double* s2h_out;
+    int32_t* status;
+    const float* wk;
+    const float* wl;
+    const float2* tw1024_t;
+    const float2* tw256_t;
+    float2* dscratch;
+    int frames;
+    int L;
+    int kmax;
+    double log_pfa, power_factor, inv_count;
+    float scale;
+    long long stagger_ns;
+    int dbg;
+};
+cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
+cudaError_t launch_fused_ws(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
 }  // namespace ofdmr
 
 using namespace ofdmr;
@@ -82,6 +109,9 @@ struct ofdmr_context {
     cudaStream_t aux_stream = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fast = false;           // N = N' = 1024, M = M' = 256 specialised kernels
+    bool fused = false;          // + DFT-CE with 0 < L <= 128: persistent one-frame-per-CTA kernel
+    int fused_grid = 0;
+    float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
     float2* tw1024_t = nullptr;  // [t1*32 + j] = W_1024^{j t1}
     float2* tw256_t = nullptr;   // [t1*16 + j] = W_256^{j t1}
     // slot-0 aliases used by the single-stream entry points
@@ -400,6 +430,7 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
     c->inv_count = 1.0 / double(size_t(n) * size_t(m));
     c->scale = float(1.0 / (double(n) * double(m)));
     c->fast = n == 1024 && np == 1024 && m == 256 && mp == 256;
+    c->fused = c->fast && cfg->estimator == OFDMR_EST_DFT_CE && cfg->n_cp > 0 && cfg->n_cp <= 128;
     if (c->fast) {
         c->rows_per_block = fast_rows_per_block();
         c->nblk = (np + c->rows_per_block - 1) / c->rows_per_block;
@@ -462,6 +493,13 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         if (e == cudaSuccess) e = cudaMemcpy(c->tw1024_t, t1024.data(), sizeof(float2) * 1024, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->tw256_t, t256.data(), sizeof(float2) * 256, cudaMemcpyHostToDevice);
     }
+    if (e == cudaSuccess && c->fused) {
+        int sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
+        c->fused_grid = 2 * sms;  // 2 resident CTAs per SM (128 regs x 256 threads, ~102 KB smem)
+        // two frames in flight per 2-CTA cluster (pass A of frame i+1 overlaps pass C of frame i)
+        if (e == cudaSuccess) e = cudaMalloc(&c->dscratch, sizeof(float2) * 128 * 256 * size_t(c->fused_grid));
+    }
     c->gbuf = c->slot[0].gbuf;
     c->partial = c->slot[0].partial;
     c->cand = c->slot[0].cand;
@@ -489,6 +527,7 @@ void ofdmr_destroy(ofdmr_context* c) {
     }
     cudaFree(c->tw1024_t);
     cudaFree(c->tw256_t);
+    cudaFree(c->dscratch);
     if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -773,6 +812,57 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
     const size_t pframe = size_t(g.n_prime) * size_t(g.m_prime);
     const int K = g.max_targets;
     if (status) OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
+    if (c->fused && p_out == nullptr) {
+        // one persistent launch over the whole batch
+        FusedArgs fa{};
+        fa.y = static_cast<const float2*>(y);
+        fa.x = static_cast<const float2*>(x);
+        fa.sigma2 = sigma2;
+        fa.k_per_frame = kpf;
+        fa.det_delay = d;
+        fa.det_doppler = dp;
+        fa.det_power = pw;
+        fa.counts = cnt;
+        fa.s2h_out = s2h_out;
+        fa.status = status;
+        const bool win = g.window == OFDMR_WINDOW_HAMMING;
+        fa.wk = win ? c->wk : nullptr;
+        fa.wl = win ? c->wl : nullptr;
+        fa.tw1024_t = c->tw1024_t;
+        fa.tw256_t = c->tw256_t;
+        fa.dscratch = c->dscratch;
+        fa.L = g.n_cp;
+        fa.kmax = K;
+        fa.log_pfa = c->log_pfa;
+        fa.power_factor = c->pf;
+        fa.inv_count = c->inv_count;
+        fa.scale = c->scale;
+        {
+            const char* st = getenv("OFDMR_STAGGER_NS");
+            fa.stagger_ns = st ? atoll(st) : 0;
+            const char* dbg = getenv("OFDMR_FUSED_DBG");
+            fa.dbg = dbg ? atoi(dbg) : 0;
+        }
+        for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
+            const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);
+            fa.frames = int(nf);
+            cudaError_t e;
+            {
+                StageTimer t(c, 0, c->stream);
+                const char* var = getenv("OFDMR_FUSED");
+                if (var && var[0] == 'w') {
+                    // warp-specialised variant: one 384-thread CTA per SM (producer/consumer warps)
+                    e = launch_fused_ws(fa, win, int(std::min<int64_t>(c->fused_grid / 2, 2 * nf)), c->stream);
+                } else {
+                    // default: two 256-thread CTAs per SM, 2-CTA cluster per frame
+                    e = launch_fused_ce(fa, win, int(std::min<int64_t>(c->fused_grid, 2 * nf)), c->stream);
+                }
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "fused_ce");
+            ++c->launches;
+        }
+        return OFDMR_OK;
+    }
     const bool two = !c->profiling && frames > c->chunk;
     if (two) {
         OFDMR_CUDA(cudaEventRecord(c->ev_fork, c->stream));

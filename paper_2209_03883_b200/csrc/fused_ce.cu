@@ -1,0 +1,581 @@
+// Persistent fused receiver kernel for the DFT-CE pipeline at N = N' = 1024, M = M' = 256,
+// L <= 128 (cfg1 / cfg4): one CTA owns one frame at a time, all three passes in-CTA, no
+// cross-CTA synchronisation, one launch per batch.
+//
+//   pass A  (32 column tiles of 8 symbols, one warp per column): tile load fuses LS
+//           division (estimation.cpp:10-21), the zero-cell check and sum 1/|x|^2
+//           (pipeline.cpp:18-23); warp IFFT_1024; keep the first L taps x 1/N (DFT-CE,
+//           estimation.cpp:23-39) -> D (L x M c64, per-CTA scratch, L2-resident).
+//   pass B  row FFT_256 of the L tap rows with the symbol window w_l (periodogram.cpp:52-57)
+//           -> D' in place.  Linear k-axis and l-axis operators commute, so doing the
+//           l-axis transform on the L-row compressed form is exact and 8x cheaper than on
+//           all N' rows.
+//   pass C  per column tile: input-pruned FFT_1024 of the L taps (back to subcarriers),
+//           x w_k, delay IFFT_1024 (periodogram.cpp:60), |.|^2/(NM) (:63-73) into a rolling
+//           window of P columns in shared memory; strict wrapped 3x3 local maxima >= eta
+//           (:77-136) over columns whose neighbours are resident; running per-frame top-K.
+//           With a rectangular window the k-chain is the identity up to N (exact shortcut).
+//
+// Memory per frame: 4 MiB of HBM reads (Y, x_tx), 1 MiB of L2 traffic (D, D'), ~100 B out.
+#include <cooperative_groups.h>
+
+#include "radar_kernels.cuh"
+#include "warp_fft.cuh"
+
+namespace ofdmr {
+
+#ifdef OFDMR_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[16];
+#define PH_INIT() long long _ph_t = clock64();
+#define PH(i)                                                              \
+    do {                                                                   \
+        if (threadIdx.x == 0) {                                            \
+            const long long _n = clock64();                                \
+            atomicAdd(&g_phase_cycles[i], (unsigned long long)(_n - _ph_t)); \
+            _ph_t = _n;                                                    \
+        }                                                                  \
+    } while (0)
+#else
+#define PH_INIT()
+#define PH(i)
+#endif
+
+struct FusedArgs {
+    const float2* y;
+    const float2* x;
+    const double* sigma2;
+    const int32_t* k_per_frame;
+    int32_t* det_delay;
+    int32_t* det_doppler;
+    float* det_power;
+    int32_t* counts;
+    double* s2h_out;
+    int32_t* status;
+    const float* wk;           // null for rectangular
+    const float* wl;
+    const float2* tw1024_t;
+    const float2* tw256_t;
+    float2* dscratch;          // [gridDim.x][128 * 256]
+    int frames;
+    int L;
+    int kmax;
+    double log_pfa, power_factor, inv_count;
+    float scale;
+    long long stagger_ns;      // unused (kept for ABI of the debug build)
+    int dbg;                   // debug switches (experiments only): 1 = no A loads, 2 = no LS math
+};
+
+namespace {
+
+constexpr int kM = 256;
+constexpr int kN = 1024;
+constexpr int kVS = 1057;         // padded column buffer (pad_len(1024))
+constexpr int kTileList = 1024;   // per-tile candidate list (exact fallback beyond)
+
+struct FusedSmem {
+    float2 tw[1024];
+    float2 tw256[256];
+    float2 cols[8 * kVS];         // per-warp column buffers / pass-A,C tiles / pass-B scratch
+    float keep[4][kN];            // rank 1: previous step's columns 6, 7; rank 0: frame columns 0, 1 (2, 3)
+    float ext[2][kN];             // partner columns staged for this step's detection
+    unsigned long long tl[kTileList];  // per-frame candidate list (strict maxima >= eta)
+    unsigned long long run[kMaxK];     // per-CTA top-K (descending, 0-padded)
+    unsigned long long cand2[kMaxK];
+    unsigned long long sbest[8];
+    int sidx[8];
+    const float* dA[10];               // per-step detection descriptors (uniform across the CTA)
+    const float* dB[10];
+    const float* dC[10];
+    int dsn[10];
+    int dcnt;
+    double red[8];
+    int tcnt;
+    int zc_part;
+    int overflow;
+    int zcs[2];
+    double part;
+    double etas[2];
+    double s2hs[2];
+};
+
+// Strict wrapped 3x3 maximum test on P columns a, b, c (b tested) at row r.
+__device__ __forceinline__ bool strict_max3(const float* a, const float* b, const float* c, int r, float v) {
+    const int ru = (r - 1) & (kN - 1), rd = (r + 1) & (kN - 1);
+    return !(a[ru] >= v || a[r] >= v || a[rd] >= v || b[ru] >= v || b[rd] >= v || c[ru] >= v || c[r] >= v ||
+             c[rd] >= v);
+}
+
+// Warp 0: merge the tile list (cnt keys) into the running top-K (K keys, sorted desc).
+__device__ void warp_merge_topk(unsigned long long* run, unsigned long long* tl, int cnt, int K,
+                                unsigned long long* tmp) {
+    const int lane = threadIdx.x & 31;
+    for (int r = 0; r < K; ++r) {
+        unsigned long long best = 0;
+        int where = -1;  // >= 0: tl index; < 0: -(run index) - 2
+        for (int i = lane; i < cnt; i += 32)
+            if (tl[i] > best) { best = tl[i]; where = i; }
+        for (int i = lane; i < K; i += 32)
+            if (run[i] > best) { best = run[i]; where = -i - 2; }
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int ow = __shfl_xor_sync(0xffffffffu, where, o);
+            if (ob > best) { best = ob; where = ow; }
+        }
+        if (lane == 0) {
+            tmp[r] = best;
+            if (best != 0) {
+                if (where >= 0) tl[where] = 0;
+                else run[-where - 2] = 0;
+            }
+        }
+        __syncwarp();
+    }
+    for (int i = lane; i < K; i += 32) run[i] = tmp[i];
+    __syncwarp();
+}
+
+}  // namespace
+
+// Pull the 128-B lines of one 8-column tile (1024 rows of Y and x_tx) into L2 so the next
+// tile's loads hit L2 while this tile computes (the pair covers both 64-B halves of a line).
+__device__ __forceinline__ void prefetch_tile(const float2* y, const float2* x, size_t fbase, int c0, int mode) {
+    if (mode == 1) return;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const size_t off = fbase + (size_t)(threadIdx.x + 256 * j) * kM + c0;
+        if (mode == 2) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(y + off));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(x + off));
+        } else if (mode == 3) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(y + off) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(x + off) : "memory");
+        } else {
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(y + off));
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(x + off));
+        }
+    }
+}
+
+// Smallest float t with (double)v >= eta  <=>  v >= t for every float v (exact fp32 test).
+__device__ __forceinline__ float eta_float(double eta) {
+    float e = (float)eta;
+    if ((double)e < eta) e = nextafterf(e, INFINITY);
+    return e;
+}
+
+template <bool HAMMING>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024_kernel(FusedArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FusedSmem& s = *reinterpret_cast<FusedSmem*>(smem_raw);
+    const int rank = (int)cluster.block_rank();             // 0 or 1: which 8-column half of each 16
+    FusedSmem& p = *cluster.map_shared_rank(&s, rank ^ 1);  // partner CTA's shared memory (DSMEM)
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int L = a.L;
+    const int K = a.kmax;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const float* pbase = reinterpret_cast<const float*>(s.cols);
+    auto lcol = [&](int c) -> const float* { return pbase + c * (2 * kVS); };
+    auto dbuf = [&](int parity) { return a.dscratch + ((size_t)cid * 2 + parity) * 128 * kM; };
+
+    for (int i = tid; i < 1024; i += 256) s.tw[i] = a.tw1024_t[i];
+    s.tw256[tid] = a.tw256_t[tid];
+    if (tid == 0) s.overflow = 0;
+    __syncthreads();
+    PH_INIT();
+
+    // ---------------------------------------------------------------- pass A, one tile
+    // column tile u (8 symbols) of frame f: LS divide -> IFFT_N -> L taps x 1/N -> D
+    auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell) {
+        const size_t fbase = (size_t)f * kN * kM;
+        const int c0 = 16 * u + 8 * rank;
+        float inv_tile = 0.f;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            float4 yv[8], xv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = tid + (half * 8 + q) * 256;
+                const size_t off = fbase + (size_t)(idx >> 2) * kM + c0 + (idx & 3) * 2;
+                if (a.dbg & 1) {
+                    yv[q] = make_float4(1.f, 0.f, 1.f, 0.f);
+                    xv[q] = make_float4(1.f, 0.f, 1.f, 0.f);
+                } else {
+                    yv[q] = __ldcs(reinterpret_cast<const float4*>(a.y + off));
+                    xv[q] = __ldcs(reinterpret_cast<const float4*>(a.x + off));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int idx = tid + (half * 8 + q) * 256;
+                const int k = idx >> 2, c = (idx & 3) * 2;
+                const float4 y4 = yv[q], x4 = xv[q];
+                if (a.dbg & 2) {
+                    const int pk = k + (k >> 5);
+                    s.cols[c * kVS + pk] = make_float2(y4.x, y4.y);
+                    s.cols[(c + 1) * kVS + pk] = make_float2(y4.z, y4.w);
+                    continue;
+                }
+                const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
+                const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
+                zero_cell |= (n0 == 0.f) | (n1 == 0.f);
+                const float i0 = n0 == 0.f ? 0.f : __frcp_rn(n0);
+                const float i1 = n1 == 0.f ? 0.f : __frcp_rn(n1);
+                inv_tile += i0 + i1;
+                const int pk = k + (k >> 5);
+                s.cols[c * kVS + pk] =
+                    make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
+                s.cols[(c + 1) * kVS + pk] =
+                    make_float2(fmaf(y4.z, x4.z, y4.w * x4.w) * i1, fmaf(y4.w, x4.z, -y4.z * x4.w) * i1);
+            }
+        }
+        inv_acc += (double)inv_tile;  // fp32 within a tile (32 terms), fp64 across tiles
+        __syncthreads();
+        PH(0);
+        // stream the next tile into L2 while this one computes (one step ahead)
+        if (u < 15) prefetch_tile(a.y, a.x, fbase, c0 + 16, (a.dbg >> 2) & 3);
+        else if (f + ncl < a.frames) prefetch_tile(a.y, a.x, (size_t)(f + ncl) * kN * kM, 8 * rank, (a.dbg >> 2) & 3);
+        {
+            float2* col = s.cols + w * kVS;
+            float2 v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = col[lane + 33 * i];
+            warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: taps t1 + 32 t2
+            __syncwarp();
+            constexpr float inv_n = 1.0f / 1024.0f;
+#pragma unroll
+            for (int t2 = 0; t2 < 4; ++t2) {
+                const int tap = lane + 32 * t2;
+                col[lane + 33 * t2] = tap < L ? cscale(v[t2], inv_n) : make_float2(0.f, 0.f);
+            }
+        }
+        __syncthreads();
+        PH(1);
+        for (int idx = tid; idx < L * 4; idx += 256) {
+            const int k = idx >> 2, c = (idx & 3) * 2;
+            const int pk = k + (k >> 5);
+            const float2 v0 = s.cols[c * kVS + pk];
+            const float2 v1 = s.cols[(c + 1) * kVS + pk];
+            __stcg(reinterpret_cast<float4*>(dsc + (size_t)k * kM + c0 + c), make_float4(v0.x, v0.y, v1.x, v1.y));
+        }
+        __syncthreads();
+        PH(2);
+    };
+
+    // ---------------------------------------------------------------- end of pass A
+    // combine the pair's sum 1/|x|^2 -> sigma_h^2, eta (slot = frame parity); D complete
+    auto A_finish = [&](int f, int slot, double inv_acc, int zero_cell) {
+        double v = inv_acc;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int zc = __any_sync(0xffffffffu, zero_cell);
+        if (lane == 0) s.red[w] = v;
+        if (tid == 0) s.zc_part = 0;
+        __syncthreads();
+        if (lane == 0 && zc) atomicOr(&s.zc_part, 1);
+        if (tid == 0) {
+            double acc = 0.0;
+            for (int i = 0; i < 8; ++i) acc += s.red[i];
+            s.part = acc;
+        }
+        __threadfence();
+        cluster.sync();  // D complete in global (both halves); partials visible
+        if (tid == 0) {
+            const double p0 = rank == 0 ? s.part : p.part;
+            const double p1 = rank == 0 ? p.part : s.part;
+            const double acc = p0 + p1;  // same order in both CTAs
+            const double sg = a.sigma2[f];
+            const double s2h = sg <= 0.0 ? 0.0 : sg * acc * a.inv_count;
+            s.zcs[slot] = s.zc_part | p.zc_part;
+            s.etas[slot] = -s2h * a.log_pfa * a.power_factor;
+            s.s2hs[slot] = s2h;
+        }
+        cluster.sync();  // partner finished reading our partial
+        PH(3);
+    };
+
+    // ---------------------------------------------------------------- pass B
+    auto B_pass = [&](float2* dsc) {
+        const int hw = tid >> 4, j = tid & 15;
+        float2* tb = s.cols + hw * (16 * 17);
+        const int rlo = rank * (L / 2), rhi = rank == 0 ? L / 2 : L;
+        for (int r0 = rlo; r0 < rhi; r0 += 16) {
+            const int r = r0 + hw;
+            const bool valid = r < rhi;
+            float2 v[16];
+            const float2* src = dsc + (size_t)(valid ? r : rlo) * kM;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                float2 uu = valid ? __ldcg(src + j + 16 * i) : make_float2(0.f, 0.f);
+                if (HAMMING) uu = cscale(uu, __ldg(a.wl + j + 16 * i));
+                v[i] = uu;
+            }
+            halfwarp_fft256<false>(v, tb, s.tw256);
+            if (valid) {
+                float2* dst = dsc + (size_t)r * kM;
+#pragma unroll
+                for (int t2 = 0; t2 < 16; ++t2) __stcg(dst + j + 16 * t2, v[t2]);
+            }
+        }
+        __syncthreads();
+        __threadfence();
+        cluster.sync();  // D' complete
+        PH(4);
+    };
+
+    // ---------------------------------------------------------------- pass C, one step
+    auto C_tile = [&](int u, const float2* dsc, float ef) {
+        const int c0 = 16 * u + 8 * rank;
+        for (int idx = tid; idx < 128 * 4; idx += 256) {
+            const int k = idx >> 2, c = (idx & 3) * 2;
+            float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (k < L) v4 = __ldcg(reinterpret_cast<const float4*>(dsc + (size_t)k * kM + c0 + c));
+            const int pk = k + (k >> 5);
+            s.cols[c * kVS + pk] = make_float2(v4.x, v4.y);
+            s.cols[(c + 1) * kVS + pk] = make_float2(v4.z, v4.w);
+        }
+        __syncthreads();
+        PH(5);
+        {
+            float2* col = s.cols + w * kVS;
+            float* pcol = reinterpret_cast<float*>(col);
+            float2 v[32];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = col[lane + 33 * i];
+            if constexpr (HAMMING) {
+                warp_fft1024<false, 4>(v, col, s.tw);
+#pragma unroll
+                for (int t2 = 0; t2 < 32; ++t2) v[t2] = cscale(v[t2], __ldg(a.wk + lane + 32 * t2));
+                warp_fft1024<true, 32>(v, col, s.tw);
+                __syncwarp();
+#pragma unroll
+                for (int t2 = 0; t2 < 32; ++t2) pcol[lane + 32 * t2] = cnorm(v[t2]) * a.scale;
+            } else {
+                __syncwarp();
+#pragma unroll
+                for (int t2 = 0; t2 < 32; ++t2) {
+                    float pv = 0.f;
+                    if (t2 < 4) pv = cnorm(cscale(v[t2], 1024.0f)) * a.scale;
+                    pcol[lane + 32 * t2] = pv;
+                }
+            }
+        }
+        __syncthreads();
+        PH(6);
+        cluster.sync();  // both halves' P columns (and the partner's kept columns) ready
+        {
+            const float* pb = reinterpret_cast<const float*>(p.cols);
+            for (int r = tid; r < kN; r += 256) {
+                if (rank == 0) {
+                    s.ext[0][r] = p.keep[1][r];           // column 16u-1 (partner's previous last)
+                    s.ext[1][r] = pb[r];                  // column 16u+8 (partner's first)
+                } else {
+                    s.ext[0][r] = pb[7 * (2 * kVS) + r];  // column 16u+7 (partner's last)
+                    s.ext[1][r] = pb[r];                  // column 16u   (partner's first)
+                }
+            }
+        }
+        if (tid == 0) {
+            // rank 0: 16u..16u+7 (16u skipped at u = 0, done at the wrap)
+            // rank 1: 16u+8..16u+14 and its deferred 16u-1 (u >= 1); 16u+15 waits a step
+            int n = 0;
+            for (int jdx = 0; jdx < 8; ++jdx) {
+                if (rank == 0) {
+                    if (u == 0 && jdx == 0) continue;
+                    s.dA[n] = jdx == 0 ? s.ext[0] : lcol(jdx - 1);
+                    s.dC[n] = jdx == 7 ? s.ext[1] : lcol(jdx + 1);
+                } else {
+                    if (jdx == 7) continue;
+                    s.dA[n] = jdx == 0 ? s.ext[0] : lcol(jdx - 1);
+                    s.dC[n] = lcol(jdx + 1);
+                }
+                s.dB[n] = lcol(jdx);
+                s.dsn[n] = c0 + jdx;
+                ++n;
+            }
+            if (rank == 1 && u > 0) {
+                s.dA[n] = s.keep[0];
+                s.dB[n] = s.keep[1];
+                s.dC[n] = s.ext[1];
+                s.dsn[n] = c0 - 9;
+                ++n;
+            }
+            s.dcnt = n;
+        }
+        cluster.sync();  // partner done reading our columns / kept columns; table visible
+        PH(7);
+        const int dcnt = s.dcnt;
+        for (int e = 0; e < dcnt; ++e) {
+            const float* A = s.dA[e];
+            const float* B = s.dB[e];
+            const float* Cc = s.dC[e];
+            const int sc = (s.dsn[e] + kM / 2) & (kM - 1);
+#pragma unroll
+            for (int q = 0; q < kN / 256; ++q) {
+                const int r = tid + q * 256;
+                const float vv = B[r];
+                if (vv >= ef && strict_max3(A, B, Cc, r, vv)) {
+                    const int slot = atomicAdd(&s.tcnt, 1);
+                    if (slot < kTileList) s.tl[slot] = make_key(vv, (uint32_t)(r * kM + sc));
+                }
+            }
+        }
+        __syncthreads();
+        PH(8);
+        for (int r = tid; r < kN; r += 256) {
+            if (rank == 1) {
+                s.keep[0][r] = lcol(6)[r];
+                s.keep[1][r] = lcol(7)[r];
+            } else if (u == 0) {
+                s.keep[2][r] = lcol(0)[r];
+                s.keep[3][r] = lcol(1)[r];
+            }
+        }
+        __syncthreads();
+        PH(9);
+    };
+
+    // ---------------------------------------------------------------- end of pass C
+    auto C_finish = [&](int f, int slot, float ef) {
+        // wrap: rank 0 tests column 0 (needs 255 = partner keep[1], and 1); rank 1 tests 255
+        cluster.sync();
+        for (int r = tid; r < kN; r += 256) s.ext[0][r] = rank == 0 ? p.keep[1][r] : p.keep[2][r];
+        cluster.sync();
+        for (int r = tid; r < kN; r += 256) {
+            const float *A, *B, *Cc;
+            int sn;
+            if (rank == 0) {
+                A = s.ext[0];
+                B = s.keep[2];
+                Cc = s.keep[3];
+                sn = 0;
+            } else {
+                A = s.keep[0];
+                B = s.keep[1];
+                Cc = s.ext[0];
+                sn = 255;
+            }
+            const float vv = B[r];
+            if (!(vv >= ef) || !strict_max3(A, B, Cc, r, vv)) continue;
+            const int sc = (sn + kM / 2) & (kM - 1);
+            const int sl = atomicAdd(&s.tcnt, 1);
+            if (sl < kTileList) s.tl[sl] = make_key(vv, (uint32_t)(r * kM + sc));
+        }
+        __syncthreads();
+        // per-CTA top-K of the frame's candidates (> kTileList strict maxima above eta in one
+        // half-frame sets status bit 1 so the host recomputes the frame on the general path)
+        if (tid == 0 && s.tcnt > kTileList) s.overflow = 1;
+        block_topk<256>(s.tl, min(s.tcnt, kTileList), K, s.run, s.sbest, s.sidx);
+        __syncthreads();
+        cluster.sync();  // both per-CTA lists final
+        if (rank == 0) {
+            if (w == 0) {
+                for (int i = lane; i < K; i += 32) s.tl[i] = p.run[i];
+                __syncwarp();
+                warp_merge_topk(s.run, s.tl, K, K, s.cand2);
+            }
+            __syncthreads();
+            const int kf = a.k_per_frame ? min(a.k_per_frame[f], K) : K;
+            if (tid < K) {
+                const unsigned long long key = tid < kf ? s.run[tid] : 0ull;
+                const size_t o = (size_t)f * K + tid;
+                if (key == 0) {
+                    a.det_delay[o] = 0;
+                    a.det_doppler[o] = 0;
+                    a.det_power[o] = 0.f;
+                } else {
+                    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
+                    a.det_delay[o] = (int32_t)(idx >> 8);
+                    a.det_doppler[o] = (int32_t)(idx & 255) - 128;
+                    a.det_power[o] = __uint_as_float((uint32_t)(key >> 32));
+                }
+            }
+            if (tid == 0) {
+                int n = 0;
+                for (int i = 0; i < kf; ++i) n += s.run[i] != 0;
+                a.counts[f] = n;
+                if (a.s2h_out) a.s2h_out[f] = s.s2hs[slot];
+                if (a.status && s.zcs[slot]) atomicOr(a.status + f, 1);
+                if (a.status && (s.overflow || p.overflow)) atomicOr(a.status + f, 2);
+            }
+        }
+        cluster.sync();  // partner's run list consumed before the next frame resets it
+        if (tid == 0) s.overflow = 0;
+        PH(10);
+    };
+
+    // ---------------------------------------------------------------- schedule
+    // prologue: pass A + B of the first frame; then each round interleaves pass A of frame
+    // i+1 (HBM streaming) with pass C of frame i (issue-bound) tile by tile.
+    if (cid < a.frames) {
+        double inv_acc = 0.0;
+        int zc = 0;
+        for (int u = 0; u < 16; ++u) A_tile(cid, u, dbuf(0), inv_acc, zc);
+        A_finish(cid, 0, inv_acc, zc);
+        B_pass(dbuf(0));
+    }
+    int it = 0;
+    for (int fC = cid; fC < a.frames; fC += ncl, ++it) {
+        const int fN = fC + ncl;
+        const bool hasN = fN < a.frames;
+        const int sc = it & 1, sn = sc ^ 1;
+        if (tid == 0) s.tcnt = 0;
+        for (int i = tid; i < K; i += 256) s.run[i] = 0ull;
+        const float ef = eta_float(s.etas[sc]);
+        __syncthreads();
+        double inv_acc = 0.0;
+        int zc = 0;
+        for (int u = 0; u < 16; ++u) {
+            if (hasN) A_tile(fN, u, dbuf(sn), inv_acc, zc);
+            C_tile(u, dbuf(sc), ef);
+        }
+        C_finish(fC, sc, ef);
+        if (hasN) {
+            A_finish(fN, sn, inv_acc, zc);
+            B_pass(dbuf(sn));
+        }
+    }
+}
+
+size_t fused_ce_smem() { return sizeof(FusedSmem); }
+
+}  // namespace ofdmr
+
+extern "C" int ofdmr_debug_phase_cycles(unsigned long long* out, int reset) {
+#ifdef OFDMR_PHASE_TIMING
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, ofdmr::g_phase_cycles, sizeof(unsigned long long) * 16);
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(ofdmr::g_phase_cycles, z, sizeof(z));
+    }
+    return 16;
+#else
+    (void)out;
+    (void)reset;
+    return 0;
+#endif
+}
+
+namespace ofdmr {
+
+cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st) {
+    const size_t smem = sizeof(FusedSmem);
+    grid &= ~1;  // whole clusters
+    if (grid < 2) grid = 2;
+    if (hamming) {
+        cudaError_t e = cudaFuncSetAttribute(fused_ce1024_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        fused_ce1024_kernel<true><<<grid, 256, smem, st>>>(a);
+    } else {
+        cudaError_t e = cudaFuncSetAttribute(fused_ce1024_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        fused_ce1024_kernel<false><<<grid, 256, smem, st>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace ofdmr
