@@ -443,6 +443,7 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         if (chunk < 1) chunk = 1;
         if (chunk > 256) chunk = 256;
     }
+    if (c->fused && cfg->chunk_frames <= 0) chunk = 512;  // host-buffer path: fill every cluster
     c->chunk = chunk;
 
     std::vector<float2> tw(kTwLenHost);
