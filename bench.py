@@ -206,8 +206,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2209_03883_b200.receiver import Receiver
 
+    from paper_2209_03883_b200.shard import shard_range
+
     F = cfg.frames
-    lo, hi = rank * F // world, (rank + 1) * F // world
+    lo, hi = shard_range(F, rank, world)
     nf = hi - lo
     pool = make_pool(cfg, lo, min(args.pool, nf))
     P = len(pool.y)
@@ -223,22 +225,18 @@ def main():
     s2 = torch.from_numpy(s2_host).to(dev)
     kf = torch.from_numpy(k_host).to(dev)
 
+    from paper_2209_03883_b200.shard import DetectionGather
+
     rx = Receiver.from_config(cfg, chunk_frames=args.chunk, device=local)
     dets = rx._dets(nf)
     K = cfg.max_targets
-    packed = torch.empty(nf, 3 * K + 1, dtype=torch.int32, device=dev)
-    gathered = [torch.empty(hi2 - lo2, 3 * K + 1, dtype=torch.int32, device=dev)
-                for lo2, hi2 in ((r * F // world, (r + 1) * F // world) for r in range(world))] if rank == 0 else None
+    gather = DetectionGather(F, K, rank, world, dev)
 
     def step():
         rx._stream()
         rx.pipeline_raw(y, x, s2, kf, dets, nf)
-        if world > 1:
-            packed[:, :K] = dets.delay_bin
-            packed[:, K:2 * K] = dets.doppler_bin
-            packed[:, 2 * K:3 * K] = dets.peak_power.view(torch.int32)
-            packed[:, 3 * K] = dets.counts
-            dist.gather(packed, gathered, dst=0)
+        if world > 1:  # detections of every shard to rank 0 (NCCL all_gather of padded records)
+            gather(dets.delay_bin, dets.doppler_bin, dets.peak_power, dets.counts)
 
     for _ in range(args.warmup):
         step()

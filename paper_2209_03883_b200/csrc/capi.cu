@@ -33,6 +33,16 @@ struct FastRowArgs {
 cudaError_t launch_colpass_fast(const ColArgs& a, bool ls, bool win, const float2* tw_t, int frames, cudaStream_t st);
 cudaError_t launch_rowpass_fast(const FastRowArgs& a, int frames, cudaStream_t st);
 int fast_rows_per_block();
+struct PersistArgs {
+    ColArgs col;
+    FastRowArgs row;
+    const float2* tw1024_t;
+    int frames, cf, ring, nchunks, nblk;
+    int* ticket;
+    int* done_cols;
+    int* done_rows;
+};
+cudaError_t launch_pgram_persist(const PersistArgs& pa, bool ls, bool win, int grid, cudaStream_t st);
 struct FusedArgs {
     const float2* y;
     const float2* x;
@@ -112,6 +122,16 @@ struct ofdmr_context {
     bool fused = false;          // + DFT-CE with 0 < L <= 128: persistent one-frame-per-CTA kernel
     int fused_grid = 0;
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
+    // persistent periodogram / LS pipeline (fast shapes): L2-sized ring of intermediates
+    struct Persist {
+        int cf = 8, ring = 4, grid = 0;
+        float2* gring = nullptr;              // ring x cf x N' x M c64
+        double* pring = nullptr;              // ring x cf x ntiles partials
+        unsigned long long* cring = nullptr;  // ring x cf x nblk x K keys
+        int* fdone = nullptr;                 // ring x cf merge counters
+        int* counters = nullptr;              // ticket + done_cols[cap] + done_rows[cap]
+        int64_t cap = 0;
+    } ps;
     float2* tw1024_t = nullptr;  // [t1*32 + j] = W_1024^{j t1}
     float2* tw256_t = nullptr;   // [t1*16 + j] = W_256^{j t1}
     // slot-0 aliases used by the single-stream entry points
@@ -377,6 +397,86 @@ int run_pipeline_chunk(ofdmr_context* c, int si, const float2* y, const float2* 
 
 }  // namespace
 
+namespace {
+
+// Persistent periodogram / LS-pipeline launch over a whole batch (fast shapes).
+// h != null: periodogram of H (map only).  y/x != null: LS pipeline with detection.
+int run_persist(ofdmr_context* c, const float2* h, const float2* y, const float2* x, const double* sigma2,
+                const int32_t* kpf, int32_t* d, int32_t* dp, float* pw, int32_t* cnt, double* s2h_out, float* p_out,
+                int32_t* status, int64_t frames) {
+    const ofdmr_config& g = c->cfg;
+    auto& ps = c->ps;
+    const int nchunks = int((frames + ps.cf - 1) / ps.cf);
+    const int64_t need = 1 + frames + nchunks;
+    if (need > ps.cap) {
+        cudaFree(ps.counters);
+        ps.counters = nullptr;
+        ps.cap = 0;
+        OFDMR_CUDA(cudaMalloc(&ps.counters, sizeof(int) * size_t(need)));
+        ps.cap = need;
+    }
+    OFDMR_CUDA(cudaMemsetAsync(ps.counters, 0, sizeof(int) * size_t(need), c->stream));
+    const bool win = g.window == OFDMR_WINDOW_HAMMING;
+    PersistArgs pa{};
+    pa.col = base_col(c);
+    pa.col.y = y;
+    pa.col.x = x;
+    pa.col.h = h;
+    pa.col.g_out = ps.gring;
+    pa.col.g_rows = g.n_prime;
+    pa.col.status = status;
+    pa.col.inv_partial = y ? ps.pring : nullptr;
+    if (win) {
+        pa.col.wk = c->wk;
+        pa.col.wl = c->wl;
+    }
+    FastRowArgs& r = pa.row;
+    r.r.g = ps.gring;
+    r.r.p_out = p_out;
+    r.r.inv_partial = y ? ps.pring : nullptr;
+    r.r.ntiles = c->ntiles;
+    r.r.sigma2 = sigma2;
+    r.r.log_pfa = c->log_pfa;
+    r.r.power_factor = c->pf;
+    r.r.inv_count = c->inv_count;
+    r.r.scale = c->scale;
+    r.r.n_prime = g.n_prime;
+    r.r.g_rows = g.n_prime;
+    r.r.m = g.n_symbols;
+    r.r.kmax = g.max_targets;
+    r.r.cand = ps.cring;
+    r.r.detect = y ? 1 : 0;
+    r.tw256_t = c->tw256_t;
+    r.frame_done = ps.fdone;
+    r.k_per_frame = kpf;
+    r.det_delay = d;
+    r.det_doppler = dp;
+    r.det_power = pw;
+    r.counts = cnt;
+    r.s2h_out = s2h_out;
+    pa.tw1024_t = c->tw1024_t;
+    pa.frames = int(frames);
+    pa.cf = ps.cf;
+    pa.ring = ps.ring;
+    pa.nchunks = nchunks;
+    pa.nblk = c->nblk;
+    pa.ticket = ps.counters;
+    pa.done_cols = ps.counters + 1;
+    pa.done_rows = ps.counters + 1 + frames;
+    const int64_t items = int64_t(frames) * (32 + c->nblk);
+    const int grid = int(std::min<int64_t>(ps.grid, items));
+    cudaError_t e;
+    {
+        StageTimer t(c, 0, c->stream);
+        e = launch_pgram_persist(pa, y != nullptr, win, grid, c->stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "pgram_persist");
+    ++c->launches;
+    return OFDMR_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* ofdmr_last_error(void) { return g_last_error.c_str(); }
@@ -494,6 +594,19 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         if (e == cudaSuccess) e = cudaMemcpy(c->tw1024_t, t1024.data(), sizeof(float2) * 1024, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->tw256_t, t256.data(), sizeof(float2) * 256, cudaMemcpyHostToDevice);
     }
+    if (e == cudaSuccess && c->fast) {
+        auto& ps = c->ps;
+        int sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
+        ps.grid = 2 * sms;
+        const size_t slots = size_t(ps.ring) * ps.cf;
+        if (e == cudaSuccess) e = cudaMalloc(&ps.gring, slots * size_t(np) * size_t(m) * sizeof(float2));
+        if (e == cudaSuccess) e = cudaMalloc(&ps.pring, slots * size_t(c->ntiles) * sizeof(double));
+        if (e == cudaSuccess)
+            e = cudaMalloc(&ps.cring, slots * size_t(c->nblk) * size_t(cfg->max_targets) * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMalloc(&ps.fdone, slots * sizeof(int));
+        if (e == cudaSuccess) e = cudaMemset(ps.fdone, 0, slots * sizeof(int));
+    }
     if (e == cudaSuccess && c->fused) {
         int sms = 0;
         e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -529,6 +642,11 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->tw1024_t);
     cudaFree(c->tw256_t);
     cudaFree(c->dscratch);
+    cudaFree(c->ps.gring);
+    cudaFree(c->ps.pring);
+    cudaFree(c->ps.cring);
+    cudaFree(c->ps.fdone);
+    cudaFree(c->ps.counters);
     if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -670,6 +788,9 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
     // the general (non-shortcut) G layout is always N' rows; the chunk buffer holds g_rows rows
     const int64_t chunk = c->shortcut ? std::max<int64_t>(1, c->chunk * c->g_rows / g.n_prime) : c->chunk;
     (void)chunk;
+    if (c->fast && getenv("OFDMR_NO_PERSIST") == nullptr)
+        return run_persist(c, static_cast<const float2*>(h), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, nullptr, nullptr, p, nullptr, frames);
     const int64_t pchunk = c->chunk;  // slot buffers hold chunk x N' rows
     const bool two = !c->profiling;
     if (two) {
@@ -863,6 +984,19 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
             ++c->launches;
         }
         return OFDMR_OK;
+    }
+    if (c->fast && g.estimator == OFDMR_EST_LS && getenv("OFDMR_NO_PERSIST") == nullptr) {
+        int32_t* st = status;
+        if (!st) {
+            // status is required by the column items; use scratch for big batches chunk-wise
+            if (frames <= c->chunk) {
+                OFDMR_CUDA(cudaMemsetAsync(c->status_scratch, 0, sizeof(int32_t) * size_t(frames), c->stream));
+                st = c->status_scratch;
+            }
+        }
+        if (st)
+            return run_persist(c, nullptr, static_cast<const float2*>(y), static_cast<const float2*>(x), sigma2, kpf,
+                               d, dp, pw, cnt, s2h_out, p_out, st, frames);
     }
     const bool two = !c->profiling && frames > c->chunk;
     if (two) {

@@ -25,18 +25,17 @@ constexpr int kListCap = 512;        // candidate list in smem; exact fallback s
 
 enum : int { kLS = 1, kCE = 2, kPrune = 4, kWin = 8, kShortcut = 16 };
 
+// One column tile (8 symbols x 1024 subcarriers) of input frame f; G / partials are
+// addressed by frame slot fslot (== f for the per-chunk launches, a ring slot for the
+// persistent schedule).  tw must already hold the 1024-entry table (synced by the caller
+// or by the first barrier below).
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) colpass1024_fast(ColArgs a, const float2* __restrict__ tw_t) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2* tw = reinterpret_cast<float2*>(smem_raw);   // 1024: tw[t1*32 + j] = W^{j t1}
-    float2* tile = tw + 1024;                            // 8 x kColVS
-    __shared__ double red[8];
+__device__ __forceinline__ void col_item(const ColArgs& a, const float2* tw, float2* tile, double* red, int f,
+                                         int tile_idx, int fslot) {
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int f = blockIdx.y, tile_idx = blockIdx.x, c0 = tile_idx * kFastC;
+    const int c0 = tile_idx * kFastC;
     const int m = a.m;
     const size_t fbase = (size_t)f * 1024 * m;
-
-    for (int i = tid; i < 1024; i += 256) tw[i] = tw_t[i];
 
     // Tile load: 16 float4 per thread per array, issued in two batches of 8 so that
     // 8 (H) or 16 (Y and X) independent 16-B loads per thread are in flight.
@@ -95,7 +94,7 @@ __global__ void __launch_bounds__(256, 2) colpass1024_fast(ColArgs a, const floa
         if (a.inv_partial != nullptr && tid == 0) {
             double s = 0.0;
             for (int i = 0; i < 8; ++i) s += red[i];
-            a.inv_partial[(size_t)f * a.ntiles + tile_idx] = s;
+            a.inv_partial[(size_t)fslot * a.ntiles + tile_idx] = s;
         }
     }
 
@@ -140,7 +139,7 @@ __global__ void __launch_bounds__(256, 2) colpass1024_fast(ColArgs a, const floa
     __syncthreads();
 
     // ---- coalesced row-segment store of G (out_rows x 8 columns); G stays in L2
-    float2* g = a.g_out + (size_t)f * a.g_rows * m;
+    float2* g = a.g_out + (size_t)fslot * a.g_rows * m;
 #pragma unroll 4
     for (int idx = tid; idx < out_rows * (kFastC / 2); idx += 256) {
         const int k = idx >> 2;
@@ -150,6 +149,16 @@ __global__ void __launch_bounds__(256, 2) colpass1024_fast(ColArgs a, const floa
         const float2 v1 = tile[(c + 1) * kColVS + p];
         *reinterpret_cast<float4*>(g + (size_t)k * m + c0 + c) = make_float4(v0.x, v0.y, v1.x, v1.y);
     }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) colpass1024_fast(ColArgs a, const float2* __restrict__ tw_t) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* tw = reinterpret_cast<float2*>(smem_raw);   // 1024: tw[t1*32 + j] = W^{j t1}
+    float2* tile = tw + 1024;                            // 8 x kColVS
+    __shared__ double red[8];
+    for (int i = threadIdx.x; i < 1024; i += 256) tw[i] = tw_t[i];
+    col_item<MODE>(a, tw, tile, red, blockIdx.y, blockIdx.x, blockIdx.y);
 }
 
 struct FastRowArgs {
@@ -179,15 +188,19 @@ __device__ __forceinline__ unsigned long long qualify256(const float* pt, int tr
     return make_key(v, (uint32_t)((r0 + tr - 1) * 256 + c));
 }
 
-constexpr size_t kRowSmem = sizeof(float) * (kRowR + 2) * 256 + sizeof(float2) * (256 + 16 * 16 * 17) +
-                            sizeof(unsigned long long) * kListCap;
 
-__global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
+
+// Row-pass region: (R + 2) x 256 fp32 P tile, 16 half-warp transpose buffers, list.
+constexpr size_t kRowRegion = sizeof(float) * (kRowR + 2) * 256 + sizeof(float2) * (16 * 16 * 17) +
+                              sizeof(unsigned long long) * kListCap;
+
+// One block of kRowR rows of P for input frame f (outputs by f; G, partials, candidates and
+// the merge counter by frame slot fslot); nblk blocks per frame.
+__device__ void row_item(const FastRowArgs& e, unsigned char* region, const float2* tw, int f, int fslot, int rb,
+                         int nblk) {
     const RowArgs& a = e.r;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float* ptile = reinterpret_cast<float*>(smem_raw);                       // (R + 2) x 256
-    float2* tw = reinterpret_cast<float2*>(ptile + (kRowR + 2) * 256);      // 256
-    float2* tbufs = tw + 256;                                                // 16 x (16 x 17)
+    float* ptile = reinterpret_cast<float*>(region);                                   // (R + 2) x 256
+    float2* tbufs = reinterpret_cast<float2*>(ptile + (kRowR + 2) * 256);             // 16 x (16 x 17)
     unsigned long long* list = reinterpret_cast<unsigned long long*>(tbufs + 16 * 16 * 17);
     __shared__ unsigned long long s_top[kMaxK];
     __shared__ unsigned long long s_best[8];
@@ -195,17 +208,13 @@ __global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
     __shared__ int s_cnt, s_last;
 
     const int tid = threadIdx.x;
-    const int f = blockIdx.y, rb = blockIdx.x;
     const int np = 1024, m = 256;
     const int r0 = rb * kRowR;
     const int nrows = min(kRowR, np - r0);
     const int TR = nrows + 2;
     const int hw = tid >> 4, j = tid & 15;
 
-    tw[tid] = e.tw256_t[tid];
-    __syncthreads();
-
-    const float2* gf = a.g + (size_t)f * a.g_rows * m;
+    const float2* gf = a.g + (size_t)fslot * a.g_rows * m;
     for (int t0 = 0; t0 < TR; t0 += 16) {
         // a warp's two half-warps must stay converged (the half-warp FFT uses __syncwarp):
         // rows past the tile or at/after g_rows (exactly zero) load zeros, stores are predicated
@@ -222,7 +231,7 @@ __global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
             float2 v[16];
             const float2* src = gf + (size_t)(nonzero ? gr : 0) * m;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = nonzero ? __ldcs(src + j + 16 * i) : make_float2(0.f, 0.f);
+            for (int i = 0; i < 16; ++i) v[i] = nonzero ? __ldcg(src + j + 16 * i) : make_float2(0.f, 0.f);
             halfwarp_fft256<false>(v, tbufs + hw * 16 * 17, tw);
             if (in_tile) {
 #pragma unroll
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
                 s2h = 0.0;
             } else {
                 double acc = 0.0;
-                for (int t = 0; t < a.ntiles; ++t) acc += a.inv_partial[(size_t)f * a.ntiles + t];
+                for (int t = 0; t < a.ntiles; ++t) acc += a.inv_partial[(size_t)fslot * a.ntiles + t];
                 s2h = s2h * acc * a.inv_count;
             }
         }
@@ -305,21 +314,21 @@ __global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
         }
     }
     __syncthreads();
-    unsigned long long* out = a.cand + ((size_t)f * gridDim.x + rb) * K;
+    unsigned long long* out = a.cand + ((size_t)fslot * nblk + rb) * K;
     for (int i = tid; i < K; i += 256) out[i] = s_top[i];
 
     // ---- last block of this frame merges all blocks' candidates
     __threadfence();
     __syncthreads();
     if (tid == 0) {
-        const int prev = atomicAdd(e.frame_done + f, 1);
-        s_last = prev == (int)gridDim.x - 1;
+        const int prev = atomicAdd(e.frame_done + fslot, 1);
+        s_last = prev == nblk - 1;
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    unsigned long long* all = a.cand + (size_t)f * gridDim.x * K;
-    const int total = gridDim.x * K;
+    unsigned long long* all = a.cand + (size_t)fslot * nblk * K;
+    const int total = nblk * K;
     const int kf = e.k_per_frame ? min(e.k_per_frame[f], K) : K;
     block_topk_global(all, total, kf, s_top, s_best, s_idx);
     __syncthreads();
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
         int n = 0;
         for (int i = 0; i < kf; ++i) n += s_top[i] != 0;
         e.counts[f] = n;
-        e.frame_done[f] = 0;  // ready for the next launch
+        e.frame_done[fslot] = 0;  // ready for the next use of this slot
         if (e.s2h_out != nullptr) {
             double s2h = a.sigma2[f];
             if (a.inv_partial != nullptr) {
@@ -349,13 +358,114 @@ __global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
                     s2h = 0.0;
                 } else {
                     double acc = 0.0;
-                    for (int t = 0; t < a.ntiles; ++t) acc += a.inv_partial[(size_t)f * a.ntiles + t];
+                    for (int t = 0; t < a.ntiles; ++t) acc += a.inv_partial[(size_t)fslot * a.ntiles + t];
                     s2h = s2h * acc * a.inv_count;
                 }
             }
             e.s2h_out[f] = s2h;
         }
     }
+}
+
+__global__ void __launch_bounds__(256) rowpass256_fast(FastRowArgs e) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* tw = reinterpret_cast<float2*>(smem_raw);
+    tw[threadIdx.x] = e.tw256_t[threadIdx.x];
+    __syncthreads();
+    row_item(e, smem_raw + 256 * sizeof(float2), tw, blockIdx.y, blockIdx.y, blockIdx.x, gridDim.x);
+}
+
+// ------------------------------------------------------------------ persistent ------
+// One launch for a whole batch: CTAs pull ordered tickets; ticket space per step s is
+// [column items of chunk s | row items of chunk s - 1].  Row items of frame f wait on
+// done_cols[f] == 32; column items of chunk c wait until the row items of chunk c - ring
+// (previous user of the same intermediate slot) are done.  Every waited-on item has a
+// smaller ticket and waits only on smaller tickets, and all CTAs are resident, so the
+// spins always terminate.
+struct PersistArgs {
+    ColArgs col;
+    FastRowArgs row;
+    const float2* tw1024_t;
+    int frames, cf, ring, nchunks, nblk;
+    int* ticket;
+    int* done_cols;   // [frames]
+    int* done_rows;   // [nchunks]
+};
+
+__device__ __forceinline__ void spin_until(const int* p, int target) {
+    if (threadIdx.x == 0) {
+        while (atomicAdd(const_cast<int*>(p), 0) < target) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) pgram_persist(PersistArgs pa) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float2* tw = reinterpret_cast<float2*>(smem_raw);   // 1024
+    float2* tw256 = tw + 1024;                           // 256
+    unsigned char* region = reinterpret_cast<unsigned char*>(tw256 + 256);
+    __shared__ double red[8];
+    __shared__ int s_ticket;
+    for (int i = threadIdx.x; i < 1024; i += 256) tw[i] = pa.tw1024_t[i];
+    tw256[threadIdx.x] = pa.row.tw256_t[threadIdx.x];
+    __syncthreads();
+    const int Lc = pa.cf * 32, Lr = pa.cf * pa.nblk;
+    const long long total = (long long)(pa.nchunks + 1) * (Lc + Lr);
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = atomicAdd(pa.ticket, 1);
+        __syncthreads();
+        const long long t = s_ticket;
+        __syncthreads();
+        if (t >= total) break;
+        const int s = (int)(t / (Lc + Lr));
+        const int r = (int)(t % (Lc + Lr));
+        if (r < Lc) {
+            const int c = s;
+            if (c >= pa.nchunks) continue;
+            const int f = c * pa.cf + r / 32, tile = r % 32;
+            if (f >= pa.frames) continue;
+            if (c >= pa.ring) spin_until(pa.done_rows + (c - pa.ring), Lr);
+            const int fslot = (c % pa.ring) * pa.cf + (f - c * pa.cf);
+            col_item<MODE>(pa.col, tw, reinterpret_cast<float2*>(region), red, f, tile, fslot);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(pa.done_cols + f, 1);
+            }
+        } else {
+            const int c = s - 1;
+            if (c < 0) continue;
+            const int rr = r - Lc;
+            const int f = c * pa.cf + rr / pa.nblk, rb = rr % pa.nblk;
+            if (f < pa.frames) {
+                spin_until(pa.done_cols + f, 32);
+                const int fslot = (c % pa.ring) * pa.cf + (f - c * pa.cf);
+                row_item(pa.row, region, tw256, f, fslot, rb, pa.nblk);
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(pa.done_rows + c, 1);  // counts every row ticket of the chunk
+            }
+        }
+    }
+}
+
+constexpr size_t kPersistSmem = sizeof(float2) * (1024 + 256) +
+                                (kRowRegion > sizeof(float2) * kFastC * kColVS ? kRowRegion
+                                                                                : sizeof(float2) * kFastC * kColVS);
+
+cudaError_t launch_pgram_persist(const PersistArgs& pa, bool ls, bool win, int grid, cudaStream_t st) {
+    auto go = [&](auto kern) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPersistSmem);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, 256, kPersistSmem, st>>>(pa);
+        return cudaGetLastError();
+    };
+    if (ls) return win ? go(pgram_persist<kLS | kWin>) : go(pgram_persist<kLS>);
+    return win ? go(pgram_persist<kWin>) : go(pgram_persist<0>);
 }
 
 // ------------------------------------------------------------------ launch ------
@@ -390,6 +500,7 @@ cudaError_t launch_colpass_fast(const ColArgs& a, bool ls, bool win, const float
 }
 
 cudaError_t launch_rowpass_fast(const FastRowArgs& a, int frames, cudaStream_t st) {
+    constexpr size_t kRowSmem = sizeof(float2) * 256 + kRowRegion;
     cudaError_t err = cudaFuncSetAttribute(rowpass256_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem);
     if (err != cudaSuccess) return err;
     dim3 grid((1024 + kRowR - 1) / kRowR, frames);
