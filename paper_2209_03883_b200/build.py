@@ -87,10 +87,17 @@ def build_oracle(with_ref: bool = True) -> None:
         _run(["make", "-s", "-f", str(mk), "ref"])
 
 
+def build_examples() -> None:
+    """C++ integration example against the reference headers (needs /root/reference)."""
+    if Path("/root/reference/proj/include").is_dir() and (ROOT / "oracle" / "_ref" / "libofdmref.so").exists():
+        _run(["make", "-s", "-f", str(ROOT / "examples" / "Makefile"), "all"])
+
+
 def build_all(force: bool = False) -> None:
     build_gen(force)
     build_cuda(force)
     build_oracle()
+    build_examples()
 
 
 if __name__ == "__main__":

@@ -222,3 +222,17 @@ def test_sft_small_grids_match_oracle(cuda):
         assert ne == ref["n_entries"]
         got = [(int(out["k"][f, i]), int(out["l"][f, i])) for i in range(ne)]
         assert got == [(a, b) for a, b, _ in ref["entries"]]
+
+
+def test_cpp_shim_against_reference_sources(cuda):
+    """examples/shim_vs_reference: a reference C++ caller switched to ofdmradar::b200::
+    (include/ofdmradar_b200.hpp) reproduces the reference's own receiver functions."""
+    import subprocess
+    from pathlib import Path
+
+    exe = Path(__file__).resolve().parents[1] / "examples" / "_bin" / "shim_vs_reference"
+    if not exe.exists():
+        pytest.skip("integration example not built (needs the reference tree at build time)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
