@@ -86,8 +86,14 @@ struct FusedSmem {
     const float* dA[10];               // per-step detection descriptors (uniform across the CTA)
     const float* dB[10];
     const float* dC[10];
+    const unsigned short* dL[10];      // candidate rows of the tested column (P >= eta)
+    int dN[10];                        // their count (-1: list overflowed -> scan the column)
     int dsn[10];
     int dcnt;
+    unsigned short clist[8][64];       // per-column candidate rows of the current step
+    int ccnt[8];
+    unsigned short klist[2][64];       // kept lists: [0] rank 1 previous column 7, [1] rank 0 column 0
+    int kcnt[2];
     double red[8];
     int tcnt;
     int zc_part;
@@ -327,6 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     // ---------------------------------------------------------------- pass C, one step
     auto C_tile = [&](int u, const float2* dsc, float ef) {
         const int c0 = 16 * u + 8 * rank;
+        if (tid < 8) s.ccnt[tid] = 0;
         for (int idx = tid; idx < 128 * 4; idx += 256) {
             const int k = idx >> 2, c = (idx & 3) * 2;
             float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -350,7 +357,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 warp_fft1024<true, 32>(v, col, s.tw);
                 __syncwarp();
 #pragma unroll
-                for (int t2 = 0; t2 < 32; ++t2) pcol[lane + 32 * t2] = cnorm(v[t2]) * a.scale;
+                for (int t2 = 0; t2 < 32; ++t2) {
+                    const float pv = cnorm(v[t2]) * a.scale;
+                    pcol[lane + 32 * t2] = pv;
+                    if (pv >= ef) {  // rare: ~1 % of cells
+                        const int pos = atomicAdd(&s.ccnt[w], 1);
+                        if (pos < 64) s.clist[w][pos] = (unsigned short)(lane + 32 * t2);
+                    }
+                }
             } else {
                 __syncwarp();
 #pragma unroll
@@ -358,6 +372,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                     float pv = 0.f;
                     if (t2 < 4) pv = cnorm(cscale(v[t2], 1024.0f)) * a.scale;
                     pcol[lane + 32 * t2] = pv;
+                    if (pv >= ef) {
+                        const int pos = atomicAdd(&s.ccnt[w], 1);
+                        if (pos < 64) s.clist[w][pos] = (unsigned short)(lane + 32 * t2);
+                    }
                 }
             }
         }
@@ -391,6 +409,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                     s.dC[n] = lcol(jdx + 1);
                 }
                 s.dB[n] = lcol(jdx);
+                s.dL[n] = s.clist[jdx];
+                s.dN[n] = s.ccnt[jdx] > 64 ? -1 : s.ccnt[jdx];
                 s.dsn[n] = c0 + jdx;
                 ++n;
             }
@@ -398,6 +418,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 s.dA[n] = s.keep[0];
                 s.dB[n] = s.keep[1];
                 s.dC[n] = s.ext[1];
+                s.dL[n] = s.klist[0];
+                s.dN[n] = s.kcnt[0];
                 s.dsn[n] = c0 - 9;
                 ++n;
             }
@@ -405,15 +427,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         }
         cluster.sync();  // partner done reading our columns / kept columns; table visible
         PH(7);
-        const int dcnt = s.dcnt;
-        for (int e = 0; e < dcnt; ++e) {
+        const int dcnt = (a.dbg & 32) ? 0 : s.dcnt;
+        for (int e = w; e < dcnt; e += 8) {
             const float* A = s.dA[e];
             const float* B = s.dB[e];
             const float* Cc = s.dC[e];
             const int sc = (s.dsn[e] + kM / 2) & (kM - 1);
-#pragma unroll
-            for (int q = 0; q < kN / 256; ++q) {
-                const int r = tid + q * 256;
+            const int cnt = s.dN[e];
+            const int lim = cnt < 0 ? kN : cnt;  // overflowed list: scan every row
+            for (int i = lane; i < lim; i += 32) {
+                const int r = cnt < 0 ? i : (int)s.dL[e][i];
                 const float vv = B[r];
                 if (vv >= ef && strict_max3(A, B, Cc, r, vv)) {
                     const int slot = atomicAdd(&s.tcnt, 1);
@@ -432,6 +455,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 s.keep[3][r] = lcol(1)[r];
             }
         }
+        {
+            const int kc = rank == 1 ? 7 : 0;
+            const int kk = rank == 1 ? 0 : 1;
+            if (rank == 1 || u == 0) {
+                if (tid < 64) s.klist[kk][tid] = s.clist[kc][tid];
+                if (tid == 0) s.kcnt[kk] = s.ccnt[kc] > 64 ? -1 : s.ccnt[kc];
+            }
+        }
         __syncthreads();
         PH(9);
     };
@@ -442,25 +473,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         cluster.sync();
         for (int r = tid; r < kN; r += 256) s.ext[0][r] = rank == 0 ? p.keep[1][r] : p.keep[2][r];
         cluster.sync();
-        for (int r = tid; r < kN; r += 256) {
+        if (w == 0) {
             const float *A, *B, *Cc;
-            int sn;
+            int sn, cnt;
+            const unsigned short* lst;
             if (rank == 0) {
                 A = s.ext[0];
                 B = s.keep[2];
                 Cc = s.keep[3];
                 sn = 0;
+                lst = s.klist[1];
+                cnt = s.kcnt[1];
             } else {
                 A = s.keep[0];
                 B = s.keep[1];
                 Cc = s.ext[0];
                 sn = 255;
+                lst = s.klist[0];
+                cnt = s.kcnt[0];
             }
-            const float vv = B[r];
-            if (!(vv >= ef) || !strict_max3(A, B, Cc, r, vv)) continue;
             const int sc = (sn + kM / 2) & (kM - 1);
-            const int sl = atomicAdd(&s.tcnt, 1);
-            if (sl < kTileList) s.tl[sl] = make_key(vv, (uint32_t)(r * kM + sc));
+            const int lim = cnt < 0 ? kN : cnt;
+            for (int i = lane; i < lim; i += 32) {
+                const int r = cnt < 0 ? i : (int)lst[i];
+                const float vv = B[r];
+                if (!(vv >= ef) || !strict_max3(A, B, Cc, r, vv)) continue;
+                const int sl = atomicAdd(&s.tcnt, 1);
+                if (sl < kTileList) s.tl[sl] = make_key(vv, (uint32_t)(r * kM + sc));
+            }
         }
         __syncthreads();
         // per-CTA top-K of the frame's candidates (> kTileList strict maxima above eta in one
