@@ -171,6 +171,104 @@ def run_reference(args, cfg, rank: int):
     print(json.dumps(out), flush=True)
 
 
+def extra_configs(args, dev, local, threads):
+    """Per-config GPU throughput next to the reference CPU implementation (bounded samples).
+    Not part of `value`; reported under "configs" in the JSON line."""
+    import torch
+
+    import oracle as O
+    from paper_2209_03883_b200 import configs, gen
+    from paper_2209_03883_b200.receiver import Receiver
+
+    out = {}
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    def ref_rate(cfg, fb, frames):
+        if not O.ref_available():
+            return None
+        R = O.ref()
+        K = cfg.max_targets
+        d = np.zeros((frames, K), np.int64)
+        v = np.zeros((frames, K), np.int64)
+        w = np.zeros((frames, K))
+        cnt = np.zeros(frames, np.int64)
+        kf = np.ascontiguousarray(fb.n_targets[:frames], np.int32)
+        t0 = time.perf_counter()
+        R.ref_receive_batch(cfg.n, cfg.m, cfg.n_prime, cfg.m_prime, cfg.estimator, cfg.n_cp, cfg.window, cfg.pfa,
+                            np.ascontiguousarray(fb.y[:frames]).ctypes.data,
+                            np.ascontiguousarray(fb.x[:frames]).ctypes.data,
+                            np.ascontiguousarray(fb.sigma2[:frames]).ctypes.data, frames, kf.ctypes.data, K,
+                            d.ctypes.data, v.ctypes.data, w.ctypes.data, cnt.ctypes.data, threads)
+        return frames / (time.perf_counter() - t0)
+
+    def pipeline_cfg(cfg, pool_n, frames, reps, cpu_frames):
+        fb = gen.frames(cfg, 0, pool_n)
+        reps_t = -(-frames // pool_n)
+        y = torch.from_numpy(fb.y).to(dev).repeat(reps_t, 1, 1)[:frames].contiguous()
+        x = torch.from_numpy(fb.x).to(dev).repeat(reps_t, 1, 1)[:frames].contiguous()
+        s2 = torch.from_numpy(np.tile(fb.sigma2, reps_t)[:frames]).to(dev)
+        kf = torch.from_numpy(np.tile(fb.n_targets, reps_t)[:frames].astype(np.int32)).to(dev) \
+            if cfg.per_frame_k else None
+        rx = Receiver.from_config(cfg, device=local)
+        dets = rx._dets(frames)
+        ms = timed(lambda: (rx._stream(), rx.pipeline_raw(y, x, s2, kf, dets, frames)), reps)
+        rx.close()
+        del y, x
+        r = {"frames": frames, "gpu_frames_per_s": frames / (ms / 1e3), "gpu_ms_per_batch": ms,
+             "window": "hamming" if cfg.window else "rectangular", "estimator": "dft-ce" if cfg.estimator else "ls"}
+        cr = ref_rate(cfg, fb, min(cpu_frames, pool_n))
+        if cr:
+            r["cpu_reference_frames_per_s"] = cr
+            r["cpu_threads"] = threads
+        return r
+
+    out["cfg0"] = pipeline_cfg(configs.CFG0, 1, 1, 20, 1)
+    out["cfg0"]["latency_ms"] = out["cfg0"]["gpu_ms_per_batch"]
+    out["cfg1"] = pipeline_cfg(configs.CFG1, 64, 64, 10, 64)
+    out["cfg4_rect_window"] = pipeline_cfg(configs.CFG4.replace(window=0, frames=8192), 64, 8192, 3, 64)
+    out["cfg2"] = pipeline_cfg(configs.CFG2, 8, 256, 2, 8)
+    # cfg3: FPS-SFT on 1024 x 1024 on-grid sparse grids
+    c3 = configs.CFG3
+    h, s2, _, _ = gen.sparse_frames(c3.n, c3.m, c3.targets, c3.snr_db, c3.base_seed, 0, 64)
+    seeds = np.array([gen.derive_seed(c3.base_seed + f, 0x736674) for f in range(c3.frames)], np.uint64)
+    s2t = np.tile(s2, c3.frames // 64)
+    hd = torch.from_numpy(h).to(dev).repeat(c3.frames // 64, 1, 1).contiguous()
+    rx = Receiver(16, 16, device=local)
+    ms = timed(lambda: rx.sft(hd, seeds, s2t, i_max=c3.i_max, pfa=c3.pfa, decimation=c3.decimation), 3)
+    r3 = {"frames": c3.frames, "gpu_frames_per_s": c3.frames / (ms / 1e3), "gpu_ms_per_batch": ms,
+          "note": "includes the host-side slope/offset draws and the per-call overflow check"}
+    if O.ref_available():
+        R = O.ref()
+        n = min(64, 4 * threads)
+        ME = 64
+        k = np.zeros((n, ME), np.int64)
+        l = np.zeros((n, ME), np.int64)
+        ar = np.zeros((n, ME))
+        ai = np.zeros((n, ME))
+        ne = np.zeros(n, np.int64)
+        hh = np.ascontiguousarray(h[:n])
+        t0 = time.perf_counter()
+        R.ref_sft_batch_c64(hh.ctypes.data, c3.n, c3.m, n, c3.i_max, np.ascontiguousarray(seeds[:n]).ctypes.data,
+                            np.ascontiguousarray(s2[:n]).ctypes.data, c3.pfa, c3.decimation, ME, k.ctypes.data,
+                            l.ctypes.data, ar.ctypes.data, ai.ctypes.data, ne.ctypes.data, threads)
+        r3["cpu_reference_frames_per_s"] = n / (time.perf_counter() - t0)
+        r3["cpu_threads"] = threads
+    out["cfg3_fps_sft"] = r3
+    del hd
+    rx.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -183,6 +281,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-periodogram", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the per-config (cfg0-3) measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -383,6 +482,13 @@ def main():
                "sample": f"{sample} distinct cfg4 frames x {reps_c} repeats (median), one frame per host thread; "
                          "reference sources + substitute FFT (FFTW3 absent)"}
 
+    configs_out = None
+    if not args.no_extra and rank == 0 and world == 1:
+        try:
+            configs_out = extra_configs(args, dev, local, os.cpu_count() or 1)
+        except Exception as exc:  # the headline number must not depend on the extras
+            configs_out = {"error": repr(exc)}
+
     if rank == 0:
         out = {
             "metric": "range-Doppler frames/sec (1024x256 c64)", "value": value, "unit": "frames/s",
@@ -395,7 +501,7 @@ def main():
                        "frames": F, "frames_per_rank": nf, "parallelism": f"frame-shard x{world}",
                        "l2": "inputs larger than L2 (32 GiB resident, no reuse between steps)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "periodogram_2d": periodogram,
+            "periodogram_2d": periodogram, "configs": configs_out,
         }
         print(json.dumps(out), flush=True)
     rx.close()
