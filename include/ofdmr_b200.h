@@ -119,6 +119,13 @@ int ofdmr_extract_peaks(ofdmr_context* ctx, const float* p, const double* eta, c
 int ofdmr_pipeline(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
                    const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
                    int32_t* counts, double* sigma2_h_out, float* p_out, int32_t* status, int64_t frames);
+/* Status bit 1 (value 2) after ofdmr_pipeline: the fused fast path kept at most 1024
+ * strict local maxima above eta per half-frame and this frame had more (only when sigma2
+ * is mis-set far below the noise floor); recompute such frames with this entry point,
+ * which always takes the chunked two-pass path (exact for any candidate count). */
+int ofdmr_pipeline_general(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
+                           const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
+                           int32_t* counts, double* sigma2_h_out, float* p_out, int32_t* status, int64_t frames);
 /* Same on HOST buffers (pinned recommended): copies inside, double-buffered, synchronous.
  * Returns OFDMR_ERR_CONFIG if any frame had a zero X cell. */
 int ofdmr_pipeline_host(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,

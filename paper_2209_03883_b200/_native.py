@@ -98,6 +98,7 @@ RECEIVER_SYMBOLS = [
     ("ofdmr_detect", i32, [vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_extract_peaks", i32, [vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
+    ("ofdmr_pipeline_general", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_host", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_sft", i32, [vp, vp, i32, i32, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
 ]

@@ -120,6 +120,7 @@ struct ofdmr_context {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool fast = false;           // N = N' = 1024, M = M' = 256 specialised kernels
     bool fused = false;          // + DFT-CE with 0 < L <= 128: persistent one-frame-per-CTA kernel
+    bool force_general = false;  // set by ofdmr_pipeline_general for one call
     int fused_grid = 0;
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
     // persistent periodogram / LS pipeline (fast shapes): L2-sized ring of intermediates
@@ -934,7 +935,7 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
     const size_t pframe = size_t(g.n_prime) * size_t(g.m_prime);
     const int K = g.max_targets;
     if (status) OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
-    if (c->fused && p_out == nullptr) {
+    if (c->fused && p_out == nullptr && !c->force_general) {
         // one persistent launch over the whole batch
         FusedArgs fa{};
         fa.y = static_cast<const float2*>(y);
@@ -1024,6 +1025,16 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
     return OFDMR_OK;
 }
 
+int ofdmr_pipeline_general(ofdmr_context* c, const void* y, const void* x, const double* sigma2, const int32_t* kpf,
+                           int32_t* d, int32_t* dp, float* pw, int32_t* cnt, double* s2h_out, float* p_out,
+                           int32_t* status, int64_t frames) {
+    if (!c) return fail(OFDMR_ERR_CONFIG, "pipeline_general: null context");
+    c->force_general = true;
+    const int rc = ofdmr_pipeline(c, y, x, sigma2, kpf, d, dp, pw, cnt, s2h_out, p_out, status, frames);
+    c->force_general = false;
+    return rc;
+}
+
 int ofdmr_pipeline_host(ofdmr_context* c, const void* y, const void* x, const double* sigma2, const int32_t* kpf,
                         int32_t* d, int32_t* dp, float* pw, int32_t* cnt, int64_t frames) {
     if (!c || !y || !x || !sigma2 || !d || !dp || !pw || !cnt)
@@ -1082,7 +1093,26 @@ int ofdmr_pipeline_host(ofdmr_context* c, const void* y, const void* x, const do
         OFDMR_CUDA(cudaMemcpyAsync(c->host_st, c->dev_st[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, c->stream));
         OFDMR_CUDA(cudaEventRecord(c->ev_done[b], c->stream));
         OFDMR_CUDA(cudaStreamSynchronize(c->stream));  // host_st is single-buffered
-        for (int64_t i = 0; i < nf; ++i) zero_cell |= (c->host_st[i] & 1) != 0;
+        bool overflow = false;
+        for (int64_t i = 0; i < nf; ++i) {
+            zero_cell |= (c->host_st[i] & 1) != 0;
+            overflow |= (c->host_st[i] & 2) != 0;
+        }
+        if (overflow) {  // > 1024 strict maxima above eta in a half-frame: exact general path
+            int rc2 = ofdmr_pipeline_general(c, c->dev_y[b], c->dev_x[b], c->dev_s2[b], kpf ? c->dev_k[b] : nullptr,
+                                             c->dev_d[b], c->dev_dp[b], c->dev_pw[b], c->dev_cnt[b], nullptr, nullptr,
+                                             c->dev_st[b], nf);
+            if (rc2) return rc2;
+            OFDMR_CUDA(cudaMemcpyAsync(d + size_t(K) * f0, c->dev_d[b], sizeof(int32_t) * K * nf,
+                                       cudaMemcpyDeviceToHost, c->stream));
+            OFDMR_CUDA(cudaMemcpyAsync(dp + size_t(K) * f0, c->dev_dp[b], sizeof(int32_t) * K * nf,
+                                       cudaMemcpyDeviceToHost, c->stream));
+            OFDMR_CUDA(cudaMemcpyAsync(pw + size_t(K) * f0, c->dev_pw[b], sizeof(float) * K * nf,
+                                       cudaMemcpyDeviceToHost, c->stream));
+            OFDMR_CUDA(cudaMemcpyAsync(cnt + f0, c->dev_cnt[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
+                                       c->stream));
+            OFDMR_CUDA(cudaStreamSynchronize(c->stream));
+        }
     }
     OFDMR_CUDA(cudaStreamSynchronize(c->stream));
     if (zero_cell) return fail(OFDMR_ERR_CONFIG, "spectral_division: zero cell in X");

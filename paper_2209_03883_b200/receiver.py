@@ -322,6 +322,24 @@ class Receiver:
                                         st.data_ptr(), F))
         if check:
             self._raise_status(st)
+            over = torch.nonzero(st & 2).flatten()
+            if over.numel():
+                # candidate-list overflow on the fused path: recompute those frames exactly
+                idx = over
+                sub = self._dets(idx.numel())
+                sub.sigma2_h = torch.empty(idx.numel(), dtype=torch.float64, device=self.device)
+                ys, xs, ss = y[idx].contiguous(), x[idx].contiguous(), s2[idx].contiguous()
+                ks = k[idx].contiguous() if k is not None else None
+                st2 = torch.empty(idx.numel(), dtype=torch.int32, device=self.device)
+                _check(self._lib.ofdmr_pipeline_general(
+                    self._h, ys.data_ptr(), xs.data_ptr(), ss.data_ptr(), ks.data_ptr() if ks is not None else None,
+                    sub.delay_bin.data_ptr(), sub.doppler_bin.data_ptr(), sub.peak_power.data_ptr(),
+                    sub.counts.data_ptr(), sub.sigma2_h.data_ptr(), None, st2.data_ptr(), idx.numel()))
+                d.delay_bin[idx] = sub.delay_bin
+                d.doppler_bin[idx] = sub.doppler_bin
+                d.peak_power[idx] = sub.peak_power
+                d.counts[idx] = sub.counts
+                d.sigma2_h[idx] = sub.sigma2_h
         return d, pmap
 
     def pipeline_raw(self, y: torch.Tensor, x: torch.Tensor, s2: torch.Tensor, k: torch.Tensor | None,

@@ -236,3 +236,22 @@ def test_cpp_shim_against_reference_sources(cuda):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_fused_candidate_overflow_recomputed_exactly(cuda):
+    """sigma2 far below the noise floor puts eta near 0, so almost every strict local
+    maximum is a candidate (> 1024 per half-frame): the fused kernel flags status bit 1 and
+    the wrapper recomputes on the general path; results must still match the oracle."""
+    cfg = configs.CFG1.replace(max_targets=8)
+    fb = gen.frames(cfg, 0, 3)
+    s2 = np.full(3, 1e-12)
+    with Receiver.from_config(cfg) as rx:
+        dets, _ = rx.pipeline(fb.y, fb.x, s2)
+        torch.cuda.synchronize()
+        hd, hv, hp, hc = rx.pipeline_host(fb.y, fb.x, s2)
+    rc = _rc(cfg)
+    for f in range(3):
+        ref, _, eta, ref_map = O.receive_frame(rc, fb.y[f], fb.x[f], 1e-12, 8, want_map=True)
+        got = dets.frame(f)
+        assert classify(got, ref, ref_map, eta, 8) != "fail", (got, ref)
+        assert [(int(a), int(b)) for a, b in zip(hd[f][: hc[f]], hv[f][: hc[f]])] == [(a, b) for a, b, _ in got]
