@@ -24,6 +24,10 @@
 
 namespace ofdmr {
 
+#ifndef A_BATCHES
+#define A_BATCHES 8  // pass-A tile load batches (16 / A_BATCHES float4 per array per batch; 8 measured best)
+#endif
+
 #ifdef OFDMR_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[16];
 #define PH_INIT() long long _ph_t = clock64();
@@ -198,11 +202,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         const int c0 = 16 * u + 8 * rank;
         float inv_tile = 0.f;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            float4 yv[8], xv[8];
+        for (int half = 0; half < A_BATCHES; ++half) {
+            constexpr int QB = 16 / A_BATCHES;
+            float4 yv[QB], xv[QB];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int idx = tid + (half * 8 + q) * 256;
+            for (int q = 0; q < QB; ++q) {
+                const int idx = tid + (half * QB + q) * 256;
                 const size_t off = fbase + (size_t)(idx >> 2) * kM + c0 + (idx & 3) * 2;
                 if (a.dbg & 1) {
                     yv[q] = make_float4(1.f, 0.f, 1.f, 0.f);
@@ -213,8 +218,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 }
             }
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int idx = tid + (half * 8 + q) * 256;
+            for (int q = 0; q < QB; ++q) {
+                const int idx = tid + (half * QB + q) * 256;
                 const int k = idx >> 2, c = (idx & 3) * 2;
                 const float4 y4 = yv[q], x4 = xv[q];
                 if (a.dbg & 2) {
