@@ -11,6 +11,7 @@
 #include "../../include/ofdmr_b200.h"
 #include "radar_kernels.cuh"
 #include "sft_kernels.cuh"
+#include "fused_args.cuh"
 
 namespace ofdmr {
 cudaError_t launch_colpass(const ColArgs& a, int n, int np, int frames, cudaStream_t st);
@@ -43,30 +44,7 @@ struct PersistArgs {
     int* done_rows;
 };
 cudaError_t launch_pgram_persist(const PersistArgs& pa, bool ls, bool win, int grid, cudaStream_t st);
-struct FusedArgs {
-    const float2* y;
-    const float2* x;
-    const double* sigma2;
-    const int32_t* k_per_frame;
-    int32_t* det_delay;
-    int32_t* det_doppler;
-    float* det_power;
-    int32_t* counts;
-    double* s2h_out;
-    int32_t* status;
-    const float* wk;
-    const float* wl;
-    const float2* tw1024_t;
-    const float2* tw256_t;
-    float2* dscratch;
-    int frames;
-    int L;
-    int kmax;
-    double log_pfa, power_factor, inv_count;
-    float scale;
-    long long stagger_ns;
-    int dbg;
-};
+
 cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
 cudaError_t launch_fused_ws(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
 }  // namespace ofdmr
@@ -123,6 +101,9 @@ struct ofdmr_context {
     bool force_general = false;  // set by ofdmr_pipeline_general for one call
     int fused_grid = 0;
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
+    float* fedges = nullptr;               // fused: per-CTA edge columns of P (16 steps x 2)
+    unsigned long long* fpend = nullptr;   // fused: per-CTA pending edge candidates
+    int* fpend_loc = nullptr;
     // persistent periodogram / LS pipeline (fast shapes): L2-sized ring of intermediates
     struct Persist {
         int cf = 8, ring = 4, grid = 0;
@@ -614,6 +595,9 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         c->fused_grid = 2 * sms;  // 2 resident CTAs per SM (128 regs x 256 threads, ~102 KB smem)
         // two frames in flight per 2-CTA cluster (pass A of frame i+1 overlaps pass C of frame i)
         if (e == cudaSuccess) e = cudaMalloc(&c->dscratch, sizeof(float2) * 128 * 256 * size_t(c->fused_grid));
+        if (e == cudaSuccess) e = cudaMalloc(&c->fedges, sizeof(float) * 16 * 2 * 1024 * size_t(c->fused_grid));
+        if (e == cudaSuccess) e = cudaMalloc(&c->fpend, sizeof(unsigned long long) * kFusedPend * size_t(c->fused_grid));
+        if (e == cudaSuccess) e = cudaMalloc(&c->fpend_loc, sizeof(int) * kFusedPend * size_t(c->fused_grid));
     }
     c->gbuf = c->slot[0].gbuf;
     c->partial = c->slot[0].partial;
@@ -643,6 +627,9 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->tw1024_t);
     cudaFree(c->tw256_t);
     cudaFree(c->dscratch);
+    cudaFree(c->fedges);
+    cudaFree(c->fpend);
+    cudaFree(c->fpend_loc);
     cudaFree(c->ps.gring);
     cudaFree(c->ps.pring);
     cudaFree(c->ps.cring);
@@ -960,12 +947,9 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
         fa.power_factor = c->pf;
         fa.inv_count = c->inv_count;
         fa.scale = c->scale;
-        {
-            const char* st = getenv("OFDMR_STAGGER_NS");
-            fa.stagger_ns = st ? atoll(st) : 0;
-            const char* dbg = getenv("OFDMR_FUSED_DBG");
-            fa.dbg = dbg ? atoi(dbg) : 0;
-        }
+        fa.edges = c->fedges;
+        fa.pend = c->fpend;
+        fa.pend_loc = c->fpend_loc;
         for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
             const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);
             fa.frames = int(nf);

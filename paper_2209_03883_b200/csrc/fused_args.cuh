@@ -1,0 +1,37 @@
+// Launch arguments of the fused DFT-CE receiver kernels (fused_ce.cu, fused_ws.cu), shared
+// with the host dispatcher (capi.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ofdmr {
+
+struct FusedArgs {
+    const float2* y;
+    const float2* x;
+    const double* sigma2;
+    const int32_t* k_per_frame;
+    int32_t* det_delay;
+    int32_t* det_doppler;
+    float* det_power;
+    int32_t* counts;
+    double* s2h_out;
+    int32_t* status;
+    const float* wk;           // null for rectangular
+    const float* wl;
+    const float2* tw1024_t;
+    const float2* tw256_t;
+    float2* dscratch;          // per cluster [2][128 * 256] compressed D (double-buffered)
+    float* edges;              // per cluster [2 ranks][16 steps][2 edges][1024] P edge columns
+    unsigned long long* pend;  // per cluster [2 ranks][kFusedPend] edge candidates
+    int* pend_loc;             // per cluster [2 ranks][kFusedPend] partner edge-column locator
+    int frames;
+    int L;
+    int kmax;
+    double log_pfa, power_factor, inv_count;
+    float scale;
+};
+
+constexpr int kFusedPend = 2048;  // pending edge candidates per CTA per frame
+
+}  // namespace ofdmr

@@ -21,6 +21,7 @@
 
 #include "radar_kernels.cuh"
 #include "warp_fft.cuh"
+#include "fused_args.cuh"
 
 namespace ofdmr {
 
@@ -44,30 +45,7 @@ __device__ unsigned long long g_phase_cycles[16];
 #define PH(i)
 #endif
 
-struct FusedArgs {
-    const float2* y;
-    const float2* x;
-    const double* sigma2;
-    const int32_t* k_per_frame;
-    int32_t* det_delay;
-    int32_t* det_doppler;
-    float* det_power;
-    int32_t* counts;
-    double* s2h_out;
-    int32_t* status;
-    const float* wk;           // null for rectangular
-    const float* wl;
-    const float2* tw1024_t;
-    const float2* tw256_t;
-    float2* dscratch;          // [gridDim.x][128 * 256]
-    int frames;
-    int L;
-    int kmax;
-    double log_pfa, power_factor, inv_count;
-    float scale;
-    long long stagger_ns;      // unused (kept for ABI of the debug build)
-    int dbg;                   // debug switches (experiments only): 1 = no A loads, 2 = no LS math
-};
+
 
 namespace {
 
@@ -80,26 +58,16 @@ struct FusedSmem {
     float2 tw[1024];
     float2 tw256[256];
     float2 cols[8 * kVS];         // per-warp column buffers / pass-A,C tiles / pass-B scratch
-    float keep[4][kN];            // rank 1: previous step's columns 6, 7; rank 0: frame columns 0, 1 (2, 3)
-    float ext[2][kN];             // partner columns staged for this step's detection
     unsigned long long tl[kTileList];  // per-frame candidate list (strict maxima >= eta)
     unsigned long long run[kMaxK];     // per-CTA top-K (descending, 0-padded)
     unsigned long long cand2[kMaxK];
     unsigned long long sbest[8];
     int sidx[8];
-    const float* dA[10];               // per-step detection descriptors (uniform across the CTA)
-    const float* dB[10];
-    const float* dC[10];
-    const unsigned short* dL[10];      // candidate rows of the tested column (P >= eta)
-    int dN[10];                        // their count (-1: list overflowed -> scan the column)
-    int dsn[10];
-    int dcnt;
     unsigned short clist[8][64];       // per-column candidate rows of the current step
     int ccnt[8];
-    unsigned short klist[2][64];       // kept lists: [0] rank 1 previous column 7, [1] rank 0 column 0
-    int kcnt[2];
     double red[8];
     int tcnt;
+    int pcnt;                          // pending edge candidates of the frame (global scratch)
     int zc_part;
     int overflow;
     int zcs[2];
@@ -148,21 +116,12 @@ __device__ void warp_merge_topk(unsigned long long* run, unsigned long long* tl,
 
 // Pull the 128-B lines of one 8-column tile (1024 rows of Y and x_tx) into L2 so the next
 // tile's loads hit L2 while this tile computes (the pair covers both 64-B halves of a line).
-__device__ __forceinline__ void prefetch_tile(const float2* y, const float2* x, size_t fbase, int c0, int mode) {
-    if (mode == 1) return;
+__device__ __forceinline__ void prefetch_tile(const float2* y, const float2* x, size_t fbase, int c0) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const size_t off = fbase + (size_t)(threadIdx.x + 256 * j) * kM + c0;
-        if (mode == 2) {
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(y + off));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(x + off));
-        } else if (mode == 3) {
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(y + off) : "memory");
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(x + off) : "memory");
-        } else {
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(y + off));
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(x + off));
-        }
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(y + off));
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(x + off));
     }
 }
 
@@ -209,25 +168,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             for (int q = 0; q < QB; ++q) {
                 const int idx = tid + (half * QB + q) * 256;
                 const size_t off = fbase + (size_t)(idx >> 2) * kM + c0 + (idx & 3) * 2;
-                if (a.dbg & 1) {
-                    yv[q] = make_float4(1.f, 0.f, 1.f, 0.f);
-                    xv[q] = make_float4(1.f, 0.f, 1.f, 0.f);
-                } else {
-                    yv[q] = __ldcs(reinterpret_cast<const float4*>(a.y + off));
-                    xv[q] = __ldcs(reinterpret_cast<const float4*>(a.x + off));
-                }
+                yv[q] = __ldcs(reinterpret_cast<const float4*>(a.y + off));
+                xv[q] = __ldcs(reinterpret_cast<const float4*>(a.x + off));
             }
 #pragma unroll
             for (int q = 0; q < QB; ++q) {
                 const int idx = tid + (half * QB + q) * 256;
                 const int k = idx >> 2, c = (idx & 3) * 2;
                 const float4 y4 = yv[q], x4 = xv[q];
-                if (a.dbg & 2) {
-                    const int pk = k + (k >> 5);
-                    s.cols[c * kVS + pk] = make_float2(y4.x, y4.y);
-                    s.cols[(c + 1) * kVS + pk] = make_float2(y4.z, y4.w);
-                    continue;
-                }
+
                 const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
                 const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
                 zero_cell |= (n0 == 0.f) | (n1 == 0.f);
@@ -245,8 +194,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         __syncthreads();
         PH(0);
         // stream the next tile into L2 while this one computes (one step ahead)
-        if (u < 15) prefetch_tile(a.y, a.x, fbase, c0 + 16, (a.dbg >> 2) & 3);
-        else if (f + ncl < a.frames) prefetch_tile(a.y, a.x, (size_t)(f + ncl) * kN * kM, 8 * rank, (a.dbg >> 2) & 3);
+        if (u < 15) prefetch_tile(a.y, a.x, fbase, c0 + 16);
+        else if (f + ncl < a.frames) prefetch_tile(a.y, a.x, (size_t)(f + ncl) * kN * kM, 8 * rank);
         {
             float2* col = s.cols + w * kVS;
             float2 v[32];
@@ -336,6 +285,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     };
 
     // ---------------------------------------------------------------- pass C, one step
+    // Pass C, one step.  Columns 1..6 of the tile are tested locally; the tile's edge
+    // columns 0 and 7 are pre-tested against their own side here and finished at the end of
+    // the frame against the partner's stored edge columns, so no cluster barrier is needed
+    // inside the step loop.
+    float* my_edges = a.edges + ((size_t)cid * 2 + rank) * 16 * 2 * kN;
+    const float* partner_edges = a.edges + ((size_t)cid * 2 + (rank ^ 1)) * 16 * 2 * kN;
+    unsigned long long* my_pend = a.pend + ((size_t)cid * 2 + rank) * kFusedPend;
+    int* my_ploc = a.pend_loc + ((size_t)cid * 2 + rank) * kFusedPend;
     auto C_tile = [&](int u, const float2* dsc, float ef) {
         const int c0 = 16 * u + 8 * rank;
         if (tid < 8) s.ccnt[tid] = 0;
@@ -386,131 +343,83 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         }
         __syncthreads();
         PH(6);
-        cluster.sync();  // both halves' P columns (and the partner's kept columns) ready
         {
-            const float* pb = reinterpret_cast<const float*>(p.cols);
-            for (int r = tid; r < kN; r += 256) {
-                if (rank == 0) {
-                    s.ext[0][r] = p.keep[1][r];           // column 16u-1 (partner's previous last)
-                    s.ext[1][r] = pb[r];                  // column 16u+8 (partner's first)
-                } else {
-                    s.ext[0][r] = pb[7 * (2 * kVS) + r];  // column 16u+7 (partner's last)
-                    s.ext[1][r] = pb[r];                  // column 16u   (partner's first)
-                }
-            }
-        }
-        if (tid == 0) {
-            // rank 0: 16u..16u+7 (16u skipped at u = 0, done at the wrap)
-            // rank 1: 16u+8..16u+14 and its deferred 16u-1 (u >= 1); 16u+15 waits a step
-            int n = 0;
-            for (int jdx = 0; jdx < 8; ++jdx) {
-                if (rank == 0) {
-                    if (u == 0 && jdx == 0) continue;
-                    s.dA[n] = jdx == 0 ? s.ext[0] : lcol(jdx - 1);
-                    s.dC[n] = jdx == 7 ? s.ext[1] : lcol(jdx + 1);
-                } else {
-                    if (jdx == 7) continue;
-                    s.dA[n] = jdx == 0 ? s.ext[0] : lcol(jdx - 1);
-                    s.dC[n] = lcol(jdx + 1);
-                }
-                s.dB[n] = lcol(jdx);
-                s.dL[n] = s.clist[jdx];
-                s.dN[n] = s.ccnt[jdx] > 64 ? -1 : s.ccnt[jdx];
-                s.dsn[n] = c0 + jdx;
-                ++n;
-            }
-            if (rank == 1 && u > 0) {
-                s.dA[n] = s.keep[0];
-                s.dB[n] = s.keep[1];
-                s.dC[n] = s.ext[1];
-                s.dL[n] = s.klist[0];
-                s.dN[n] = s.kcnt[0];
-                s.dsn[n] = c0 - 9;
-                ++n;
-            }
-            s.dcnt = n;
-        }
-        cluster.sync();  // partner done reading our columns / kept columns; table visible
-        PH(7);
-        const int dcnt = (a.dbg & 32) ? 0 : s.dcnt;
-        for (int e = w; e < dcnt; e += 8) {
-            const float* A = s.dA[e];
-            const float* B = s.dB[e];
-            const float* Cc = s.dC[e];
-            const int sc = (s.dsn[e] + kM / 2) & (kM - 1);
-            const int cnt = s.dN[e];
-            const int lim = cnt < 0 ? kN : cnt;  // overflowed list: scan every row
+            // warp w tests tile column w: interior columns completely, edge columns (0, 7)
+            // against their own-side neighbours only (-> pending, finished at frame end)
+            const float* pb = reinterpret_cast<const float*>(s.cols);
+            const int jdx = w;
+            const float* B = pb + jdx * (2 * kVS);
+            const float* A = jdx > 0 ? pb + (jdx - 1) * (2 * kVS) : nullptr;
+            const float* Cc = jdx < 7 ? pb + (jdx + 1) * (2 * kVS) : nullptr;
+            const int sn = c0 + jdx;
+            const int sc = (sn + kM / 2) & (kM - 1);
+            const int cnt = s.ccnt[jdx];
+            const int lim = cnt > 64 ? kN : cnt;  // overflowed list: scan every row
             for (int i = lane; i < lim; i += 32) {
-                const int r = cnt < 0 ? i : (int)s.dL[e][i];
+                const int r = cnt > 64 ? i : (int)s.clist[jdx][i];
                 const float vv = B[r];
-                if (vv >= ef && strict_max3(A, B, Cc, r, vv)) {
+                if (!(vv >= ef)) continue;
+                const int ru = (r - 1) & (kN - 1), rd = (r + 1) & (kN - 1);
+                if (B[ru] >= vv || B[rd] >= vv) continue;
+                if (A && (A[ru] >= vv || A[r] >= vv || A[rd] >= vv)) continue;
+                if (Cc && (Cc[ru] >= vv || Cc[r] >= vv || Cc[rd] >= vv)) continue;
+                const unsigned long long key = make_key(vv, (uint32_t)(r * kM + sc));
+                if (A && Cc) {
                     const int slot = atomicAdd(&s.tcnt, 1);
-                    if (slot < kTileList) s.tl[slot] = make_key(vv, (uint32_t)(r * kM + sc));
+                    if (slot < kTileList) s.tl[slot] = key;
+                } else {
+                    // partner edge column holding the missing neighbour: (partner step, edge)
+                    int pu, pe;
+                    if (rank == 0) {
+                        if (jdx == 0) { pu = (u + 15) & 15; pe = 1; }   // 16u-1: partner step u-1, col 7
+                        else { pu = u; pe = 0; }                        // 16u+8: partner step u, col 0
+                    } else {
+                        if (jdx == 0) { pu = u; pe = 1; }               // 16u+7: partner step u, col 7
+                        else { pu = (u + 1) & 15; pe = 0; }             // 16u+16: partner step u+1, col 0
+                    }
+                    const int slot = atomicAdd(&s.pcnt, 1);
+                    if (slot < kFusedPend) {
+                        my_pend[slot] = key;
+                        my_ploc[slot] = pu * 2 + pe;
+                    }
                 }
+            }
+        }
+        // this step's edge columns for the partner's end-of-frame tests
+        {
+            const float* pb = reinterpret_cast<const float*>(s.cols);
+            for (int i = tid; i < 2 * kN; i += 256) {
+                const int e = i >> 10, r = i & (kN - 1);
+                __stcg(my_edges + ((size_t)u * 2 + e) * kN + r, pb[(e ? 7 : 0) * (2 * kVS) + r]);
             }
         }
         __syncthreads();
         PH(8);
-        for (int r = tid; r < kN; r += 256) {
-            if (rank == 1) {
-                s.keep[0][r] = lcol(6)[r];
-                s.keep[1][r] = lcol(7)[r];
-            } else if (u == 0) {
-                s.keep[2][r] = lcol(0)[r];
-                s.keep[3][r] = lcol(1)[r];
-            }
-        }
-        {
-            const int kc = rank == 1 ? 7 : 0;
-            const int kk = rank == 1 ? 0 : 1;
-            if (rank == 1 || u == 0) {
-                if (tid < 64) s.klist[kk][tid] = s.clist[kc][tid];
-                if (tid == 0) s.kcnt[kk] = s.ccnt[kc] > 64 ? -1 : s.ccnt[kc];
-            }
-        }
-        __syncthreads();
-        PH(9);
     };
 
     // ---------------------------------------------------------------- end of pass C
     auto C_finish = [&](int f, int slot, float ef) {
-        // wrap: rank 0 tests column 0 (needs 255 = partner keep[1], and 1); rank 1 tests 255
-        cluster.sync();
-        for (int r = tid; r < kN; r += 256) s.ext[0][r] = rank == 0 ? p.keep[1][r] : p.keep[2][r];
-        cluster.sync();
-        if (w == 0) {
-            const float *A, *B, *Cc;
-            int sn, cnt;
-            const unsigned short* lst;
-            if (rank == 0) {
-                A = s.ext[0];
-                B = s.keep[2];
-                Cc = s.keep[3];
-                sn = 0;
-                lst = s.klist[1];
-                cnt = s.kcnt[1];
-            } else {
-                A = s.keep[0];
-                B = s.keep[1];
-                Cc = s.ext[0];
-                sn = 255;
-                lst = s.klist[0];
-                cnt = s.kcnt[0];
-            }
-            const int sc = (sn + kM / 2) & (kM - 1);
-            const int lim = cnt < 0 ? kN : cnt;
-            for (int i = lane; i < lim; i += 32) {
-                const int r = cnt < 0 ? i : (int)lst[i];
-                const float vv = B[r];
-                if (!(vv >= ef) || !strict_max3(A, B, Cc, r, vv)) continue;
-                const int sl = atomicAdd(&s.tcnt, 1);
-                if (sl < kTileList) s.tl[sl] = make_key(vv, (uint32_t)(r * kM + sc));
-            }
+        (void)ef;
+        __threadfence();
+        cluster.sync();  // both CTAs' edge columns and pending lists are in global memory
+        PH(9);
+        const int np = min(s.pcnt, kFusedPend);
+        for (int i = tid; i < np; i += 256) {
+            const unsigned long long key = __ldcg(my_pend + i);
+            const int loc = __ldcg(my_ploc + i);
+            const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull);
+            const int r = (int)(idx >> 8);
+            const float vv = __uint_as_float((uint32_t)(key >> 32));
+            const float* col = partner_edges + (size_t)loc * kN;
+            const float n0 = __ldcg(col + ((r - 1) & (kN - 1))), n1 = __ldcg(col + r), n2 = __ldcg(col + ((r + 1) & (kN - 1)));
+            if (n0 >= vv || n1 >= vv || n2 >= vv) continue;
+            const int sl = atomicAdd(&s.tcnt, 1);
+            if (sl < kTileList) s.tl[sl] = key;
         }
         __syncthreads();
-        // per-CTA top-K of the frame's candidates (> kTileList strict maxima above eta in one
+        // per-CTA top-K of the frame's candidates (> kTileList / kFusedPend candidates in one
         // half-frame sets status bit 1 so the host recomputes the frame on the general path)
-        if (tid == 0 && s.tcnt > kTileList) s.overflow = 1;
+        if (tid == 0 && (s.tcnt > kTileList || s.pcnt > kFusedPend)) s.overflow = 1;
         block_topk<256>(s.tl, min(s.tcnt, kTileList), K, s.run, s.sbest, s.sidx);
         __syncthreads();
         cluster.sync();  // both per-CTA lists final
@@ -545,7 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 if (a.status && (s.overflow || p.overflow)) atomicOr(a.status + f, 2);
             }
         }
-        cluster.sync();  // partner's run list consumed before the next frame resets it
+        cluster.sync();  // partner's run list and edge columns consumed
         if (tid == 0) s.overflow = 0;
         PH(10);
     };
@@ -565,7 +474,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         const int fN = fC + ncl;
         const bool hasN = fN < a.frames;
         const int sc = it & 1, sn = sc ^ 1;
-        if (tid == 0) s.tcnt = 0;
+        if (tid == 0) {
+            s.tcnt = 0;
+            s.pcnt = 0;
+        }
         for (int i = tid; i < K; i += 256) s.run[i] = 0ull;
         const float ef = eta_float(s.etas[sc]);
         __syncthreads();

@@ -18,33 +18,11 @@
 
 #include "radar_kernels.cuh"
 #include "warp_fft.cuh"
+#include "fused_args.cuh"
 
 namespace ofdmr {
 
-struct FusedArgs {
-    const float2* y;
-    const float2* x;
-    const double* sigma2;
-    const int32_t* k_per_frame;
-    int32_t* det_delay;
-    int32_t* det_doppler;
-    float* det_power;
-    int32_t* counts;
-    double* s2h_out;
-    int32_t* status;
-    const float* wk;
-    const float* wl;
-    const float2* tw1024_t;
-    const float2* tw256_t;
-    float2* dscratch;
-    int frames;
-    int L;
-    int kmax;
-    double log_pfa, power_factor, inv_count;
-    float scale;
-    long long stagger_ns;
-    int dbg;
-};
+
 
 namespace {
 

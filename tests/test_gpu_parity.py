@@ -30,6 +30,12 @@ def _pipeline_parity(cfg, frames, first=0, check_map=False):
         torch.cuda.synchronize()
         pmap = pmap.cpu().numpy()
         s2h = dets.sigma2_h.cpu().numpy()
+        # production path (no map requested): the fused single-launch kernel where eligible
+        l0 = rx.launch_count
+        fdets, _ = rx.pipeline(fb.y, fb.x, fb.sigma2, k_per_frame=kf)
+        torch.cuda.synchronize()
+        if _fused_eligible(cfg):
+            assert rx.launch_count - l0 == 1, "fused kernel expected"
     rc = _rc(cfg)
     stats = {"ok": 0, "tie": 0, "fail": 0}
     for f in range(frames):
@@ -38,13 +44,18 @@ def _pipeline_parity(cfg, frames, first=0, check_map=False):
         assert abs(s2h[f] - ref_s2h) <= 1e-6 * ref_s2h
         err = np.abs(pmap[f] - ref_map).max() / ref_map.max()
         assert err <= MAP_TOL, (cfg.name, f, err)
-        got = dets.frame(f)
-        verdict = classify(got, ref, ref_map, eta, k)
-        stats[verdict] += 1
-        assert verdict != "fail", (cfg.name, f, got, ref)
-        assert powers_close(got, ref), (got, ref)
-    assert stats["tie"] <= max(1, frames // 100), stats
+        for dd in (dets, fdets):
+            got = dd.frame(f)
+            verdict = classify(got, ref, ref_map, eta, k)
+            stats[verdict] += 1
+            assert verdict != "fail", (cfg.name, f, got, ref)
+            assert powers_close(got, ref), (got, ref)
+    assert stats["tie"] <= max(2, frames // 50), stats
     return stats
+
+
+def _fused_eligible(cfg):
+    return (cfg.n, cfg.m, cfg.n_prime, cfg.m_prime) == (1024, 256, 1024, 256) and cfg.estimator == 1 and 0 < cfg.n_cp <= 128
 
 
 def test_spectral_division_and_zero_cell(cuda):
@@ -255,3 +266,48 @@ def test_fused_candidate_overflow_recomputed_exactly(cuda):
         got = dets.frame(f)
         assert classify(got, ref, ref_map, eta, 8) != "fail", (got, ref)
         assert [(int(a), int(b)) for a, b in zip(hd[f][: hc[f]], hv[f][: hc[f]])] == [(a, b) for a, b, _ in got]
+
+
+@pytest.mark.parametrize("window", [1, 0])
+def test_fused_tile_boundary_peaks(cuda, window):
+    """Targets whose periodogram peaks sit on the fused kernel's tile and CTA boundaries
+    (Doppler columns = 0, 7, 8, 15 mod 16, i.e. the columns whose 3x3 test needs the partner
+    CTA's edge columns, incl. the wrap 255 <-> 0), in adjacent pairs of near-equal power
+    one column apart, and rows shifted by -1/0/+1 so the deciding neighbour is in every
+    position of the partner column.  Fused (no map) detections must match the oracle."""
+    # K below the number of planted targets: every reported peak is a target peak (weak
+    # sidelobe/noise maxima far below the frame maximum are not resolvable to 1e-4 in fp32)
+    cfg = configs.CFG1.replace(window=window, max_targets=8, per_frame_k=False)
+    n, m = cfg.n, cfg.m
+    rng = np.random.default_rng(7)
+    frames = 12
+    x = np.exp(1j * (np.pi / 2) * rng.integers(0, 4, (frames, n, m)) + 1j * np.pi / 4).astype(np.complex64)
+    nn = np.arange(n)[:, None]
+    mm = np.arange(m)[None, :]
+    y = np.empty_like(x)
+    for f in range(frames):
+        h = np.zeros((n, m), np.complex128)
+        for j in range(10):
+            c = int(rng.choice([7, 15])) + 16 * int(rng.integers(0, 16))  # left column of the pair
+            d = int(rng.integers(2, 120))
+            for side, cc in enumerate((c, (c + 1) % m)):
+                dd = d + (int(rng.integers(-1, 2)) if side else 0)
+                amp = 1.0 + 0.02 * rng.standard_normal()
+                h += amp * np.exp(-2j * np.pi * nn * dd / n) * np.exp(2j * np.pi * mm * (cc - m // 2) / m)
+        noise = 0.05 * (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m))) / np.sqrt(2)
+        y[f] = (x[f] * h + noise).astype(np.complex64)
+    s2 = np.full(frames, 0.05 ** 2)
+    rc = _rc(cfg)
+    with Receiver.from_config(cfg) as rx:
+        l0 = rx.launch_count
+        dets, _ = rx.pipeline(y, x, s2)
+        torch.cuda.synchronize()
+        assert rx.launch_count - l0 == 1
+    hits = 0
+    for f in range(frames):
+        ref, _, eta, ref_map = O.receive_frame(rc, y[f], x[f], float(s2[f]), cfg.max_targets, want_map=True)
+        got = dets.frame(f)
+        assert classify(got, ref, ref_map, eta, cfg.max_targets) != "fail", (f, got, ref)
+        assert powers_close(got, ref)
+        hits += sum(1 for _, b, _ in ref if (b + m // 2) % 16 in (0, 7, 8, 15))
+    assert hits >= frames * 3  # the boundary columns really were exercised

@@ -12,8 +12,8 @@ os.environ.setdefault("OFDMR_LIB", os.path.join(os.path.dirname(os.path.dirname(
 from paper_2209_03883_b200 import _native, configs, gen  # noqa: E402
 from paper_2209_03883_b200.receiver import Receiver  # noqa: E402
 
-NAMES = ["A_load", "A_fft", "A_store", "A_reduce+sync", "B_rowfft", "C_load", "C_fft", "C_cluster+copy",
-         "C_detect", "C_merge+keep", "wrap+out"]
+NAMES = ["A_load", "A_fft", "A_store", "A_reduce+sync", "B_rowfft", "C_load", "C_fft", "-",
+         "C_detect+edges", "finish_sync", "resolve+topk+out"]
 cfg = configs.CFG4
 F = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 pool = gen.frames(cfg, 0, 64)
