@@ -104,6 +104,7 @@ struct ofdmr_context {
     float* fedges = nullptr;               // fused: per-CTA edge columns of P (16 steps x 2)
     unsigned long long* fpend = nullptr;   // fused: per-CTA pending edge candidates
     int* fpend_loc = nullptr;
+    unsigned long long* ftlist = nullptr;  // fused: per-CTA frame candidate list
     // persistent periodogram / LS pipeline (fast shapes): L2-sized ring of intermediates
     struct Persist {
         int cf = 8, ring = 4, grid = 0;
@@ -598,6 +599,7 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         if (e == cudaSuccess) e = cudaMalloc(&c->fedges, sizeof(float) * 16 * 2 * 1024 * size_t(c->fused_grid));
         if (e == cudaSuccess) e = cudaMalloc(&c->fpend, sizeof(unsigned long long) * kFusedPend * size_t(c->fused_grid));
         if (e == cudaSuccess) e = cudaMalloc(&c->fpend_loc, sizeof(int) * kFusedPend * size_t(c->fused_grid));
+        if (e == cudaSuccess) e = cudaMalloc(&c->ftlist, sizeof(unsigned long long) * 1024 * size_t(c->fused_grid));
     }
     c->gbuf = c->slot[0].gbuf;
     c->partial = c->slot[0].partial;
@@ -630,6 +632,7 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->fedges);
     cudaFree(c->fpend);
     cudaFree(c->fpend_loc);
+    cudaFree(c->ftlist);
     cudaFree(c->ps.gring);
     cudaFree(c->ps.pring);
     cudaFree(c->ps.cring);
@@ -950,6 +953,7 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
         fa.edges = c->fedges;
         fa.pend = c->fpend;
         fa.pend_loc = c->fpend_loc;
+        fa.tlist = c->ftlist;
         for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
             const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);
             fa.frames = int(nf);

@@ -24,7 +24,8 @@ struct FusedArgs {
     float2* dscratch;          // per cluster [2][128 * 256] compressed D (double-buffered)
     float* edges;              // per cluster [2 ranks][16 steps][2 edges][1024] P edge columns
     unsigned long long* pend;  // per cluster [2 ranks][kFusedPend] edge candidates
-    int* pend_loc;             // per cluster [2 ranks][kFusedPend] partner edge-column locator
+    int* pend_loc;
+    unsigned long long* tlist; // per CTA [kTileList] frame candidate list             // per cluster [2 ranks][kFusedPend] partner edge-column locator
     int frames;
     int L;
     int kmax;

@@ -25,9 +25,13 @@
 
 namespace ofdmr {
 
-#ifndef A_BATCHES
-#define A_BATCHES 8  // pass-A tile load batches (16 / A_BATCHES float4 per array per batch; 8 measured best)
+#ifndef PF_AHEAD
+#define PF_AHEAD 0  // L2 prefetch distance of pass-A tiles
 #endif
+#ifndef RING
+#define RING 4
+#endif
+constexpr int kRing = RING;  // pass-A cp.async staging ring depth (stages of 64 rows x 8 symbols)
 
 #ifdef OFDMR_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[16];
@@ -52,13 +56,14 @@ namespace {
 constexpr int kM = 256;
 constexpr int kN = 1024;
 constexpr int kVS = 1057;         // padded column buffer (pad_len(1024))
-constexpr int kTileList = 1024;   // per-tile candidate list (exact fallback beyond)
+constexpr int kTileList = 1024;   // per-CTA frame candidate list (exact fallback beyond)
 
 struct FusedSmem {
     float2 tw[1024];
     float2 tw256[256];
     float2 cols[8 * kVS];         // per-warp column buffers / pass-A,C tiles / pass-B scratch
-    unsigned long long tl[kTileList];  // per-frame candidate list (strict maxima >= eta)
+    float4 stg[kRing][2][256];    // pass-A staging ring: thread-private 16-B slots of Y and x_tx
+    unsigned long long prun[kMaxK];    // partner CTA's top-K (rank 0 merge)
     unsigned long long run[kMaxK];     // per-CTA top-K (descending, 0-padded)
     unsigned long long cand2[kMaxK];
     unsigned long long sbest[8];
@@ -77,11 +82,6 @@ struct FusedSmem {
 };
 
 // Strict wrapped 3x3 maximum test on P columns a, b, c (b tested) at row r.
-__device__ __forceinline__ bool strict_max3(const float* a, const float* b, const float* c, int r, float v) {
-    const int ru = (r - 1) & (kN - 1), rd = (r + 1) & (kN - 1);
-    return !(a[ru] >= v || a[r] >= v || a[rd] >= v || b[ru] >= v || b[rd] >= v || c[ru] >= v || c[r] >= v ||
-             c[rd] >= v);
-}
 
 // Warp 0: merge the tile list (cnt keys) into the running top-K (K keys, sorted desc).
 __device__ void warp_merge_topk(unsigned long long* run, unsigned long long* tl, int cnt, int K,
@@ -116,6 +116,14 @@ __device__ void warp_merge_topk(unsigned long long* run, unsigned long long* tl,
 
 // Pull the 128-B lines of one 8-column tile (1024 rows of Y and x_tx) into L2 so the next
 // tile's loads hit L2 while this tile computes (the pair covers both 64-B halves of a line).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ void prefetch_tile(const float2* y, const float2* x, size_t fbase, int c0) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -154,48 +162,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     __syncthreads();
     PH_INIT();
 
+    // pass-A input stream: cp.async ring over this CTA's linear sequence of tiles
+    // (frame cid tiles 0..15, frame cid + ncl tiles 0..15, ...); one commit group per stage
+    int ring_pos = 0;
+    auto a_issue = [&](int f, int u, int st, int slot) {
+        if (st >= 16) {
+            st -= 16;
+            if (++u == 16) {
+                u = 0;
+                f += ncl;
+            }
+        }
+        if (f < a.frames) {
+            const int idx = tid + st * 256;
+            const size_t off = (size_t)f * kN * kM + (size_t)(idx >> 2) * kM + 16 * u + 8 * rank + (idx & 3) * 2;
+            cp_async16(&s.stg[slot][0][tid], a.y + off);
+            cp_async16(&s.stg[slot][1][tid], a.x + off);
+        }
+        cp_async_commit();
+    };
+    if (cid < a.frames)
+        for (int st = 0; st < kRing; ++st) a_issue(cid, 0, st, st);
+
     // ---------------------------------------------------------------- pass A, one tile
     // column tile u (8 symbols) of frame f: LS divide -> IFFT_N -> L taps x 1/N -> D
     auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell) {
-        const size_t fbase = (size_t)f * kN * kM;
         const int c0 = 16 * u + 8 * rank;
         float inv_tile = 0.f;
-#pragma unroll
-        for (int half = 0; half < A_BATCHES; ++half) {
-            constexpr int QB = 16 / A_BATCHES;
-            float4 yv[QB], xv[QB];
-#pragma unroll
-            for (int q = 0; q < QB; ++q) {
-                const int idx = tid + (half * QB + q) * 256;
-                const size_t off = fbase + (size_t)(idx >> 2) * kM + c0 + (idx & 3) * 2;
-                yv[q] = __ldcs(reinterpret_cast<const float4*>(a.y + off));
-                xv[q] = __ldcs(reinterpret_cast<const float4*>(a.x + off));
-            }
-#pragma unroll
-            for (int q = 0; q < QB; ++q) {
-                const int idx = tid + (half * QB + q) * 256;
-                const int k = idx >> 2, c = (idx & 3) * 2;
-                const float4 y4 = yv[q], x4 = xv[q];
-
-                const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
-                const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
-                zero_cell |= (n0 == 0.f) | (n1 == 0.f);
-                const float i0 = n0 == 0.f ? 0.f : __frcp_rn(n0);
-                const float i1 = n1 == 0.f ? 0.f : __frcp_rn(n1);
-                inv_tile += i0 + i1;
-                const int pk = k + (k >> 5);
-                s.cols[c * kVS + pk] =
-                    make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
-                s.cols[(c + 1) * kVS + pk] =
-                    make_float2(fmaf(y4.z, x4.z, y4.w * x4.w) * i1, fmaf(y4.w, x4.z, -y4.z * x4.w) * i1);
-            }
+#pragma unroll 4
+        for (int st = 0; st < 16; ++st) {
+            // stage st of this tile landed in ring slot (this thread's own 16-B slots)
+            cp_async_wait<kRing - 1>();
+            const int slot = (ring_pos + st) % kRing;
+            const float4 y4 = s.stg[slot][0][tid];
+            const float4 x4 = s.stg[slot][1][tid];
+            const int idx = tid + st * 256;
+            const int k = idx >> 2, c = (idx & 3) * 2;
+            const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
+            const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
+            zero_cell |= (n0 == 0.f) | (n1 == 0.f);
+            const float i0 = n0 == 0.f ? 0.f : __frcp_rn(n0);
+            const float i1 = n1 == 0.f ? 0.f : __frcp_rn(n1);
+            inv_tile += i0 + i1;
+            const int pk = k + (k >> 5);
+            const float2 r0 = make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
+            const float2 r1 = make_float2(fmaf(y4.z, x4.z, y4.w * x4.w) * i1, fmaf(y4.w, x4.z, -y4.z * x4.w) * i1);
+            s.cols[c * kVS + pk] = r0;
+            s.cols[(c + 1) * kVS + pk] = r1;
+            // refill the slot (after its values were consumed) with the stage kRing ahead in
+            // this CTA's linear sequence of pass-A tiles
+            a_issue(f, u, st + kRing, slot);
         }
+        ring_pos = (ring_pos + 16) % kRing;
         inv_acc += (double)inv_tile;  // fp32 within a tile (32 terms), fp64 across tiles
         __syncthreads();
         PH(0);
         // stream the next tile into L2 while this one computes (one step ahead)
-        if (u < 15) prefetch_tile(a.y, a.x, fbase, c0 + 16);
-        else if (f + ncl < a.frames) prefetch_tile(a.y, a.x, (size_t)(f + ncl) * kN * kM, 8 * rank);
+        // stream tile PF_AHEAD steps ahead into L2 while this one computes
+        if (PF_AHEAD > 0) {
+            int pu = u + PF_AHEAD, pf = f;
+            if (pu >= 16) {
+                pu -= 16;
+                pf += ncl;
+            }
+            if (pf < a.frames) prefetch_tile(a.y, a.x, (size_t)pf * kN * kM, 16 * pu + 8 * rank);
+        }
         {
             float2* col = s.cols + w * kVS;
             float2 v[32];
@@ -293,6 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     const float* partner_edges = a.edges + ((size_t)cid * 2 + (rank ^ 1)) * 16 * 2 * kN;
     unsigned long long* my_pend = a.pend + ((size_t)cid * 2 + rank) * kFusedPend;
     int* my_ploc = a.pend_loc + ((size_t)cid * 2 + rank) * kFusedPend;
+    unsigned long long* tl = a.tlist + (size_t)blockIdx.x * kTileList;  // frame candidates (L2)
     auto C_tile = [&](int u, const float2* dsc, float ef) {
         const int c0 = 16 * u + 8 * rank;
         if (tid < 8) s.ccnt[tid] = 0;
@@ -366,7 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 const unsigned long long key = make_key(vv, (uint32_t)(r * kM + sc));
                 if (A && Cc) {
                     const int slot = atomicAdd(&s.tcnt, 1);
-                    if (slot < kTileList) s.tl[slot] = key;
+                    if (slot < kTileList) tl[slot] = key;
                 } else {
                     // partner edge column holding the missing neighbour: (partner step, edge)
                     int pu, pe;
@@ -414,20 +446,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             const float n0 = __ldcg(col + ((r - 1) & (kN - 1))), n1 = __ldcg(col + r), n2 = __ldcg(col + ((r + 1) & (kN - 1)));
             if (n0 >= vv || n1 >= vv || n2 >= vv) continue;
             const int sl = atomicAdd(&s.tcnt, 1);
-            if (sl < kTileList) s.tl[sl] = key;
+            if (sl < kTileList) tl[sl] = key;
         }
         __syncthreads();
         // per-CTA top-K of the frame's candidates (> kTileList / kFusedPend candidates in one
         // half-frame sets status bit 1 so the host recomputes the frame on the general path)
         if (tid == 0 && (s.tcnt > kTileList || s.pcnt > kFusedPend)) s.overflow = 1;
-        block_topk<256>(s.tl, min(s.tcnt, kTileList), K, s.run, s.sbest, s.sidx);
+        block_topk<256>(tl, min(s.tcnt, kTileList), K, s.run, s.sbest, s.sidx);
         __syncthreads();
         cluster.sync();  // both per-CTA lists final
         if (rank == 0) {
             if (w == 0) {
-                for (int i = lane; i < K; i += 32) s.tl[i] = p.run[i];
+                for (int i = lane; i < K; i += 32) s.prun[i] = p.run[i];
                 __syncwarp();
-                warp_merge_topk(s.run, s.tl, K, K, s.cand2);
+                warp_merge_topk(s.run, s.prun, K, K, s.cand2);
             }
             __syncthreads();
             const int kf = a.k_per_frame ? min(a.k_per_frame[f], K) : K;
