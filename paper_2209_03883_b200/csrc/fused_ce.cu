@@ -120,6 +120,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -163,57 +168,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     PH_INIT();
 
     // pass-A input stream: cp.async ring over this CTA's linear sequence of tiles
-    // (frame cid tiles 0..15, frame cid + ncl tiles 0..15, ...); one commit group per stage
-    int ring_pos = 0;
-    auto a_issue = [&](int f, int u, int st, int slot) {
-        if (st >= 16) {
-            st -= 16;
-            if (++u == 16) {
-                u = 0;
-                f += ncl;
-            }
-        }
-        if (f < a.frames) {
-            const int idx = tid + st * 256;
-            const size_t off = (size_t)f * kN * kM + (size_t)(idx >> 2) * kM + 16 * u + 8 * rank + (idx & 3) * 2;
-            cp_async16(&s.stg[slot][0][tid], a.y + off);
-            cp_async16(&s.stg[slot][1][tid], a.x + off);
+    // (frame cid tiles 0..15, frame cid + ncl tiles 0..15, ...); stage = 64 rows x 8 symbols
+    // of Y and x_tx; one commit group per stage; each thread only reads its own slots
+    int ifr = cid, iu = 0, ist = 0, islot = 0, cslot = 0;
+    const size_t lane_off = (size_t)(tid >> 2) * kM + 8 * rank + (tid & 3) * 2;
+    size_t ioff = (size_t)cid * kN * kM + lane_off;
+    auto a_issue = [&]() {
+        if (ifr < a.frames) {
+            cp_async16(&s.stg[islot][0][tid], a.y + ioff);
+            cp_async16(&s.stg[islot][1][tid], a.x + ioff);
         }
         cp_async_commit();
+        islot = islot + 1 == kRing ? 0 : islot + 1;
+        ioff += (size_t)64 * kM;
+        if (++ist == 16) {
+            ist = 0;
+            if (++iu == 16) {
+                iu = 0;
+                ifr += ncl;
+            }
+            ioff = (size_t)ifr * kN * kM + 16 * iu + lane_off;
+        }
     };
-    if (cid < a.frames)
-        for (int st = 0; st < kRing; ++st) a_issue(cid, 0, st, st);
+    for (int st = 0; st < kRing; ++st) a_issue();
 
     // ---------------------------------------------------------------- pass A, one tile
     // column tile u (8 symbols) of frame f: LS divide -> IFFT_N -> L taps x 1/N -> D
-    auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell) {
+    // dC: pass-C D' of the step's C tile, loaded into dpre right after the FFT so the
+    // L2 latency overlaps the tap store
+    auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell, const float2* dC, float4 (&dpre)[2]) {
+        (void)f;
         const int c0 = 16 * u + 8 * rank;
         float inv_tile = 0.f;
 #pragma unroll 4
         for (int st = 0; st < 16; ++st) {
             // stage st of this tile landed in ring slot (this thread's own 16-B slots)
             cp_async_wait<kRing - 1>();
-            const int slot = (ring_pos + st) % kRing;
-            const float4 y4 = s.stg[slot][0][tid];
-            const float4 x4 = s.stg[slot][1][tid];
+            const float4 y4 = s.stg[cslot][0][tid];
+            const float4 x4 = s.stg[cslot][1][tid];
+            cslot = cslot + 1 == kRing ? 0 : cslot + 1;
             const int idx = tid + st * 256;
             const int k = idx >> 2, c = (idx & 3) * 2;
             const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
             const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
             zero_cell |= (n0 == 0.f) | (n1 == 0.f);
-            const float i0 = n0 == 0.f ? 0.f : __frcp_rn(n0);
-            const float i1 = n1 == 0.f ? 0.f : __frcp_rn(n1);
+            const float i0 = n0 == 0.f ? 0.f : rcp_approx(n0);
+            const float i1 = n1 == 0.f ? 0.f : rcp_approx(n1);
             inv_tile += i0 + i1;
             const int pk = k + (k >> 5);
             const float2 r0 = make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
             const float2 r1 = make_float2(fmaf(y4.z, x4.z, y4.w * x4.w) * i1, fmaf(y4.w, x4.z, -y4.z * x4.w) * i1);
             s.cols[c * kVS + pk] = r0;
             s.cols[(c + 1) * kVS + pk] = r1;
-            // refill the slot (after its values were consumed) with the stage kRing ahead in
-            // this CTA's linear sequence of pass-A tiles
-            a_issue(f, u, st + kRing, slot);
+            // refill the slot (its values were consumed above) with the stage kRing ahead
+            a_issue();
         }
-        ring_pos = (ring_pos + 16) % kRing;
         inv_acc += (double)inv_tile;  // fp32 within a tile (32 terms), fp64 across tiles
         __syncthreads();
         PH(0);
@@ -233,6 +242,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = col[lane + 33 * i];
             warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: taps t1 + 32 t2
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int idx = tid + j * 256;
+                const int k = idx >> 2;
+                dpre[j] = dC && k < L ? __ldcg(reinterpret_cast<const float4*>(dC + (size_t)k * kM + c0 + (idx & 3) * 2))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
             __syncwarp();
             constexpr float inv_n = 1.0f / 1024.0f;
 #pragma unroll
@@ -325,13 +341,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     unsigned long long* my_pend = a.pend + ((size_t)cid * 2 + rank) * kFusedPend;
     int* my_ploc = a.pend_loc + ((size_t)cid * 2 + rank) * kFusedPend;
     unsigned long long* tl = a.tlist + (size_t)blockIdx.x * kTileList;  // frame candidates (L2)
-    auto C_tile = [&](int u, const float2* dsc, float ef) {
+    auto C_tile = [&](int u, const float2* dsc, float ef, bool pre, const float4 (&dpre)[2]) {
         const int c0 = 16 * u + 8 * rank;
         if (tid < 8) s.ccnt[tid] = 0;
-        for (int idx = tid; idx < 128 * 4; idx += 256) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int idx = tid + j * 256;
             const int k = idx >> 2, c = (idx & 3) * 2;
-            float4 v4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (k < L) v4 = __ldcg(reinterpret_cast<const float4*>(dsc + (size_t)k * kM + c0 + c));
+            float4 v4 = dpre[j];
+            if (!pre)
+                v4 = k < L ? __ldcg(reinterpret_cast<const float4*>(dsc + (size_t)k * kM + c0 + c))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
             const int pk = k + (k >> 5);
             s.cols[c * kVS + pk] = make_float2(v4.x, v4.y);
             s.cols[(c + 1) * kVS + pk] = make_float2(v4.z, v4.w);
@@ -497,7 +517,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     if (cid < a.frames) {
         double inv_acc = 0.0;
         int zc = 0;
-        for (int u = 0; u < 16; ++u) A_tile(cid, u, dbuf(0), inv_acc, zc);
+        float4 dpre[2];
+        for (int u = 0; u < 16; ++u) A_tile(cid, u, dbuf(0), inv_acc, zc, nullptr, dpre);
         A_finish(cid, 0, inv_acc, zc);
         B_pass(dbuf(0));
     }
@@ -516,8 +537,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         double inv_acc = 0.0;
         int zc = 0;
         for (int u = 0; u < 16; ++u) {
-            if (hasN) A_tile(fN, u, dbuf(sn), inv_acc, zc);
-            C_tile(u, dbuf(sc), ef);
+            float4 dpre[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+            if (hasN) A_tile(fN, u, dbuf(sn), inv_acc, zc, dbuf(sc), dpre);
+            C_tile(u, dbuf(sc), ef, hasN, dpre);
         }
         C_finish(fC, sc, ef);
         if (hasN) {
