@@ -47,6 +47,9 @@ cudaError_t launch_pgram_persist(const PersistArgs& pa, bool ls, bool win, int g
 
 cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
 cudaError_t launch_fused_ws(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
+cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_t st);
+int fused_pg_max_clusters();
+int fused_pg_cluster();
 }  // namespace ofdmr
 
 using namespace ofdmr;
@@ -100,6 +103,8 @@ struct ofdmr_context {
     bool fused = false;          // + DFT-CE with 0 < L <= 128: persistent one-frame-per-CTA kernel
     bool force_general = false;  // set by ofdmr_pipeline_general for one call
     int fused_grid = 0;
+    int pg_clusters = 0;              // fused periodogram: co-resident 8-CTA clusters
+    float2* pg_scratch = nullptr;     // fused periodogram: per-cluster 1024 x 256 G (L2)
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
     float* fedges = nullptr;               // fused: per-CTA edge columns of P (16 steps x 2)
     unsigned long long* fpend = nullptr;   // fused: per-CTA pending edge candidates
@@ -629,6 +634,7 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->tw1024_t);
     cudaFree(c->tw256_t);
     cudaFree(c->dscratch);
+    cudaFree(c->pg_scratch);
     cudaFree(c->fedges);
     cudaFree(c->fpend);
     cudaFree(c->fpend_loc);
@@ -779,6 +785,39 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
     // the general (non-shortcut) G layout is always N' rows; the chunk buffer holds g_rows rows
     const int64_t chunk = c->shortcut ? std::max<int64_t>(1, c->chunk * c->g_rows / g.n_prime) : c->chunk;
     (void)chunk;
+    if (c->fast && g.n_subcarriers == 1024 && g.n_symbols == 256 && g.n_prime == 1024 && g.m_prime == 256 &&
+        getenv("OFDMR_PG_PERSIST") == nullptr) {
+        // fused single-launch periodogram (8-CTA cluster per frame, G in L2)
+        if (!c->pg_scratch) {
+            c->pg_clusters = fused_pg_max_clusters();
+            if (c->pg_clusters <= 0) return fail(OFDMR_ERR_CUDA, "fused periodogram: no co-resident cluster");
+            OFDMR_CUDA(cudaMalloc(&c->pg_scratch, sizeof(float2) * 1024 * 256 * size_t(c->pg_clusters)));
+        }
+        PgArgs pa{};
+        pa.h = static_cast<const float2*>(h);
+        pa.p = p;
+        const bool win = g.window == OFDMR_WINDOW_HAMMING;
+        pa.wk = win ? c->wk : nullptr;
+        pa.wl = win ? c->wl : nullptr;
+        pa.tw1024_t = c->tw1024_t;
+        pa.tw256_t = c->tw256_t;
+        pa.gscratch = c->pg_scratch;
+        pa.scale = c->scale;
+        for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
+            const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);
+            pa.h = static_cast<const float2*>(h) + fc * f0;
+            pa.p = p + pframe * f0;
+            pa.frames = int(nf);
+            cudaError_t e;
+            {
+                StageTimer t(c, 0, c->stream);
+                e = launch_fused_pg(pa, win, fused_pg_cluster() * int(std::min<int64_t>(c->pg_clusters, nf)), c->stream);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "fused_pg");
+            ++c->launches;
+        }
+        return OFDMR_OK;
+    }
     if (c->fast && getenv("OFDMR_NO_PERSIST") == nullptr)
         return run_persist(c, static_cast<const float2*>(h), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                            nullptr, nullptr, nullptr, p, nullptr, frames);
@@ -1124,3 +1163,13 @@ int ofdmr_sft(ofdmr_context* c, const void* h, int32_t n, int32_t m, const ofdmr
 }
 
 }  // extern "C"
+
+// Debug/introspection (tools only): integer properties of a context.
+extern "C" long long ofdmr_debug_info(ofdmr_context* c, const char* key) {
+    if (!c || !key) return -1;
+    const std::string k(key);
+    if (k == "pg_clusters") return c->pg_clusters;
+    if (k == "fused_grid") return c->fused_grid;
+    if (k == "pg_max_clusters") return ofdmr::fused_pg_max_clusters();
+    return -1;
+}

@@ -28,6 +28,9 @@ namespace ofdmr {
 #ifndef PF_AHEAD
 #define PF_AHEAD 0  // L2 prefetch distance of pass-A tiles
 #endif
+#ifndef TW_GLOBAL
+#define TW_GLOBAL 0  // 1: FFT1024 twiddles read through L1 from global (frees 8 KB of smem)
+#endif
 #ifndef RING
 #define RING 4
 #endif
@@ -55,11 +58,13 @@ namespace {
 
 constexpr int kM = 256;
 constexpr int kN = 1024;
-constexpr int kVS = 1057;         // padded column buffer (pad_len(1024))
+constexpr int kVS = 1058;         // padded column buffer (>= pad_len(1024); 2 mod 8 -> conflict-free tile writes)
 constexpr int kTileList = 1024;   // per-CTA frame candidate list (exact fallback beyond)
 
 struct FusedSmem {
+#if !TW_GLOBAL
     float2 tw[1024];
+#endif
     float2 tw256[256];
     float2 cols[8 * kVS];         // per-warp column buffers / pass-A,C tiles / pass-B scratch
     float4 stg[kRing][2][256];    // pass-A staging ring: thread-private 16-B slots of Y and x_tx
@@ -161,7 +166,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     auto lcol = [&](int c) -> const float* { return pbase + c * (2 * kVS); };
     auto dbuf = [&](int parity) { return a.dscratch + ((size_t)cid * 2 + parity) * 128 * kM; };
 
+#if TW_GLOBAL
+    const float2* twp = a.tw1024_t;
+#else
     for (int i = tid; i < 1024; i += 256) s.tw[i] = a.tw1024_t[i];
+    const float2* twp = s.tw;
+#endif
     s.tw256[tid] = a.tw256_t[tid];
     if (tid == 0) s.overflow = 0;
     __syncthreads();
@@ -241,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             float2 v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = col[lane + 33 * i];
-            warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: taps t1 + 32 t2
+            warp_fft1024<true, 32, TW_GLOBAL>(v, col, twp);  // lane t1: taps t1 + 32 t2
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int idx = tid + j * 256;
@@ -365,10 +375,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
 #pragma unroll
             for (int i = 0; i < 4; ++i) v[i] = col[lane + 33 * i];
             if constexpr (HAMMING) {
-                warp_fft1024<false, 4>(v, col, s.tw);
+                warp_fft1024<false, 4, TW_GLOBAL>(v, col, twp);
 #pragma unroll
                 for (int t2 = 0; t2 < 32; ++t2) v[t2] = cscale(v[t2], __ldg(a.wk + lane + 32 * t2));
-                warp_fft1024<true, 32>(v, col, s.tw);
+                warp_fft1024<true, 32, TW_GLOBAL>(v, col, twp);
                 __syncwarp();
 #pragma unroll
                 for (int t2 = 0; t2 < 32; ++t2) {

@@ -109,14 +109,14 @@ template <bool INV> __device__ __forceinline__ void dft32_in4(float2* x) {
 // read when NZ == 4).  col: this warp's padded smem vector (>= pad_len(1024) float2),
 // free for use.  tw: smem table tw[t1 * 32 + j] = W_1024^{j t1} (forward).  On exit lane
 // t1 holds X[t1 + 32 t2] in v[t2].
-template <bool INV, int NZ>
+template <bool INV, int NZ, bool GTW = false>
 __device__ __forceinline__ void warp_fft1024(float2 (&v)[32], float2* col, const float2* tw) {
     const int lane = threadIdx.x & 31;
     if constexpr (NZ == 4) dft32_in4<INV>(v);
     else dft32<INV>(v);
 #pragma unroll
     for (int t1 = 1; t1 < 32; ++t1) {
-        float2 w = tw[t1 * 32 + lane];
+        float2 w = GTW ? __ldg(tw + t1 * 32 + lane) : tw[t1 * 32 + lane];  // GTW: read-only global table
         if (INV) w.y = -w.y;
         v[t1] = cmul(v[t1], w);
     }

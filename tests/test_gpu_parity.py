@@ -311,3 +311,24 @@ def test_fused_tile_boundary_peaks(cuda, window):
         assert powers_close(got, ref)
         hits += sum(1 for _, b, _ in ref if (b + m // 2) % 16 in (0, 7, 8, 15))
     assert hits >= frames * 3  # the boundary columns really were exercised
+
+
+@pytest.mark.parametrize("window", [0, 1])
+def test_fused_periodogram_many_frames_per_cluster(cuda, window, monkeypatch):
+    """More frames than co-resident clusters (each cluster loops over several frames, G
+    reused): every frame of the fused single-launch periodogram must match the ticketed
+    persistent kernel, and sampled frames the oracle."""
+    n, m, F = 1024, 256, 96
+    rng = np.random.default_rng(11)
+    h = (rng.standard_normal((F, n, m)) + 1j * rng.standard_normal((F, n, m))).astype(np.complex64)
+    with Receiver(n, m, window=window) as rx:
+        l0 = rx.launch_count
+        p = rx.periodogram(h).cpu().numpy()
+        assert rx.launch_count - l0 == 1
+        monkeypatch.setenv("OFDMR_PG_PERSIST", "1")
+        q = rx.periodogram(h).cpu().numpy()
+    for f in range(F):
+        assert np.abs(p[f] - q[f]).max() / q[f].max() <= MAP_TOL, f
+    for f in (0, 41, F - 1):
+        ref = O.periodogram(h[f].astype(np.complex128), window, n, m)
+        assert np.abs(p[f] - ref).max() / ref.max() <= MAP_TOL
