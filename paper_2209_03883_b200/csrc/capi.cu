@@ -105,6 +105,7 @@ struct ofdmr_context {
     int fused_grid = 0;
     int pg_clusters = 0;              // fused periodogram: co-resident 8-CTA clusters
     float2* pg_scratch = nullptr;     // fused periodogram: per-cluster 1024 x 256 G (L2)
+    int* pg_counters = nullptr;       // fused periodogram: per-group barrier counters
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
     float* fedges = nullptr;               // fused: per-CTA edge columns of P (16 steps x 2)
     unsigned long long* fpend = nullptr;   // fused: per-CTA pending edge candidates
@@ -635,6 +636,7 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->tw256_t);
     cudaFree(c->dscratch);
     cudaFree(c->pg_scratch);
+    cudaFree(c->pg_counters);
     cudaFree(c->fedges);
     cudaFree(c->fpend);
     cudaFree(c->fpend_loc);
@@ -792,7 +794,9 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
             c->pg_clusters = fused_pg_max_clusters();
             if (c->pg_clusters <= 0) return fail(OFDMR_ERR_CUDA, "fused periodogram: no co-resident cluster");
             OFDMR_CUDA(cudaMalloc(&c->pg_scratch, sizeof(float2) * 1024 * 256 * size_t(c->pg_clusters)));
+            OFDMR_CUDA(cudaMalloc(&c->pg_counters, sizeof(int) * size_t(c->pg_clusters)));
         }
+        OFDMR_CUDA(cudaMemsetAsync(c->pg_counters, 0, sizeof(int) * size_t(c->pg_clusters), c->stream));
         PgArgs pa{};
         pa.h = static_cast<const float2*>(h);
         pa.p = p;
@@ -802,6 +806,7 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
         pa.tw1024_t = c->tw1024_t;
         pa.tw256_t = c->tw256_t;
         pa.gscratch = c->pg_scratch;
+        pa.group_counters = c->pg_counters;
         pa.scale = c->scale;
         for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
             const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);

@@ -48,6 +48,7 @@ struct PgArgs {
     const float2* tw1024_t;
     const float2* tw256_t;
     float2* gscratch;          // per cluster 1024 x 256 intermediate (L2 resident)
+    int* group_counters;       // per frame group barrier counter (zeroed before each launch)
     int frames;
     float scale;               // 1 / (N M)
 };

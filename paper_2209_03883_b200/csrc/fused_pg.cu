@@ -2,20 +2,23 @@
 //   P[n][(m + M/2) mod M] = |FFT_M( IFFT_N( H .* w_k w_l ) )|^2 / (N M)
 // (periodogram.cpp:39-75; the map ofdmr_periodogram returns).
 //
-// One 8-CTA thread-block cluster per frame (2 CTAs per SM, 8 warps each):
-//   column pass  CTA r, step u (0..3) owns symbols 64u + 8r .. +7, so at every step the cluster
-//                reads 512 contiguous bytes of each subcarrier row of H.  H arrives through a
+// One group of G = 16 CTAs per frame (2 CTAs per SM, 8 warps each; a persistent grid of
+// 18 groups), synchronised by a counting global-memory barrier (all CTAs are resident):
+//   column pass  CTA r, step u owns symbols 8G u + 8r .. +7, so at every step the group reads
+//                8G * 8 contiguous bytes of each subcarrier row of H.  H arrives through a
 //                thread-private cp.async ring (4 x 8 KB); w_k w_l on the fly; each warp runs
-//                one register-resident IFFT_1024; the 1024 x 8 tile of G goes to a per-cluster
-//                2 MiB L2 scratch as 64-B row segments.
-//   cluster barrier (G complete)
-//   row pass     CTA r owns rows 128r .. 128r + 127: half-warp FFT_256 per row, |.|^2 / (N M)
-//                with the Doppler fftshift, streamed to P as 64-B segments; the rows of the
-//                next round are loaded while the current round transforms.
-//   split cluster barrier (arrive after the last G read, wait before the first G write of the
-//                next frame), so no CTA waits for its peers between frames.
+//                one register-resident IFFT_1024; the 1024 x 8 tile of G goes to a per-group
+//                2 MiB scratch as 64-B row segments.
+//   group barrier (G complete)
+//   row pass     CTA r owns rows 1024/G r ..: half-warp FFT_256 per row (twiddles in
+//                registers), |.|^2 / (N M) with the Doppler fftshift, streamed to P; the rows
+//                of the next round are loaded while the current round transforms.
+//   split barrier (arrive after the last G read, wait before the first G write of the next
+//                frame), so no CTA waits for its peers between frames.
 // The ring keeps prefetching the next frame's H during the row pass.  Frames in flight = the
-// number of co-resident clusters (<= 37), i.e. <= 74 MiB of G, which stays in L2.
+// number of groups (18), i.e. 36 MiB of G, which stays in L2: measured DRAM traffic is
+// 3.7 MiB/frame against 3 MiB algorithmic (a 2-CTA hardware cluster per frame, PG_SW=0,
+// PG_CLUSTER=2, runs at the same speed but spills G: 7.2 MiB/frame).
 #include <cooperative_groups.h>
 
 #include "fused_args.cuh"
@@ -32,7 +35,10 @@ constexpr int kN = 1024, kM = 256;
 constexpr int kVS = 1058;       // padded column stride (float2; 2 mod 8 -> conflict-free tile writes)
 constexpr int kPgRing = 4;      // H staging ring depth (stages of 128 rows x 8 symbols)
 #ifndef PG_CLUSTER
-#define PG_CLUSTER 2
+#define PG_CLUSTER 16
+#endif
+#ifndef PG_SW
+#define PG_SW 1  // 1: the PG_CLUSTER CTAs of a frame are a software group (global-memory barrier)
 #endif
 constexpr int kPgCluster = PG_CLUSTER;  // CTAs per frame
 constexpr int kPgSteps = 256 / (8 * kPgCluster);   // column tiles per CTA
@@ -52,8 +58,48 @@ __device__ __forceinline__ void pg_cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void pg_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void pg_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+#if !PG_SW
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+#endif
+#if PG_SW
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+#endif
+
+// Frame-group barrier: a hardware cluster barrier, or (PG_SW) a monotonically counting
+// global-memory barrier over the group's CTAs (all CTAs of the persistent grid are resident).
+struct GroupBarrier {
+    int* counter;
+    int phase;
+    __device__ void arrive() {
+#if PG_SW
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(counter, 1);
+        }
+        ++phase;
+#else
+        cluster_arrive();
+#endif
+    }
+    __device__ void wait() {
+#if PG_SW
+        if (threadIdx.x == 0) {
+            const int target = kPgCluster * phase;
+            while (ld_acquire(counter) < target) __nanosleep(32);
+            __threadfence();
+        }
+        __syncthreads();
+#else
+        cluster_wait();
+#endif
+    }
+};
 
 }  // namespace
 
@@ -74,11 +120,15 @@ __device__ unsigned long long g_pg_phase[8];
 #endif
 
 template <bool HAMMING>
-__global__ void __cluster_dims__(kPgCluster, 1, 1) __launch_bounds__(256, 2) fused_pg1024_kernel(PgArgs a) {
+__global__ void
+#if !PG_SW
+__cluster_dims__(kPgCluster, 1, 1)
+#endif
+__launch_bounds__(256, 2) fused_pg1024_kernel(PgArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PgSmem& s = *reinterpret_cast<PgSmem*>(smem_raw);
-    cg::cluster_group cluster = cg::this_cluster();
-    const int rank = (int)cluster.block_rank();
+    const int rank = (int)(blockIdx.x % kPgCluster);
+    GroupBarrier bar{a.group_counters + blockIdx.x / kPgCluster, 0};
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int cid = blockIdx.x / kPgCluster, ncl = gridDim.x / kPgCluster;
     float2* g = a.gscratch + (size_t)cid * kN * kM;
@@ -157,7 +207,7 @@ __global__ void __cluster_dims__(kPgCluster, 1, 1) __launch_bounds__(256, 2) fus
             }
             __syncthreads();
             PGPH(1);
-            if (u == 0 && !first) cluster_wait();  // peers finished reading the previous frame's G
+            if (u == 0 && !first) bar.wait();  // peers finished reading the previous frame's G
             first = false;
             PGPH(2);
 #pragma unroll 4
@@ -173,7 +223,8 @@ __global__ void __cluster_dims__(kPgCluster, 1, 1) __launch_bounds__(256, 2) fus
             PGPH(3);
         }
         __threadfence();
-        cluster.sync();  // G of frame f complete
+        bar.arrive();  // G of frame f complete
+        bar.wait();
         PGPH(4);
 
         // ------------------------------------------------------------ row pass
@@ -181,7 +232,9 @@ __global__ void __cluster_dims__(kPgCluster, 1, 1) __launch_bounds__(256, 2) fus
             const int hw = tid >> 4, j = tid & 15;
             float2* tb = s.cols + hw * (16 * 17);
             float* pf = a.p + (size_t)f * kN * kM;
-            float2 v[16], vn[16];
+            float2 v[16], vn[16], twr[16];
+#pragma unroll
+            for (int t1 = 0; t1 < 16; ++t1) twr[t1] = s.tw256[t1 * 16 + j];
             const int rbase = kPgRows * rank + hw;
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = __ldcg(g + (size_t)rbase * kM + j + 16 * i);
@@ -191,7 +244,7 @@ __global__ void __cluster_dims__(kPgCluster, 1, 1) __launch_bounds__(256, 2) fus
 #pragma unroll
                     for (int i = 0; i < 16; ++i) vn[i] = __ldcg(g + (size_t)(n + 16) * kM + j + 16 * i);
                 }
-                halfwarp_fft256<false>(v, tb, s.tw256);
+                halfwarp_fft256_rt<false>(v, tb, twr);
                 float* prow = pf + (size_t)n * kM;
 #pragma unroll
                 for (int t2 = 0; t2 < 16; ++t2) __stcs(prow + ((j + 16 * t2 + 128) & 255), cnorm(v[t2]) * a.scale);
@@ -201,9 +254,9 @@ __global__ void __cluster_dims__(kPgCluster, 1, 1) __launch_bounds__(256, 2) fus
         }
         __syncthreads();   // row-pass scratch (cols) free before the next frame's tiles land in it
         PGPH(5);
-        cluster_arrive();  // our G reads are done (matched by the wait before the next G write)
+        bar.arrive();  // our G reads are done (matched by the wait before the next G write)
     }
-    if (!first) cluster_wait();  // balance the last arrive before exit
+    if (!first) bar.wait();  // balance the last arrive before exit
 }
 
 }  // namespace ofdmr
@@ -245,6 +298,17 @@ cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_
 // Co-resident 8-CTA clusters of the kernel (the persistent grid is this many clusters).
 int fused_pg_max_clusters() {
     const size_t smem = sizeof(PgSmem);
+#if PG_SW
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaFuncSetAttribute(fused_pg1024_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_pg1024_kernel<false>, 256, smem) != cudaSuccess)
+        return 0;
+    return per_sm * sms / kPgCluster;
+#endif
     if (cudaFuncSetAttribute(fused_pg1024_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return 0;

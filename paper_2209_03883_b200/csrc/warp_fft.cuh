@@ -151,4 +151,25 @@ __device__ __forceinline__ void halfwarp_fft256(float2 (&v)[16], float2* buf, co
     dft16<INV>(v);
 }
 
+// Same with the sub-lane's twiddles held in registers: twr[t1] = W_256^{j t1} (forward),
+// loaded once by callers that transform many rows per lane.
+template <bool INV>
+__device__ __forceinline__ void halfwarp_fft256_rt(float2 (&v)[16], float2* buf, const float2 (&twr)[16]) {
+    const int j = threadIdx.x & 15;
+    dft16<INV>(v);
+#pragma unroll
+    for (int t1 = 1; t1 < 16; ++t1) {
+        float2 w = twr[t1];
+        if (INV) w.y = -w.y;
+        v[t1] = cmul(v[t1], w);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t1 = 0; t1 < 16; ++t1) buf[t1 * 17 + j] = v[t1];
+    __syncwarp();
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) v[jj] = buf[j * 17 + jj];
+    dft16<INV>(v);
+}
+
 }  // namespace ofdmr
