@@ -12,7 +12,7 @@ os.environ.setdefault("OFDMR_LIB", os.path.join(os.path.dirname(os.path.dirname(
 from paper_2209_03883_b200 import _native  # noqa: E402
 from paper_2209_03883_b200.receiver import Receiver  # noqa: E402
 
-NAMES = ["col_load", "col_fft", "G_wait", "G_store", "cluster_sync", "row_pass"]
+NAMES = ["col_load", "col_fft", "G_wait", "G_store", "group_barrier", "row_pass"]
 F = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 win = sys.argv[2] if len(sys.argv) > 2 else "rectangular"
 h = torch.randn(64, 1024, 256, dtype=torch.complex64, device="cuda").repeat(-(-F // 64), 1, 1)[:F].contiguous()
