@@ -35,6 +35,20 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 MAX_T = 16
 
 
+def load_traffic(kernel: str, frames: int):
+    """DRAM bytes per launch of `kernel` for `frames` frames, from the committed ncu
+    measurement (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per
+    frame of a capture of the same kernel), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)[kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"bytes_per_launch": t["dram_bytes_per_frame"] * frames,
+            "source": f"profiles/traffic.json: {t['source']} ({t['dram_bytes_per_frame']:.0f} B/frame)"}
+
+
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -380,11 +394,14 @@ def main():
     hbm = float(peaks["hbm_gbs"])
     alg_bytes_frame = 16 * cfg.n * cfg.m   # read Y and x_tx as c64
     achieved = nf * alg_bytes_frame / (kern_ms / 1e3) / 1e9
+    traffic = load_traffic("fused_ce1024", nf) if stage_n[1] == 0 else None
     roofline = {
-        "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+        "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+        "traffic": traffic["bytes_per_launch"] if traffic else None,
+        "traffic_source": traffic["source"] if traffic else None,
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-        "kernel": ("fused_ce1024 (persistent, one frame per CTA: LS + IFFT/truncate -> L x M taps -> row FFT -> "
-                   "pruned FFT x w_k -> IFFT -> |.|^2 -> 3x3 top-K)" if stage_n[1] == 0 else
+        "kernel": ("fused_ce1024 (persistent, one frame per 2-CTA cluster: LS + IFFT/truncate -> L x M taps -> "
+                   "row FFT -> pruned FFT x w_k -> IFFT -> |.|^2 -> 3x3 top-K)" if stage_n[1] == 0 else
                    "pipeline step: colpass + rowpass + merge, chunked so the intermediate stays in L2"),
         "algorithmic_bytes_per_frame": alg_bytes_frame, "frames_per_launch_chunk": int(rx.cfg.chunk_frames) or None,
         "stage_ms": ({"fused_ce": stage_ms[0]} if stage_n[1] == 0 else
@@ -419,9 +436,13 @@ def main():
         per._stream()
         per._lib.ofdmr_periodogram(per._h, h.data_ptr(), pm.data_ptr(), pf)
         pst, _ = per.get_profile()
+        ptraffic = load_traffic("fused_pg1024", pf)
         periodogram = {"frames": pf, "frames_per_s": pf / (pms / 1e3), "ms_per_step": pms,
+                       "kernel": "fused_pg1024 (persistent, 16-CTA frame groups, G in L2)",
                        "algorithmic_bytes_per_frame": pbytes, "achieved_gbs": pach, "frac": pach / hbm,
-                       "stage_ms": {"colpass": pst[0], "rowpass": pst[1]}}
+                       "traffic": ptraffic["bytes_per_launch"] if ptraffic else None,
+                       "traffic_source": ptraffic["source"] if ptraffic else None,
+                       "stage_ms": {"fused_pg": pst[0]}}
         del pm
         per.close()
 

@@ -47,7 +47,6 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "radar_kernels": [],
         "fast_kernels": [],
         "fused_ce": [],
-        "fused_ws": [],
         "fused_pg": [],
         "capi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions

@@ -46,7 +46,6 @@ struct PersistArgs {
 cudaError_t launch_pgram_persist(const PersistArgs& pa, bool ls, bool win, int grid, cudaStream_t st);
 
 cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
-cudaError_t launch_fused_ws(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
 cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_t st);
 int fused_pg_max_clusters();
 int fused_pg_cluster();
@@ -1004,14 +1003,8 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
             cudaError_t e;
             {
                 StageTimer t(c, 0, c->stream);
-                const char* var = getenv("OFDMR_FUSED");
-                if (var && var[0] == 'w') {
-                    // warp-specialised variant: one 384-thread CTA per SM (producer/consumer warps)
-                    e = launch_fused_ws(fa, win, int(std::min<int64_t>(c->fused_grid / 2, 2 * nf)), c->stream);
-                } else {
-                    // default: two 256-thread CTAs per SM, 2-CTA cluster per frame
-                    e = launch_fused_ce(fa, win, int(std::min<int64_t>(c->fused_grid, 2 * nf)), c->stream);
-                }
+                // two 256-thread CTAs per SM, 2-CTA cluster per frame
+                e = launch_fused_ce(fa, win, int(std::min<int64_t>(c->fused_grid, 2 * nf)), c->stream);
             }
             if (e != cudaSuccess) return cuda_fail(e, "fused_ce");
             ++c->launches;
