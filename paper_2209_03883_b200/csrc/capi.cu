@@ -84,6 +84,7 @@ struct ofdmr_context {
     int device = 0;
     float2* tw = nullptr;        // 4096-entry e^{-j2pi t/4096}
     float* wk = nullptr;         // Hamming windows (fp32) or null for rectangular
+    float* wk_s = nullptr;       // w_k * sqrt(1 / (N M)) for the fused kernel
     float* wl = nullptr;
     // two scheduling slots (slot 0 = the caller's stream, slot 1 = an internal stream);
     // consecutive chunks alternate so one chunk's row pass overlaps the next chunk's
@@ -549,6 +550,13 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         if (e == cudaSuccess) e = cudaMalloc(&c->wl, sizeof(float) * m);
         if (e == cudaSuccess) e = cudaMemcpy(c->wk, fk.data(), sizeof(float) * n, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemcpy(c->wl, fl.data(), sizeof(float) * m, cudaMemcpyHostToDevice);
+        // fused kernel: w_k pre-multiplied by sqrt(1 / (N M)) (= 2^-9 at 1024 x 256, exact), so
+        // |w_k X|^2 needs no separate scale
+        std::vector<float> fks(n);
+        const double rs = std::sqrt(1.0 / (double(n) * double(m)));
+        for (int i = 0; i < n; ++i) fks[i] = float(wk[i] * rs);
+        if (e == cudaSuccess) e = cudaMalloc(&c->wk_s, sizeof(float) * n);
+        if (e == cudaSuccess) e = cudaMemcpy(c->wk_s, fks.data(), sizeof(float) * n, cudaMemcpyHostToDevice);
     }
     // the periodogram entry point always needs the full N' rows
     const size_t gbytes = std::max(gframe, size_t(np) * size_t(m) * sizeof(float2)) * size_t(chunk);
@@ -623,6 +631,7 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaSetDevice(c->device);
     cudaFree(c->tw);
     cudaFree(c->wk);
+    cudaFree(c->wk_s);
     cudaFree(c->wl);
     for (auto& s : c->slot) {
         cudaFree(s.gbuf);
@@ -982,7 +991,7 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
         fa.s2h_out = s2h_out;
         fa.status = status;
         const bool win = g.window == OFDMR_WINDOW_HAMMING;
-        fa.wk = win ? c->wk : nullptr;
+        fa.wk = win ? c->wk_s : nullptr;  // sqrt-scaled copy (see ofdmr_create)
         fa.wl = win ? c->wl : nullptr;
         fa.tw1024_t = c->tw1024_t;
         fa.tw256_t = c->tw256_t;

@@ -251,7 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             float2 v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = col[lane + 33 * i];
-            warp_fft1024<true, 32, TW_GLOBAL>(v, col, twp);  // lane t1: taps t1 + 32 t2
+            warp_fft1024<true, 32, TW_GLOBAL, 4>(v, col, twp);  // lane t1: taps t1 + 32 t2, t2 < 4
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int idx = tid + j * 256;
@@ -382,7 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 __syncwarp();
 #pragma unroll
                 for (int t2 = 0; t2 < 32; ++t2) {
-                    const float pv = cnorm(v[t2]) * a.scale;
+                    const float pv = cnorm(v[t2]);  // a.wk carries sqrt(scale)
                     pcol[lane + 32 * t2] = pv;
                     if (pv >= ef) {  // rare: ~1 % of cells
                         const int pos = atomicAdd(&s.ccnt[w], 1);
@@ -394,7 +394,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
 #pragma unroll
                 for (int t2 = 0; t2 < 32; ++t2) {
                     float pv = 0.f;
-                    if (t2 < 4) pv = cnorm(cscale(v[t2], 1024.0f)) * a.scale;
+                    if (t2 < 4) pv = cnorm(cscale(v[t2], 2.0f));  // |1024 v|^2 * 2^-18, exact
                     pcol[lane + 32 * t2] = pv;
                     if (pv >= ef) {
                         const int pos = atomicAdd(&s.ccnt[w], 1);

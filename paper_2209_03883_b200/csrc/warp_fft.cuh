@@ -105,11 +105,44 @@ template <bool INV> __device__ __forceinline__ void dft32_in4(float2* x) {
     in4_all<INV>(x, v, std::make_integer_sequence<int, 8>{});
 }
 
+template <bool INV, int R, int K>
+__device__ __forceinline__ void out4_acc(float2* acc, const float2* u) {
+    const float2 t = mul_w32<INV, R * K>(u[K]);
+    acc[K] = cadd(acc[K], t);
+}
+template <bool INV, int R>
+__device__ __forceinline__ void out4_step(float2* acc, const float2* x) {
+    float2 u[4] = {x[R], x[R + 8], x[R + 16], x[R + 24]};
+    dft4<INV>(u);
+    if constexpr (R == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = u[k];
+    } else {
+        out4_acc<INV, R, 0>(acc, u);
+        out4_acc<INV, R, 1>(acc, u);
+        out4_acc<INV, R, 2>(acc, u);
+        out4_acc<INV, R, 3>(acc, u);
+    }
+}
+template <bool INV, int... Rs>
+__device__ __forceinline__ void out4_all(float2* acc, const float2* x, std::integer_sequence<int, Rs...>) {
+    (out4_step<INV, Rs>(acc, x), ...);
+}
+
+// First 4 outputs of a 32-point DFT (natural order in; X[0..3] -> x[0..3]):
+// X[k] = sum_r W_32^{rk} DFT_4 over m of x[8m + r], k < 4.
+template <bool INV> __device__ __forceinline__ void dft32_out4(float2* x) {
+    float2 acc[4];
+    out4_all<INV>(acc, x, std::make_integer_sequence<int, 8>{});
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = acc[k];
+}
+
 // Warp FFT of length 1024.  On entry lane j holds v[i] = x[j + 32 i] (only v[0..NZ)
-// read when NZ == 4).  col: this warp's padded smem vector (>= pad_len(1024) float2),
+// read when NZ == 4; only v[0..4) produced when NOUT == 4).  col: this warp's padded smem vector (>= pad_len(1024) float2),
 // free for use.  tw: smem table tw[t1 * 32 + j] = W_1024^{j t1} (forward).  On exit lane
 // t1 holds X[t1 + 32 t2] in v[t2].
-template <bool INV, int NZ, bool GTW = false>
+template <bool INV, int NZ, bool GTW = false, int NOUT = 32>
 __device__ __forceinline__ void warp_fft1024(float2 (&v)[32], float2* col, const float2* tw) {
     const int lane = threadIdx.x & 31;
     if constexpr (NZ == 4) dft32_in4<INV>(v);
@@ -126,7 +159,8 @@ __device__ __forceinline__ void warp_fft1024(float2 (&v)[32], float2* col, const
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = col[lane * 33 + j];     // pidx(lane*32 + j)
-    dft32<INV>(v);
+    if constexpr (NOUT == 4) dft32_out4<INV>(v);  // only X[t1 + 32 t2], t2 < 4 (v[4..] garbage)
+    else dft32<INV>(v);
 }
 
 // Half-warp FFT of length 256 (lanes 0-15 one vector, 16-31 another).  On entry

@@ -1,0 +1,98 @@
+// Microbenchmark: HBM streaming rate of the fused kernel's pass-A access pattern (8-symbol
+// column tiles, 64-B row segments, both CTAs of a pair reading the two halves of a 128-B line)
+// through a per-thread cp.async ring, with no compute.  Usage: stream_micro [frames] [ring]
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+constexpr int kN = 1024, kM = 256;
+
+__device__ __forceinline__ void cp16(void* s, const void* g) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void waitg() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int RING, int SPIN>
+__global__ void __launch_bounds__(256, 2) stream_kernel(const float2* y, const float2* x, int frames, float* out) {
+    extern __shared__ float4 stg[];  // [RING][2][256]
+    const int tid = threadIdx.x, rank = blockIdx.x & 1, cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    int ifr = cid, iu = 0, ist = 0, islot = 0, cslot = 0;
+    const size_t lane_off = (size_t)(tid >> 2) * kM + 8 * rank + (tid & 3) * 2;
+    size_t ioff = (size_t)cid * kN * kM + lane_off;
+    auto issue = [&]() {
+        if (ifr < frames) {
+            cp16(&stg[(islot * 2 + 0) * 256 + tid], y + ioff);
+            cp16(&stg[(islot * 2 + 1) * 256 + tid], x + ioff);
+        }
+        commit();
+        islot = islot + 1 == RING ? 0 : islot + 1;
+        ioff += (size_t)64 * kM;
+        if (++ist == 16) {
+            ist = 0;
+            if (++iu == 16) { iu = 0; ifr += ncl; }
+            ioff = (size_t)ifr * kN * kM + 16 * iu + lane_off;
+        }
+    };
+    for (int i = 0; i < RING; ++i) issue();
+    float acc = 0.f;
+    for (int f = cid; f < frames; f += ncl)
+        for (int u = 0; u < 16; ++u) {
+            for (int st = 0; st < 16; ++st) {
+                waitg<RING - 1>();
+                const float4 a = stg[(cslot * 2) * 256 + tid], b = stg[(cslot * 2 + 1) * 256 + tid];
+                cslot = cslot + 1 == RING ? 0 : cslot + 1;
+                acc += a.x * b.x + a.w * b.z;
+                issue();
+            }
+            if (SPIN) {  // stand-in for the FFT phases: ALU work without memory traffic
+                float z = acc;
+#pragma unroll 1
+                for (int i = 0; i < SPIN; ++i) z = fmaf(z, 0.999f, 1e-7f);
+                acc = z;
+            }
+        }
+    if (acc == 12345.f) out[0] = acc;
+}
+
+template <int RING, int SPIN>
+void run(const float2* y, const float2* x, int frames, float* out, int sms) {
+    const size_t smem = sizeof(float4) * RING * 2 * 256;
+    cudaFuncSetAttribute(stream_kernel<RING, SPIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = 2 * sms;
+    stream_kernel<RING, SPIN><<<grid, 256, smem>>>(y, x, frames, out);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    stream_kernel<RING, SPIN><<<grid, 256, smem>>>(y, x, frames, out);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("ring %d spin %5d: %.3f ms  %.0f GB/s  (%.0f k frames/s)  %s\n", RING, SPIN, ms,
+           frames * 4.194304e6 / (ms / 1e3) / 1e9, frames / ms, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main(int argc, char** argv) {
+    const int frames = argc > 1 ? atoi(argv[1]) : 4096;
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    float2 *y, *x;
+    float* out;
+    cudaMalloc(&y, sizeof(float2) * kN * kM * (size_t)frames);
+    cudaMalloc(&x, sizeof(float2) * kN * kM * (size_t)frames);
+    cudaMalloc(&out, 4);
+    cudaMemset(y, 0, sizeof(float2) * kN * kM * (size_t)frames);
+    cudaMemset(x, 0, sizeof(float2) * kN * kM * (size_t)frames);
+    run<2, 0>(y, x, frames, out, sms);
+    run<4, 0>(y, x, frames, out, sms);
+    run<6, 0>(y, x, frames, out, sms);
+    run<8, 0>(y, x, frames, out, sms);
+    run<4, 200>(y, x, frames, out, sms);
+    run<4, 1000>(y, x, frames, out, sms);
+    run<4, 3000>(y, x, frames, out, sms);
+    run<8, 3000>(y, x, frames, out, sms);
+    return 0;
+}
