@@ -308,7 +308,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             s.etas[slot] = -s2h * a.log_pfa * a.power_factor;
             s.s2hs[slot] = s2h;
         }
-        cluster.sync();  // partner finished reading our partial
+        // (no second barrier: the partner's part / zc_part are next written in the next
+        // frame's A_finish, behind the B-pass and C_finish cluster barriers)
         PH(3);
     };
 
@@ -516,8 +517,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 if (a.status && (s.overflow || p.overflow)) atomicOr(a.status + f, 2);
             }
         }
-        cluster.sync();  // partner's run list and edge columns consumed
-        if (tid == 0) s.overflow = 0;
+        // (no barrier here: rank 1's run / overflow are next modified at the next round
+        // start, behind the next A_finish cluster barrier; the kernel ends with one)
         PH(10);
     };
 
@@ -540,6 +541,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         if (tid == 0) {
             s.tcnt = 0;
             s.pcnt = 0;
+            s.overflow = 0;
         }
         for (int i = tid; i < K; i += 256) s.run[i] = 0ull;
         const float ef = eta_float(s.etas[sc]);
@@ -557,6 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             B_pass(dbuf(sn));
         }
     }
+    cluster.sync();  // no CTA leaves while its partner may still read its shared memory
 }
 
 size_t fused_ce_smem() { return sizeof(FusedSmem); }
