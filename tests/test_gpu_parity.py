@@ -332,3 +332,35 @@ def test_fused_periodogram_many_frames_per_cluster(cuda, window, monkeypatch):
     for f in (0, 41, F - 1):
         ref = O.periodogram(h[f].astype(np.complex128), window, n, m)
         assert np.abs(p[f] - ref).max() / ref.max() <= MAP_TOL
+
+
+def test_fused_full_batch_position_independent(cuda):
+    """cfg4 at the bench's full size: 256 distinct frames tiled to 8192 (every cluster runs
+    ~55 software-pipelined rounds).  Size-independent property: every copy of a frame gets
+    bit-identical detections wherever it sits in the batch; sampled frames match the oracle."""
+    cfg = configs.CFG4
+    pool, F = 256, 8192
+    fb = gen.frames(cfg, 0, pool)
+    reps = F // pool
+    y = torch.from_numpy(fb.y).cuda().repeat(reps, 1, 1)
+    x = torch.from_numpy(fb.x).cuda().repeat(reps, 1, 1)
+    s2 = torch.from_numpy(np.tile(fb.sigma2, reps)).cuda()
+    kf = torch.from_numpy(np.tile(fb.n_targets, reps).astype(np.int32)).cuda()
+    with Receiver.from_config(cfg) as rx:
+        l0 = rx.launch_count
+        dets, _ = rx.pipeline(y, x, s2, k_per_frame=kf)
+        torch.cuda.synchronize()
+        assert rx.launch_count - l0 == 1
+    d = dets.delay_bin.cpu().numpy().reshape(reps, pool, -1)
+    v = dets.doppler_bin.cpu().numpy().reshape(reps, pool, -1)
+    p = dets.peak_power.cpu().numpy().reshape(reps, pool, -1)
+    c = dets.counts.cpu().numpy().reshape(reps, pool)
+    for arr in (d, v, p, c):
+        assert (arr == arr[0:1]).all()
+    rc = _rc(cfg)
+    for f in range(0, pool, 8):
+        k = int(fb.n_targets[f])
+        ref, _, eta, ref_map = O.receive_frame(rc, fb.y[f], fb.x[f], float(fb.sigma2[f]), k, want_map=True)
+        got = dets.frame(f)
+        assert classify(got, ref, ref_map, eta, k) != "fail", (f, got, ref)
+        assert powers_close(got, ref)
