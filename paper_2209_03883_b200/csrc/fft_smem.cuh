@@ -43,6 +43,67 @@ template <bool INV> __device__ __forceinline__ float2 mul_w4(float2 a) {
     return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
 }
 
+template <int K> struct W32c {
+    // compile-time W_32^K = cos - (+) j sin (forward / inverse)
+    static constexpr float c() {
+        constexpr float t[32] = {
+            1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
+            0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f, 0.19509032201612826785f,
+            0.0f, -0.19509032201612826785f, -0.38268343236508977173f, -0.55557023301960222474f,
+            -0.70710678118654752440f, -0.83146961230254523708f, -0.92387953251128675613f, -0.98078528040323044913f,
+            -1.0f, -0.98078528040323044913f, -0.92387953251128675613f, -0.83146961230254523708f,
+            -0.70710678118654752440f, -0.55557023301960222474f, -0.38268343236508977173f, -0.19509032201612826785f,
+            0.0f, 0.19509032201612826785f, 0.38268343236508977173f, 0.55557023301960222474f,
+            0.70710678118654752440f, 0.83146961230254523708f, 0.92387953251128675613f, 0.98078528040323044913f};
+        return t[K % 32];
+    }
+    static constexpr float s() {
+        constexpr float t[32] = {
+            0.0f, 0.19509032201612826785f, 0.38268343236508977173f, 0.55557023301960222474f,
+            0.70710678118654752440f, 0.83146961230254523708f, 0.92387953251128675613f, 0.98078528040323044913f,
+            1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
+            0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f, 0.19509032201612826785f,
+            0.0f, -0.19509032201612826785f, -0.38268343236508977173f, -0.55557023301960222474f,
+            -0.70710678118654752440f, -0.83146961230254523708f, -0.92387953251128675613f, -0.98078528040323044913f,
+            -1.0f, -0.98078528040323044913f, -0.92387953251128675613f, -0.83146961230254523708f,
+            -0.70710678118654752440f, -0.55557023301960222474f, -0.38268343236508977173f, -0.19509032201612826785f};
+        return t[K % 32];
+    }
+};
+
+template <bool INV, int K> __device__ __forceinline__ float2 mul_w32(float2 a) {
+    constexpr int k = K % 32;
+    if constexpr (k == 0) return a;
+    else if constexpr (k == 8) return mul_w4<INV>(a);
+    else if constexpr (k == 16) return make_float2(-a.x, -a.y);
+    else if constexpr (k == 24) return mul_w4<!INV>(a);
+    else {
+        constexpr float c = W32c<k>::c();
+        constexpr float s = INV ? W32c<k>::s() : -W32c<k>::s();
+        return make_float2(c * a.x - s * a.y, c * a.y + s * a.x);
+    }
+}
+
+
+// Radix-2 butterfly with a constant twiddle w = W_32^K (forward e^{-2 pi i K/32}, inverse
+// conjugate): lo = e + w o, hi = e - w o.  General K: four FMAs for lo and hi = 2e - lo
+// (six FP instructions instead of a 4-instruction multiply plus four adds).
+template <bool INV, int K>
+__device__ __forceinline__ void bfly32(float2& lo, float2& hi, float2 e, float2 o) {
+    constexpr int k = K % 32;
+    if constexpr (k == 0 || k == 8 || k == 16 || k == 24) {
+        const float2 t = mul_w32<INV, K>(o);
+        lo = cadd(e, t);
+        hi = csub(e, t);
+    } else {
+        constexpr float c = W32c<k>::c();
+        constexpr float s = INV ? W32c<k>::s() : -W32c<k>::s();
+        const float2 a = make_float2(fmaf(c, o.x, fmaf(-s, o.y, e.x)), fmaf(c, o.y, fmaf(s, o.x, e.y)));
+        hi = make_float2(fmaf(2.0f, e.x, -a.x), fmaf(2.0f, e.y, -a.y));
+        lo = a;
+    }
+}
+
 template <bool INV> __device__ __forceinline__ void dft2(float2* x) {
     const float2 a = x[0], b = x[1];
     x[0] = cadd(a, b);
@@ -59,33 +120,18 @@ template <bool INV> __device__ __forceinline__ void dft4(float2* x) {
 }
 
 template <bool INV> __device__ __forceinline__ void dft8(float2* x) {
-    constexpr float c = 0.70710678118654752440f;
     float2 e[4] = {x[0], x[2], x[4], x[6]};
     float2 o[4] = {x[1], x[3], x[5], x[7]};
     dft4<INV>(e);
     dft4<INV>(o);
-    // o1 *= W8, o2 *= W8^2, o3 *= W8^3  (W8 = e^{-+j pi/4})
-    const float2 o1 = INV ? make_float2(c * (o[1].x - o[1].y), c * (o[1].x + o[1].y))
-                          : make_float2(c * (o[1].x + o[1].y), c * (o[1].y - o[1].x));
-    const float2 o2 = mul_w4<INV>(o[2]);
-    const float2 o3 = INV ? make_float2(-c * (o[3].x + o[3].y), c * (o[3].x - o[3].y))
-                          : make_float2(c * (o[3].y - o[3].x), -c * (o[3].x + o[3].y));
-    x[0] = cadd(e[0], o[0]);
-    x[4] = csub(e[0], o[0]);
-    x[1] = cadd(e[1], o1);
-    x[5] = csub(e[1], o1);
-    x[2] = cadd(e[2], o2);
-    x[6] = csub(e[2], o2);
-    x[3] = cadd(e[3], o3);
-    x[7] = csub(e[3], o3);
+    // W_8^k = W_32^{4k}
+    bfly32<INV, 0>(x[0], x[4], e[0], o[0]);
+    bfly32<INV, 4>(x[1], x[5], e[1], o[1]);
+    bfly32<INV, 8>(x[2], x[6], e[2], o[2]);
+    bfly32<INV, 12>(x[3], x[7], e[3], o[3]);
 }
 
 template <bool INV> __device__ __forceinline__ void dft16(float2* x) {
-    // cos/sin(pi k / 8), k = 0..7
-    constexpr float C16[8] = {1.0f, 0.92387953251128675613f, 0.70710678118654752440f, 0.38268343236508977173f,
-                              0.0f, -0.38268343236508977173f, -0.70710678118654752440f, -0.92387953251128675613f};
-    constexpr float S16[8] = {0.0f, 0.38268343236508977173f, 0.70710678118654752440f, 0.92387953251128675613f,
-                              1.0f, 0.92387953251128675613f, 0.70710678118654752440f, 0.38268343236508977173f};
     float2 e[8], o[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -94,14 +140,15 @@ template <bool INV> __device__ __forceinline__ void dft16(float2* x) {
     }
     dft8<INV>(e);
     dft8<INV>(o);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        // W16^k = cos - (+) j sin for forward (inverse)
-        const float2 w = make_float2(C16[k], INV ? S16[k] : -S16[k]);
-        const float2 t = (k == 0) ? o[0] : cmul(o[k], w);
-        x[k] = cadd(e[k], t);
-        x[k + 8] = csub(e[k], t);
-    }
+    // W_16^k = W_32^{2k}
+    bfly32<INV, 0>(x[0], x[8], e[0], o[0]);
+    bfly32<INV, 2>(x[1], x[9], e[1], o[1]);
+    bfly32<INV, 4>(x[2], x[10], e[2], o[2]);
+    bfly32<INV, 6>(x[3], x[11], e[3], o[3]);
+    bfly32<INV, 8>(x[4], x[12], e[4], o[4]);
+    bfly32<INV, 10>(x[5], x[13], e[5], o[5]);
+    bfly32<INV, 12>(x[6], x[14], e[6], o[6]);
+    bfly32<INV, 14>(x[7], x[15], e[7], o[7]);
 }
 
 template <int R, bool INV> __device__ __forceinline__ void dft_r(float2* x) {

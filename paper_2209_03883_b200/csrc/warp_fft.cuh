@@ -18,52 +18,9 @@
 
 namespace ofdmr {
 
-template <int K> struct W32c {
-    // compile-time W_32^K = cos - (+) j sin (forward / inverse)
-    static constexpr float c() {
-        constexpr float t[32] = {
-            1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
-            0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f, 0.19509032201612826785f,
-            0.0f, -0.19509032201612826785f, -0.38268343236508977173f, -0.55557023301960222474f,
-            -0.70710678118654752440f, -0.83146961230254523708f, -0.92387953251128675613f, -0.98078528040323044913f,
-            -1.0f, -0.98078528040323044913f, -0.92387953251128675613f, -0.83146961230254523708f,
-            -0.70710678118654752440f, -0.55557023301960222474f, -0.38268343236508977173f, -0.19509032201612826785f,
-            0.0f, 0.19509032201612826785f, 0.38268343236508977173f, 0.55557023301960222474f,
-            0.70710678118654752440f, 0.83146961230254523708f, 0.92387953251128675613f, 0.98078528040323044913f};
-        return t[K % 32];
-    }
-    static constexpr float s() {
-        constexpr float t[32] = {
-            0.0f, 0.19509032201612826785f, 0.38268343236508977173f, 0.55557023301960222474f,
-            0.70710678118654752440f, 0.83146961230254523708f, 0.92387953251128675613f, 0.98078528040323044913f,
-            1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
-            0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f, 0.19509032201612826785f,
-            0.0f, -0.19509032201612826785f, -0.38268343236508977173f, -0.55557023301960222474f,
-            -0.70710678118654752440f, -0.83146961230254523708f, -0.92387953251128675613f, -0.98078528040323044913f,
-            -1.0f, -0.98078528040323044913f, -0.92387953251128675613f, -0.83146961230254523708f,
-            -0.70710678118654752440f, -0.55557023301960222474f, -0.38268343236508977173f, -0.19509032201612826785f};
-        return t[K % 32];
-    }
-};
-
-template <bool INV, int K> __device__ __forceinline__ float2 mul_w32(float2 a) {
-    constexpr int k = K % 32;
-    if constexpr (k == 0) return a;
-    else if constexpr (k == 8) return mul_w4<INV>(a);
-    else if constexpr (k == 16) return make_float2(-a.x, -a.y);
-    else if constexpr (k == 24) return mul_w4<!INV>(a);
-    else {
-        constexpr float c = W32c<k>::c();
-        constexpr float s = INV ? W32c<k>::s() : -W32c<k>::s();
-        return make_float2(c * a.x - s * a.y, c * a.y + s * a.x);
-    }
-}
-
 template <bool INV, int K>
 __device__ __forceinline__ void dft32_step(float2* x, const float2* e, const float2* o) {
-    const float2 t = mul_w32<INV, K>(o[K]);
-    x[K] = cadd(e[K], t);
-    x[K + 16] = csub(e[K], t);
+    bfly32<INV, K>(x[K], x[K + 16], e[K], o[K]);
 }
 
 template <bool INV, int... Ks>
