@@ -290,7 +290,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=8192)
-    ap.add_argument("--pool", type=int, default=64, help="distinct generated frames tiled into the batch")
+    ap.add_argument("--pool", type=int, default=64, help="CPU-generated frames (e2e host buffers, CPU baseline)")
+    ap.add_argument("--tiled-pool", action="store_true", help="tile the CPU pool instead of GPU-generating the batch")
     ap.add_argument("--chunk", type=int, default=0, help="frames per launch chunk (0 = library default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -317,6 +318,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    from paper_2209_03883_b200 import gen
     from paper_2209_03883_b200.receiver import Receiver
 
     from paper_2209_03883_b200.shard import shard_range
@@ -324,19 +326,27 @@ def main():
     F = cfg.frames
     lo, hi = shard_range(F, rank, world)
     nf = hi - lo
-    pool = make_pool(cfg, lo, min(args.pool, nf))
+    pool = make_pool(cfg, lo, min(args.pool, nf))  # CPU-generated: e2e host buffers, CPU baseline
     P = len(pool.y)
     reps = -(-nf // P)
-    with torch.no_grad():
-        yp = torch.from_numpy(pool.y).to(dev)
-        xp = torch.from_numpy(pool.x).to(dev)
-        y = yp.repeat(reps, 1, 1)[:nf].contiguous()
-        x = xp.repeat(reps, 1, 1)[:nf].contiguous()
-        del yp, xp
-    s2_host = np.ascontiguousarray(np.tile(pool.sigma2, reps)[:nf])
-    k_host = np.ascontiguousarray(np.tile(pool.n_targets, reps)[:nf].astype(np.int32))
-    s2 = torch.from_numpy(s2_host).to(dev)
-    kf = torch.from_numpy(k_host).to(dev)
+    if args.tiled_pool:
+        with torch.no_grad():
+            yp = torch.from_numpy(pool.y).to(dev)
+            xp = torch.from_numpy(pool.x).to(dev)
+            y = yp.repeat(reps, 1, 1)[:nf].contiguous()
+            x = xp.repeat(reps, 1, 1)[:nf].contiguous()
+            del yp, xp
+        s2 = torch.from_numpy(np.ascontiguousarray(np.tile(pool.sigma2, reps)[:nf])).to(dev)
+        kf = torch.from_numpy(np.ascontiguousarray(np.tile(pool.n_targets, reps)[:nf].astype(np.int32))).to(dev)
+        data_note = f"synthetic: seeded CPU generator, {P} distinct frames per rank tiled to {nf}"
+    else:
+        # every frame of the shard distinct: the seeded generator run on the GPU
+        # (csrc/gen_kernels.cu, same streams as the CPU generator)
+        g = gen.frames_device(cfg, lo, nf, device=dev)
+        y, x, s2, kf = g["y"], g["x"], g["sigma2"], g["n_targets"]
+        del g
+        data_note = (f"synthetic: seeded generator run on the GPU (csrc/gen_kernels.cu), frames [{lo}, {hi}) of "
+                     f"base seed {cfg.base_seed}, all distinct")
 
     from paper_2209_03883_b200.shard import DetectionGather
 
@@ -515,7 +525,7 @@ def main():
             "metric": "range-Doppler frames/sec (1024x256 c64)", "value": value, "unit": "frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 (c64 FFT); fp64 threshold/sigma",
-            "data": f"synthetic: seeded generator, {P} distinct frames per rank tiled to {nf}",
+            "data": data_note,
             "config": {"workload": "cfg4: 8192 frames 1024x256 c64 QPSK, 3-8 targets, SNR U[-10,20] dB; LS -> "
                                    "DFT-CE(L=128) -> Hamming 2-D periodogram 1024x256 -> top-K_f, detections "
                                    "gathered to rank 0",

@@ -103,6 +103,11 @@ RECEIVER_SYMBOLS = [
     ("ofdmr_sft", i32, [vp, vp, i32, i32, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
 ]
 
+# include/ofdmr_gen.h, device side (in the CUDA library)
+DEVICE_GEN_SYMBOLS = [
+    ("ofdmr_gen_device", i32, [C.POINTER(GenParams), u64, i64, i64, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp]),
+]
+
 GEN_SYMBOLS = [
     ("ofdmr_derive_seed", u64, [u64, u64]),
     ("ofdmr_gen_frame", i32, [C.POINTER(GenParams), u64, i64, vp, vp, vp, vp, vp, vp, vp, i32]),
@@ -136,7 +141,7 @@ def lib() -> C.CDLL:
                 f"{LIB_PATH} is missing: build it with `python -m paper_2209_03883_b200.build` "
                 "(there is no CPU fallback for the receiver path)"
             )
-        _lib = _bind(C.CDLL(str(LIB_PATH)), RECEIVER_SYMBOLS)
+        _lib = _bind(C.CDLL(str(LIB_PATH)), RECEIVER_SYMBOLS + DEVICE_GEN_SYMBOLS)
     return _lib
 
 

@@ -42,7 +42,7 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 
 def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
     out = PKG / "libofdmr_b200.so"
-    headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "ofdmr_b200.h"]
+    headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "ofdmr_b200.h", ROOT / "include" / "ofdmr_gen.h"]
     units = {
         "radar_kernels": [],
         "fast_kernels": [],
@@ -51,6 +51,8 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "capi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions
         "sft_kernels": ["-fmad=false"],
+        # GPU frame generator: the CPU generator's fp64 operation order (no FMA contraction)
+        "gen_kernels": ["-fmad=false"],
     }
     deps = [CSRC / f"{u}.cu" for u in units] + headers
     if not force and not _stale(out, deps):
@@ -72,7 +74,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
 def build_gen(force: bool = False) -> Path:
     out = PKG / "libofdmr_gen.so"
     src = CSRC / "gen.cpp"
-    if force or _stale(out, [src]):
+    if force or _stale(out, [src, ROOT / "include" / "ofdmr_gen.h"]):
         # default x86-64 codegen (no FMA) like the reference's Release build
         _run(["g++", "-O3", "-DNDEBUG", "-std=c++17", "-fPIC", "-shared", "-o", str(out), str(src), "-lpthread"])
     return out

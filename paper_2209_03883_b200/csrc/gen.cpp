@@ -27,6 +27,8 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/ofdmr_gen.h"
+
 namespace {
 
 using cplx = std::complex<double>;
@@ -105,19 +107,7 @@ std::vector<cplx> constellation(int order) {
 
 extern "C" {
 
-/// Generator parameters for one configuration (all frames of a batch share them).
-typedef struct ofdmr_gen_params {
-    int32_t n, m;            // subcarriers N, OFDM symbols M
-    double df_hz, fc_hz;     // subcarrier spacing, carrier
-    int32_t n_cp;            // CP samples (sets Ts)
-    int32_t qam_order;       // 4/16/64/256
-    int32_t zc_precode;      // 0: none; 1: direct D = N layout, sequence length N^2
-    int64_t zc_root;
-    int32_t targets_min, targets_max;
-    double range_lo, range_hi;
-    double vel_lo, vel_hi;
-    double snr_lo_db, snr_hi_db;  // equal => fixed SNR; +inf => noiseless
-} ofdmr_gen_params;
+/// Generator parameters: include/ofdmr_gen.h
 
 uint64_t ofdmr_derive_seed(uint64_t base, uint64_t stream) { return derive_seed(base, stream); }
 

@@ -1,0 +1,443 @@
+// GPU frame generator: the CPU generator (csrc/gen.cpp, itself a
+// restatement of the reference's make_random_frame / apply_channel / Rng, see the header of
+// include/ofdmr_gen.h) executed on the device, one CTA (256 threads) per frame, so 8192-frame
+// runs need no PCIe traffic.
+//
+// Every random stream is the reference's std::mt19937_64 stream:
+//   scene   Rng(derive_seed(fs, 0x7363656e))   thread 0, sequential
+//   phases  Rng(derive_seed(fs, 0x70686173))   thread 0, sequential  (channel.cpp:74-83)
+//   pilots  Rng(derive_seed(fx, 0))            warp 0, parallel twist (waveform.cpp:92-96)
+//   payload Rng(derive_seed(fx, 1))            warp 0, parallel twist (waveform.cpp:97-108)
+//   noise   Rng(derive_seed(fs, 0x6e6f6973))   warp 0, parallel twist (channel.cpp:90-95)
+// with fs = derive_seed(base_seed, frame), fx = derive_seed(fs, 0x667261).  The twist is
+// parallelised across the warp in its two data-independent halves; draws are consumed in the
+// reference's order: one pilot per subcarrier row, bps payload bits per payload cell
+// (MSB first), one Box-Muller pair per cell with the imaginary part taking the first normal
+// (GCC evaluates `cplx(sd*normal(), sd*normal())` right to left, checked in
+// tests/test_gpu_parity.py against the CPU generator).  Rejection draws (uniform_int at
+// v >= limit, Box-Muller at u1 == 0; probability ~2^-50 per frame) set status bit 0 and the
+// host regenerates that frame on the CPU.
+//
+// Arithmetic is fp64 in the CPU code's operation order (compiled with -fmad=false, IEEE
+// div/sqrt); sin/cos/log/pow are the GPU's (<= 2 ulp), so rare c64 cells differ by 1 ulp.
+// mean_power(x) is summed sequentially in cell order by one thread, as the CPU does.
+// Pass 1 writes x_tx (and the running |x|^2 sum); pass 2 re-reads x_tx (exact decode of the
+// c64 value back to its fp64 constellation point), applies the channel and adds the noise.
+#include <cmath>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/ofdmr_gen.h"
+
+namespace ofdmr {
+namespace {
+
+constexpr double kTwoPiG = 6.283185307179586476925286766559;
+constexpr double kCG = 3.0e8;
+constexpr int kMtN = 312, kMtM = 156;
+constexpr uint64_t kMatA = 0xB5026F5AA96619E9ull;
+constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull;
+constexpr int kMaxT = 16;
+constexpr int kMaxM = 1024;
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t base, uint64_t stream) {
+    // rng.hpp derive_seed (SplitMix64 of base ^ golden * (stream + 1))
+    uint64_t z = base + 0x9E3779B97F4A7C15ull * (stream + 1ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t temper(uint64_t y) {
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+}
+__device__ __forceinline__ uint64_t twist1(uint64_t a, uint64_t b, uint64_t m) {
+    const uint64_t x = (a & kUpper) | (b & kLower);
+    return m ^ (x >> 1) ^ ((x & 1ull) ? kMatA : 0ull);
+}
+
+// init_genrand64 (sequential; one thread)
+__device__ void mt_seed(uint64_t* mt, uint64_t seed) {
+    mt[0] = seed;
+    for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+}
+
+// Scalar generator for the short streams (thread 0 only).
+struct MtScalar {
+    uint64_t* mt;
+    int idx;
+    __device__ uint64_t next() {
+        if (idx >= kMtN) {
+            for (int i = 0; i < kMtN; ++i) mt[i] = twist1(mt[i], mt[(i + 1) % kMtN], mt[(i + kMtM) % kMtN]);
+            idx = 0;
+        }
+        return temper(mt[idx++]);
+    }
+    __device__ double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+    __device__ double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    __device__ uint64_t uniform_int(uint64_t n, int& rej) {
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+        uint64_t v;
+        do {
+            v = next();
+            if (v >= limit) rej = 1;
+        } while (v >= limit);
+        return v % n;
+    }
+};
+
+// Warp-parallel twist + temper: appends 312 outputs to the ring out[(pos + i) & mask].
+__device__ void mt_block(uint64_t* mt, uint64_t* out, uint32_t pos, uint32_t mask) {
+    const int lane = threadIdx.x & 31;
+    // first half: i < 156 reads only old words
+    for (int b = 0; b < kMtM; b += 32) {
+        const int i = b + lane;
+        uint64_t v = 0;
+        if (i < kMtM) v = twist1(mt[i], mt[i + 1], mt[i + kMtM]);
+        __syncwarp();
+        if (i < kMtM) mt[i] = v;
+        __syncwarp();
+    }
+    // second half: 156 <= i < 311 reads old mt[i], mt[i+1] and new mt[i-156]
+    for (int b = kMtM; b < kMtN - 1; b += 32) {
+        const int i = b + lane;
+        uint64_t v = 0;
+        if (i < kMtN - 1) v = twist1(mt[i], mt[i + 1], mt[i - kMtM]);
+        __syncwarp();
+        if (i < kMtN - 1) mt[i] = v;
+        __syncwarp();
+    }
+    if (lane == 0) mt[kMtN - 1] = twist1(mt[kMtN - 1], mt[0], mt[kMtM - 1]);
+    __syncwarp();
+    for (int i = lane; i < kMtN; i += 32) out[(pos + i) & mask] = temper(mt[i]);
+    __syncwarp();
+}
+
+struct GenArgs {
+    ofdmr_gen_params p;
+    uint64_t base_seed;
+    int64_t first;
+    int count;
+    float2* y;
+    float2* x;
+    double* sigma2;
+    int32_t* n_targets;
+    double* ranges;
+    double* vels;
+    double* snr_db;
+    int max_targets;
+    int32_t* status;
+    int bps;
+    int levels;             // per-axis constellation levels
+    double lev_d[16];       // axis level values (fp64, gen.cpp's li * scale), by Gray-decoded index
+    float lev_f[16];        // the same rounded to fp32 (decode of the stored c64 x)
+    int lev_of_gray[16];    // Gray code -> level index
+    double inv_sqrt2;
+    uint32_t ring_mask;     // ring size - 1 (power of two >= bits per row + 312)
+};
+
+struct GenShared {
+    uint64_t mt[kMtN];
+    int ntar;
+    int rej;
+    double snr_db;
+    double b_re[kMaxT], b_im[kMaxT], delay[kMaxT], dopp[kMaxT];
+    double d_re[kMaxT], d_im[kMaxT];  // this row's delay phasors
+    double mp;                        // running sequential sum of |x|^2
+    double sd;
+};
+
+// dynamic smem after GenShared: fph[kMaxT][M] double2, nrm[2][M] double, pilot codes [N] bytes,
+// draw ring [ring] u64
+__global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
+    extern __shared__ __align__(16) unsigned char gsm[];
+    GenShared& s = *reinterpret_cast<GenShared*>(gsm);
+    const ofdmr_gen_params& p = a.p;
+    const int n = p.n, m = p.m, tid = threadIdx.x, w = tid >> 5;
+    double2* fph = reinterpret_cast<double2*>(gsm + ((sizeof(GenShared) + 15) & ~size_t(15)));
+    double* nrm = reinterpret_cast<double*>(fph + (size_t)kMaxT * m);
+    uint64_t* ring = reinterpret_cast<uint64_t*>(nrm + 2 * m);
+    unsigned char* pil = reinterpret_cast<unsigned char*>(ring + a.ring_mask + 1);
+
+    const int f = blockIdx.x;
+    const int64_t fidx = a.first + f;
+    const uint64_t fs = splitmix(a.base_seed, (uint64_t)fidx);
+    const uint64_t fx = splitmix(fs, 0x667261ull);
+    float2* xo = a.x + (size_t)f * n * m;
+    float2* yo = a.y + (size_t)f * n * m;
+
+    // ---- scene + per-target constants (thread 0, sequential streams)
+    if (tid == 0) {
+        int rej = 0;
+        MtScalar r{s.mt, kMtN};
+        mt_seed(s.mt, splitmix(fs, 0x7363656eull));
+        int cnt = p.targets_min;
+        if (p.targets_max > p.targets_min) cnt += (int)r.uniform_int((uint64_t)(p.targets_max - p.targets_min + 1), rej);
+        double rg[kMaxT], vl[kMaxT];
+        for (int t = 0; t < cnt; ++t) {
+            rg[t] = r.uniform(p.range_lo, p.range_hi);
+            vl[t] = r.uniform(p.vel_lo, p.vel_hi);
+        }
+        double snr = p.snr_lo_db;
+        if (p.snr_hi_db != p.snr_lo_db && isfinite(p.snr_lo_db)) snr = r.uniform(p.snr_lo_db, p.snr_hi_db);
+        // phases (channel.cpp:74-83)
+        MtScalar ph{s.mt, kMtN};
+        mt_seed(s.mt, splitmix(fs, 0x70686173ull));
+        for (int t = 0; t < cnt; ++t) {
+            const double phase = ph.uniform(0.0, kTwoPiG);
+            const double gain = 1.0;
+            s.delay[t] = 2.0 * rg[t] / kCG;
+            s.dopp[t] = 2.0 * vl[t] * p.fc_hz / kCG;
+            double sn, cs;
+            sincos(phase, &sn, &cs);
+            s.b_re[t] = gain * cs;
+            s.b_im[t] = gain * sn;
+        }
+        s.ntar = cnt;
+        s.rej = rej;
+        s.snr_db = snr;
+        s.mp = 0.0;
+        a.n_targets[f] = cnt;
+        if (a.snr_db) a.snr_db[f] = snr;
+        for (int t = 0; t < cnt && t < a.max_targets; ++t) {
+            if (a.ranges) a.ranges[(size_t)f * a.max_targets + t] = rg[t];
+            if (a.vels) a.vels[(size_t)f * a.max_targets + t] = vl[t];
+        }
+    }
+    __syncthreads();
+    const int T = s.ntar;
+    const double t_useful = 1.0 / p.df_hz;
+    const double ts = t_useful + (double)p.n_cp * (t_useful / (double)n);
+    for (int i = tid; i < T * m; i += 256) {
+        const int t = i / m, l = i % m;
+        double sn, cs;
+        sincos(kTwoPiG * (double)l * ts * s.dopp[t], &sn, &cs);
+        fph[(size_t)t * m + l] = make_double2(1.0 * cs, 1.0 * sn);
+    }
+
+    // ---- pilots: n draws of uniform_int(4) (warp 0)
+    const uint32_t mask = a.ring_mask;
+    if (w == 0) {
+        if (tid == 0) mt_seed(s.mt, splitmix(fx, 0ull));
+        __syncwarp();
+        int rej = 0;
+        for (int k0 = 0; k0 < n; k0 += kMtN) {
+            mt_block(s.mt, ring, 0, mask);
+            for (int i = tid; i < kMtN && k0 + i < n; i += 32) {
+                const uint64_t v = ring[i];
+                if (v >= 0xFFFFFFFFFFFFFFFCull) rej = 1;
+                pil[k0 + i] = (unsigned char)(v % 4);
+            }
+            __syncwarp();
+        }
+        if (__any_sync(0xffffffffu, rej) && tid == 0) s.rej = 1;
+        if (tid == 0) mt_seed(s.mt, splitmix(fx, 1ull));  // payload stream
+    }
+    __syncthreads();
+
+    // ---- pass 1: x_tx row by row; mean_power summed sequentially (warp 1, lane 0)
+    const int bps = a.bps, half = bps / 2;
+    const uint32_t need = (uint32_t)(m - 1) * bps;  // payload draws per row
+    uint32_t produced = 0, consumed = 0;             // warp 0 bookkeeping (uniform in the CTA)
+    for (int k = 0; k < n; ++k) {
+        if (w == 0) {
+            while (produced < consumed + need) {
+                mt_block(s.mt, ring, produced, mask);
+                produced += kMtN;
+            }
+        } else {
+            while (produced < consumed + need) produced += kMtN;  // keep the counters uniform
+        }
+        __syncthreads();
+        double* nr = nrm + (k & 1) * m;
+        for (int l = tid; l < m; l += 256) {
+            double xr, xi;
+            if (l == 0) {
+                const unsigned b = pil[k];
+                xr = (b & 1) ? -a.inv_sqrt2 : a.inv_sqrt2;
+                xi = (b & 2) ? -a.inv_sqrt2 : a.inv_sqrt2;
+            } else {
+                unsigned wd = 0;
+                const uint32_t base = consumed + (uint32_t)(l - 1) * bps;
+                for (int b = 0; b < bps; ++b) {
+                    const uint64_t v = ring[(base + b) & mask];
+                    if (v >= 0xFFFFFFFFFFFFFFFEull) atomicOr(&s.rej, 1);
+                    wd = (wd << 1) | (unsigned)(v & 1ull);
+                }
+                const unsigned gi = wd >> half, gq = wd & ((1u << half) - 1u);
+                xr = a.lev_d[a.lev_of_gray[gi]];
+                xi = a.lev_d[a.lev_of_gray[gq]];
+            }
+            xo[(size_t)k * m + l] = make_float2((float)xr, (float)xi);
+            nr[l] = xr * xr + xi * xi;
+        }
+        consumed += need;
+        __syncthreads();
+        if (tid == 32) {  // sequential sum of this row (gen.cpp mean_power order)
+            double acc = s.mp;
+            for (int l = 0; l < m; ++l) acc += nr[l];
+            s.mp = acc;
+        }
+    }
+    __syncthreads();
+
+    // ---- sigma2 (channel.cpp:86-89) and the noise stream
+    const bool noisy = isfinite(s.snr_db);
+    if (tid == 0) {
+        double sigma2 = 0.0;
+        if (noisy) {
+            const double snr_lin = pow(10.0, s.snr_db / 10.0);
+            double tg = 0.0;
+            for (int t = 0; t < T; ++t) tg += 1.0 * 1.0;
+            const double ref_gain2 = T == 0 ? 1.0 : tg;
+            const double mp = s.mp / (double)((size_t)n * m);
+            sigma2 = ref_gain2 * mp / snr_lin;
+        }
+        s.sd = sqrt(sigma2 / 2.0);
+        a.sigma2[f] = sigma2;
+        mt_seed(s.mt, splitmix(fs, 0x6e6f6973ull));
+    }
+    __syncthreads();
+
+    // ---- pass 2: channel + noise, row by row
+    produced = 0;
+    consumed = 0;
+    const uint32_t need2 = noisy ? 2u * (uint32_t)m : 0u;
+    const double sd = s.sd;
+    for (int k = 0; k < n; ++k) {
+        if (w == 0) {
+            while (produced < consumed + need2) {
+                mt_block(s.mt, ring, produced, mask);
+                produced += kMtN;
+            }
+        } else {
+            while (produced < consumed + need2) produced += kMtN;
+        }
+        if (tid < T) {
+            double sn, cs;
+            sincos(-kTwoPiG * (double)k * p.df_hz * s.delay[tid], &sn, &cs);
+            s.d_re[tid] = 1.0 * cs;
+            s.d_im[tid] = 1.0 * sn;
+        }
+        __syncthreads();
+        for (int l = tid; l < m; l += 256) {
+            // exact fp64 x from the stored c64 value
+            const float2 xf = xo[(size_t)k * m + l];
+            double xr, xi;
+            if (l == 0) {
+                xr = xf.x < 0.f ? -a.inv_sqrt2 : a.inv_sqrt2;
+                xi = xf.y < 0.f ? -a.inv_sqrt2 : a.inv_sqrt2;
+            } else {
+                int ir = 0, iq = 0;
+                for (int q = 0; q < a.levels; ++q) {
+                    if (a.lev_f[q] == xf.x) ir = q;
+                    if (a.lev_f[q] == xf.y) iq = q;
+                }
+                xr = a.lev_d[ir];
+                xi = a.lev_d[iq];
+            }
+            double yr = 0.0, yi = 0.0;
+            for (int t = 0; t < T; ++t) {
+                // row = b * dph[k]; y += row * fph[l] * x  (std::complex products, left to right)
+                const double rr = s.b_re[t] * s.d_re[t] - s.b_im[t] * s.d_im[t];
+                const double ri = s.b_re[t] * s.d_im[t] + s.b_im[t] * s.d_re[t];
+                const double2 fp = fph[(size_t)t * m + l];
+                const double t1r = rr * fp.x - ri * fp.y;
+                const double t1i = rr * fp.y + ri * fp.x;
+                const double t2r = t1r * xr - t1i * xi;
+                const double t2i = t1r * xi + t1i * xr;
+                yr = yr + t2r;
+                yi = yi + t2i;
+            }
+            if (noisy) {
+                const uint64_t v1 = ring[(consumed + 2u * l) & mask];
+                const uint64_t v2 = ring[(consumed + 2u * l + 1u) & mask];
+                const double u1 = (double)(v1 >> 11) * 0x1.0p-53;
+                const double u2 = (double)(v2 >> 11) * 0x1.0p-53;
+                if (u1 <= 0.0) atomicOr(&s.rej, 1);
+                const double r = sqrt(-2.0 * log(u1));
+                const double ang = kTwoPiG * u2;
+                double sn, cs;
+                sincos(ang, &sn, &cs);
+                // imaginary part takes the first normal (r cos), real part the cached r sin
+                yr = yr + sd * (r * sn);
+                yi = yi + sd * (r * cs);
+            }
+            yo[(size_t)k * m + l] = make_float2((float)yr, (float)yi);
+        }
+        consumed += need2;
+        __syncthreads();
+    }
+    if (tid == 0) a.status[f] = s.rej ? 1 : 0;
+}
+
+int gray_decode_h(unsigned g) {
+    unsigned b = 0;
+    for (; g; g >>= 1) b ^= g;
+    return (int)b;
+}
+
+}  // namespace
+}  // namespace ofdmr
+
+extern "C" int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int64_t count, void* y,
+                                void* x_tx, double* sigma2, int32_t* n_targets, double* ranges, double* vels,
+                                double* snr_db, int32_t max_targets, int32_t* status, void* stream) {
+    using namespace ofdmr;
+    if (!p || !y || !x_tx || !sigma2 || !n_targets || !status || count < 0) return 2;
+    if (count == 0) return 0;
+    int bps = 0;
+    switch (p->qam_order) {
+        case 4: bps = 2; break;
+        case 16: bps = 4; break;
+        case 64: bps = 6; break;
+        case 256: bps = 8; break;
+        default: return 2;
+    }
+    if (p->zc_precode || p->n <= 0 || p->m < 2 || p->m > kMaxM || p->targets_max > kMaxT || p->targets_min < 0 ||
+        p->targets_max < p->targets_min || count > (int64_t)1 << 30)
+        return 2;
+    GenArgs a{};
+    a.p = *p;
+    a.base_seed = base_seed;
+    a.first = first;
+    a.count = (int)count;
+    a.y = static_cast<float2*>(y);
+    a.x = static_cast<float2*>(x_tx);
+    a.sigma2 = sigma2;
+    a.n_targets = n_targets;
+    a.ranges = ranges;
+    a.vels = vels;
+    a.snr_db = snr_db;
+    a.max_targets = max_targets;
+    a.status = status;
+    a.bps = bps;
+    // constellation axis levels exactly as gen.cpp constellation(): li = (L-1) - 2*gray_decode(g)
+    const int half = bps / 2, levels = 1 << half;
+    const double scale = 1.0 / std::sqrt(2.0 * (double(levels) * levels - 1.0) / 3.0);
+    a.levels = levels;
+    for (int g = 0; g < levels; ++g) {
+        const int q = gray_decode_h((unsigned)g);
+        a.lev_of_gray[g] = q;
+        const double li = double(levels - 1) - 2.0 * q;
+        a.lev_d[q] = li * scale;
+        a.lev_f[q] = (float)a.lev_d[q];
+    }
+    a.inv_sqrt2 = 1.0 / std::sqrt(2.0);
+    uint32_t ring = 1;
+    const uint32_t need = (uint32_t)std::max((p->m - 1) * bps, 2 * p->m) + kMtN;
+    while (ring < need) ring <<= 1;
+    if (ring < 512) ring = 512;
+    a.ring_mask = ring - 1;
+    const size_t smem = ((sizeof(GenShared) + 15) & ~size_t(15)) + sizeof(double2) * kMaxT * p->m +
+                        sizeof(double) * 2 * p->m + sizeof(uint64_t) * ring + (size_t)p->n;
+    cudaError_t e = cudaFuncSetAttribute(gen_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return 10;
+    gen_frame_kernel<<<(unsigned)count, 256, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}

@@ -92,3 +92,46 @@ def rng_u64(seed: int, count: int) -> np.ndarray:
     out = np.empty(count, np.uint64)
     _native.gen().ofdmr_rng_u64(seed, count, _ptr(out))
     return out
+
+
+def frames_device(cfg: RadarConfig, first: int = 0, count: int | None = None, device=None):
+    """GPU generator (csrc/gen_kernels.cu, include/ofdmr_gen.h): frames [first, first+count)
+    generated in device memory, same streams and arithmetic order as `frames` (rare 1-ulp c64
+    differences from the GPU's fp64 sin/cos/log/pow).  Frames that hit an MT19937 rejection
+    draw (status bit 0, probability ~2^-50) are regenerated with the CPU generator.
+    Returns a dict of torch tensors: y, x (complex64 [F, N, M]), sigma2 (float64), n_targets
+    (int32), ranges, vels ([F, MAX_T] float64), snr_db (float64)."""
+    import torch
+
+    count = cfg.frames if count is None else count
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    out = {
+        "y": torch.empty(count, cfg.n, cfg.m, dtype=torch.complex64, device=dev),
+        "x": torch.empty(count, cfg.n, cfg.m, dtype=torch.complex64, device=dev),
+        "sigma2": torch.empty(count, dtype=torch.float64, device=dev),
+        "n_targets": torch.empty(count, dtype=torch.int32, device=dev),
+        "ranges": torch.zeros(count, MAX_T, dtype=torch.float64, device=dev),
+        "vels": torch.zeros(count, MAX_T, dtype=torch.float64, device=dev),
+        "snr_db": torch.empty(count, dtype=torch.float64, device=dev),
+    }
+    status = torch.empty(count, dtype=torch.int32, device=dev)
+    p = gen_params(cfg)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = _native.lib().ofdmr_gen_device(C.byref(p), cfg.base_seed, first, count, out["y"].data_ptr(),
+                                         out["x"].data_ptr(), out["sigma2"].data_ptr(), out["n_targets"].data_ptr(),
+                                         out["ranges"].data_ptr(), out["vels"].data_ptr(), out["snr_db"].data_ptr(),
+                                         MAX_T, status.data_ptr(), C.c_void_p(stream))
+    if rc:
+        raise RuntimeError(f"ofdmr_gen_device failed ({rc}): {_native.last_error()}")
+    bad = torch.nonzero(status).flatten().tolist()
+    for i in bad:  # exact CPU regeneration of the (astronomically rare) rejection frames
+        fb = frames(cfg, first + i, 1, threads=1)
+        out["y"][i] = torch.from_numpy(fb.y[0]).to(dev)
+        out["x"][i] = torch.from_numpy(fb.x[0]).to(dev)
+        out["sigma2"][i] = float(fb.sigma2[0])
+        out["n_targets"][i] = int(fb.n_targets[0])
+        out["ranges"][i] = torch.from_numpy(fb.ranges[0]).to(dev)
+        out["vels"][i] = torch.from_numpy(fb.vels[0]).to(dev)
+        out["snr_db"][i] = float(fb.snr_db[0])
+    out["regenerated_on_cpu"] = len(bad)
+    return out

@@ -37,6 +37,13 @@ def test_generator_symbols():
     g = _native.gen()
     for name, _, _ in _native.GEN_SYMBOLS:
         assert hasattr(g, name)
+    # include/ofdmr_gen.h: the device generator lives in the CUDA library
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "ofdmr_gen.h").read_text(), flags=re.S)
+    declared = set(re.findall(r"\b(ofdmr_[a-z_0-9]+)\s*\(", text))
+    assert declared == {name for name, _, _ in _native.DEVICE_GEN_SYMBOLS}
+    lib = _native.lib()
+    for s in declared:
+        assert hasattr(lib, s), s
 
 
 def test_host_helpers_match_reference_formulas():
