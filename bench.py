@@ -280,6 +280,32 @@ def extra_configs(args, dev, local, threads):
     out["cfg3_fps_sft"] = r3
     del hd
     rx.close()
+
+    # §8(f) item 2: Monte-Carlo RMSE sweep (metrics.cpp:92-120) on the GPU generator + fused
+    # receiver, against the reference's own rmse_sweep (single-threaded, as the reference runs it)
+    from paper_2209_03883_b200 import montecarlo as mc
+    mcfg = configs.CFG1
+    rng_t, vel_t = np.array([8.0, 17.5, 31.0]), np.array([-35.0, 12.0, 60.0])
+    grid = [-15.0, -5.0, 5.0]
+    mc.rmse_sweep(mcfg, rng_t, vel_t, grid[:1], 64, 1)  # warm-up
+    trials = 4096
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rows = mc.rmse_sweep(mcfg, rng_t, vel_t, grid, trials, 2022)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    rmc = {"scenario": "cfg1 numerology, 3 fixed targets, SNR grid [-15, -5, 5] dB, DFT-CE L=128, Hamming",
+           "trials_per_snr": trials, "gpu_trials_per_s": len(grid) * trials / dt,
+           "rows": [[r.snr_db, r.range_rmse_m, r.velocity_rmse_mps, r.miss_rate] for r in rows],
+           "note": "wall clock incl. host matching; GPU generator + fused pipeline per batch of 2048 trials"}
+    if O.ref_available():
+        nt = 8
+        t0 = time.perf_counter()
+        O.ref_rmse_sweep((mcfg.n, mcfg.m, mcfg.n_prime, mcfg.m_prime, mcfg.df_hz, 77e9, mcfg.n_cp, mcfg.window,
+                          mcfg.pfa, mcfg.estimator, rng_t, vel_t), grid[:1], nt, 2022)
+        rmc["cpu_reference_trials_per_s"] = nt / (time.perf_counter() - t0)
+        rmc["cpu_threads"] = 1
+    out["monte_carlo_rmse_sweep"] = rmc
     return out
 
 

@@ -47,6 +47,14 @@ int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, int64_t firs
                      void* x_tx, double* sigma2, int32_t* n_targets, double* ranges, double* vels, double* snr_db,
                      int32_t max_targets, int32_t* status, void* stream);
 
+/* run_pipeline's generator half (pipeline.cpp:65-71) for a fixed scenario, as the reference's
+ * Monte-Carlo callers use it (metrics.cpp:92-120): frame i of the batch uses the run seed
+ * derive_seed(seed, first + i); targets (host arrays, <= 16) and SNR are fixed.  y, x_tx,
+ * sigma2, status as for ofdmr_gen_device.  Synchronous on `stream`. */
+int ofdmr_gen_device_explicit(const ofdmr_gen_params* p, uint64_t seed, int64_t first, int64_t count,
+                              const double* target_ranges, const double* target_vels, int32_t n_targets,
+                              double snr_db, void* y, void* x_tx, double* sigma2, int32_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,10 @@ def ref() -> C.CDLL:
             raise ImportError(f"{REF_SO} missing (built from /root/reference by `make -f oracle/Makefile ref`)")
         _ref = C.CDLL(str(REF_SO))
         i64, d = C.c_int64, C.c_double
+        _ref.ref_run_pipeline.argtypes = [i64, i64, i64, i64, d, d, i64, C.c_int, d, C.c_int, vp, vp, C.c_int32, d,
+                                          C.c_uint64, vp, vp, vp, vp, vp]
+        _ref.ref_rmse_sweep.argtypes = [i64, i64, i64, i64, d, d, i64, C.c_int, d, C.c_int, vp, vp, C.c_int32, vp,
+                                        C.c_int32, i64, C.c_uint64, vp]
         _ref.ref_receive_frame.argtypes = [i64, i64, i64, i64, C.c_int, i64, C.c_int, d, vp, vp, d, i64, vp, vp, vp,
                                            vp, vp, vp, vp]
         _ref.ref_receive_batch.argtypes = [i64, i64, i64, i64, C.c_int, i64, C.c_int, d, vp, vp, vp, i64, vp, i64, vp,
@@ -283,3 +287,34 @@ def rng_u64(seed: int, count: int) -> np.ndarray:
 
 def derive_seed(base: int, stream: int) -> int:
     return int(orc().orc_derive_seed(base, stream))
+
+
+def ref_scenario_args(n, m, n_prime, m_prime, df, fc, n_cp, window, pfa, estimator, ranges, vels):
+    r = np.ascontiguousarray(ranges, np.float64)
+    v = np.ascontiguousarray(vels, np.float64)
+    return (n, m, n_prime, m_prime, df, fc, n_cp, window, pfa, estimator, _p(r), _p(v), len(r)), (r, v)
+
+
+def ref_run_pipeline(scn, snr_db: float, seed: int):
+    """The reference's run_pipeline on a fixed scenario (oracle/_ref, test infrastructure)."""
+    args, keep = ref_scenario_args(*scn)
+    k = max(args[-1], 1)
+    d = np.zeros(k, np.int64)
+    v = np.zeros(k, np.int64)
+    r = np.zeros(k)
+    vel = np.zeros(k)
+    cnt = C.c_long()
+    rc = ref().ref_run_pipeline(*args, snr_db, seed, _p(d), _p(v), _p(r), _p(vel), C.byref(cnt))
+    assert rc == 0
+    n = cnt.value
+    return d[:n], v[:n], r[:n], vel[:n]
+
+
+def ref_rmse_sweep(scn, snr_grid, trials: int, seed: int) -> np.ndarray:
+    """The reference's rmse_sweep (metrics.cpp:92-120): rows [snr][range_rmse, vel_rmse, miss_rate]."""
+    args, keep = ref_scenario_args(*scn)
+    g = np.ascontiguousarray(snr_grid, np.float64)
+    rows = np.zeros((len(g), 3))
+    rc = ref().ref_rmse_sweep(*args, _p(g), len(g), trials, seed, _p(rows))
+    assert rc == 0
+    return rows

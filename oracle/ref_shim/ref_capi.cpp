@@ -12,7 +12,9 @@
 
 #include "ofdmradar/channel.hpp"
 #include "ofdmradar/errors.hpp"
+#include "ofdmradar/config.hpp"
 #include "ofdmradar/estimation.hpp"
+#include "ofdmradar/metrics.hpp"
 #include "ofdmradar/periodogram.hpp"
 #include "ofdmradar/pipeline.hpp"
 #include "ofdmradar/rng.hpp"
@@ -276,6 +278,74 @@ int ref_make_frame_pair(int64_t n, int64_t m, double df, double fc, int64_t n_cp
 void ref_rng_u64(uint64_t seed, int64_t count, uint64_t* out) {
     Rng r(seed);
     for (int64_t i = 0; i < count; ++i) out[i] = r.next_u64();
+}
+
+namespace {
+SimulationConfig scenario(int64_t n, int64_t m, int64_t np, int64_t mp, double df, double fc, int64_t n_cp,
+                          int window, double pfa, int estimator, const double* ranges, const double* vels,
+                          int32_t count) {
+    SimulationConfig cfg;
+    cfg.waveform = make_wave(std::size_t(n), std::size_t(m), std::size_t(np), std::size_t(mp), df, fc,
+                             std::size_t(n_cp), window, pfa);
+    for (int i = 0; i < count; ++i) {
+        RadarTarget t{};
+        t.range_m = ranges[i];
+        t.velocity_mps = vels[i];
+        cfg.targets.push_back(t);
+    }
+    cfg.estimator.kind = estimator == 1 ? EstimatorKind::DftCe : EstimatorKind::Ls;
+    cfg.detector.max_targets = std::size_t(count);
+    return cfg;
+}
+}  // namespace
+
+/// One run of the reference's run_pipeline (pipeline.cpp:60-115) on that scenario with the
+/// given run seed and SNR; detections as (delay_bin, doppler_bin, range_m, velocity_mps).
+int ref_run_pipeline(int64_t n, int64_t m, int64_t np, int64_t mp, double df, double fc, int64_t n_cp, int window,
+                     double pfa, int estimator, const double* ranges, const double* vels, int32_t count,
+                     double snr_db, uint64_t seed, long* delay, long* doppler, double* range_m, double* vel_mps,
+                     long* n_det) {
+    try {
+        SimulationConfig cfg = scenario(n, m, np, mp, df, fc, n_cp, window, pfa, estimator, ranges, vels, count);
+        cfg.channel.snr_db = snr_db;
+        const auto res = run_pipeline(cfg, seed);
+        for (std::size_t i = 0; i < res.detections.size(); ++i) {
+            delay[i] = res.detections[i].delay_bin;
+            doppler[i] = res.detections[i].doppler_bin;
+            range_m[i] = res.detections[i].range_m;
+            vel_mps[i] = res.detections[i].velocity_mps;
+        }
+        *n_det = long(res.detections.size());
+        return 0;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (...) {  // ModelValidityError (scene outside the CP / ICI bounds) and the rest
+        return 3;
+    }
+}
+
+/// The reference's own Monte-Carlo RMSE sweep (metrics.cpp:92-120) on a scenario built from
+/// plain parameters: QPSK, normalized gains, random phases, targets (ranges, vels),
+/// estimator 0 LS / 1 DFT-CE.  rows[i] = {range_rmse_m, velocity_rmse_mps, miss_rate}.
+int ref_rmse_sweep(int64_t n, int64_t m, int64_t np, int64_t mp, double df, double fc, int64_t n_cp, int window,
+                   double pfa, int estimator, const double* ranges, const double* vels, int32_t count,
+                   const double* snr_grid, int32_t n_snr, int64_t trials, uint64_t seed, double* rows) {
+    try {
+        SimulationConfig cfg = scenario(n, m, np, mp, df, fc, n_cp, window, pfa, estimator, ranges, vels, count);
+        const EstimatorKind kind = cfg.estimator.kind;
+        std::vector<double> grid(snr_grid, snr_grid + n_snr);
+        const auto out = rmse_sweep(cfg, kind, grid, std::size_t(trials), seed);
+        for (std::size_t i = 0; i < out.size(); ++i) {
+            rows[3 * i] = out[i].range_rmse_m;
+            rows[3 * i + 1] = out[i].velocity_rmse_mps;
+            rows[3 * i + 2] = out[i].miss_rate;
+        }
+        return 0;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (...) {
+        return 3;
+    }
 }
 
 }  // extern "C"

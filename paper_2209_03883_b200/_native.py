@@ -106,6 +106,8 @@ RECEIVER_SYMBOLS = [
 # include/ofdmr_gen.h, device side (in the CUDA library)
 DEVICE_GEN_SYMBOLS = [
     ("ofdmr_gen_device", i32, [C.POINTER(GenParams), u64, i64, i64, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp]),
+    ("ofdmr_gen_device_explicit", i32, [C.POINTER(GenParams), u64, i64, i64, P_f64, P_f64, i32, f64, vp, vp, vp, vp,
+                                        vp]),
 ]
 
 GEN_SYMBOLS = [

@@ -139,6 +139,10 @@ struct GenArgs {
     int lev_of_gray[16];    // Gray code -> level index
     double inv_sqrt2;
     uint32_t ring_mask;     // ring size - 1 (power of two >= bits per row + 312)
+    int explicit_scene;     // 1: fixed targets / SNR below instead of the scene stream
+    int exp_count;
+    double exp_range[kMaxT], exp_vel[kMaxT];
+    double exp_snr;
 };
 
 struct GenShared {
@@ -174,17 +178,29 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
     // ---- scene + per-target constants (thread 0, sequential streams)
     if (tid == 0) {
         int rej = 0;
-        MtScalar r{s.mt, kMtN};
-        mt_seed(s.mt, splitmix(fs, 0x7363656eull));
-        int cnt = p.targets_min;
-        if (p.targets_max > p.targets_min) cnt += (int)r.uniform_int((uint64_t)(p.targets_max - p.targets_min + 1), rej);
+        int cnt;
         double rg[kMaxT], vl[kMaxT];
-        for (int t = 0; t < cnt; ++t) {
-            rg[t] = r.uniform(p.range_lo, p.range_hi);
-            vl[t] = r.uniform(p.vel_lo, p.vel_hi);
+        double snr;
+        if (a.explicit_scene) {  // run_pipeline with the scenario's targets (pipeline.cpp:65-71)
+            cnt = a.exp_count;
+            for (int t = 0; t < cnt; ++t) {
+                rg[t] = a.exp_range[t];
+                vl[t] = a.exp_vel[t];
+            }
+            snr = a.exp_snr;
+        } else {
+            MtScalar r{s.mt, kMtN};
+            mt_seed(s.mt, splitmix(fs, 0x7363656eull));
+            cnt = p.targets_min;
+            if (p.targets_max > p.targets_min)
+                cnt += (int)r.uniform_int((uint64_t)(p.targets_max - p.targets_min + 1), rej);
+            for (int t = 0; t < cnt; ++t) {
+                rg[t] = r.uniform(p.range_lo, p.range_hi);
+                vl[t] = r.uniform(p.vel_lo, p.vel_hi);
+            }
+            snr = p.snr_lo_db;
+            if (p.snr_hi_db != p.snr_lo_db && isfinite(p.snr_lo_db)) snr = r.uniform(p.snr_lo_db, p.snr_hi_db);
         }
-        double snr = p.snr_lo_db;
-        if (p.snr_hi_db != p.snr_lo_db && isfinite(p.snr_lo_db)) snr = r.uniform(p.snr_lo_db, p.snr_hi_db);
         // phases (channel.cpp:74-83)
         MtScalar ph{s.mt, kMtN};
         mt_seed(s.mt, splitmix(fs, 0x70686173ull));
@@ -385,9 +401,11 @@ int gray_decode_h(unsigned g) {
 }  // namespace
 }  // namespace ofdmr
 
-extern "C" int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int64_t count, void* y,
-                                void* x_tx, double* sigma2, int32_t* n_targets, double* ranges, double* vels,
-                                double* snr_db, int32_t max_targets, int32_t* status, void* stream) {
+namespace {
+int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int64_t count, void* y, void* x_tx,
+               double* sigma2, int32_t* n_targets, double* ranges, double* vels, double* snr_db, int32_t max_targets,
+               int32_t* status, void* stream, const double* exp_ranges, const double* exp_vels, int32_t exp_count,
+               double exp_snr) {
     using namespace ofdmr;
     if (!p || !y || !x_tx || !sigma2 || !n_targets || !status || count < 0) return 2;
     if (count == 0) return 0;
@@ -429,6 +447,16 @@ extern "C" int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, i
         a.lev_f[q] = (float)a.lev_d[q];
     }
     a.inv_sqrt2 = 1.0 / std::sqrt(2.0);
+    if (exp_ranges) {
+        if (exp_count < 0 || exp_count > kMaxT || (exp_count > 0 && !exp_vels)) return 2;
+        a.explicit_scene = 1;
+        a.exp_count = exp_count;
+        for (int t = 0; t < exp_count; ++t) {
+            a.exp_range[t] = exp_ranges[t];
+            a.exp_vel[t] = exp_vels[t];
+        }
+        a.exp_snr = exp_snr;
+    }
     uint32_t ring = 1;
     const uint32_t need = (uint32_t)std::max((p->m - 1) * bps, 2 * p->m) + kMtN;
     while (ring < need) ring <<= 1;
@@ -440,4 +468,28 @@ extern "C" int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, i
     if (e != cudaSuccess) return 10;
     gen_frame_kernel<<<(unsigned)count, 256, smem, static_cast<cudaStream_t>(stream)>>>(a);
     return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
+}  // namespace
+
+extern "C" int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int64_t count, void* y,
+                                void* x_tx, double* sigma2, int32_t* n_targets, double* ranges, double* vels,
+                                double* snr_db, int32_t max_targets, int32_t* status, void* stream) {
+    return gen_launch(p, base_seed, first, count, y, x_tx, sigma2, n_targets, ranges, vels, snr_db, max_targets, status,
+                      stream, nullptr, nullptr, 0, 0.0);
+}
+
+extern "C" int ofdmr_gen_device_explicit(const ofdmr_gen_params* p, uint64_t seed, int64_t first, int64_t count,
+                                         const double* target_ranges, const double* target_vels, int32_t n_targets,
+                                         double snr_db, void* y, void* x_tx, double* sigma2, int32_t* status,
+                                         void* stream) {
+    static const double kNone = 0.0;
+    if (!p || n_targets < 0 || n_targets > 16) return 2;
+    int32_t* nt = nullptr;
+    if (cudaMalloc(&nt, sizeof(int32_t) * (size_t)(count > 0 ? count : 1)) != cudaSuccess) return 10;
+    const int rc = gen_launch(p, seed, first, count, y, x_tx, sigma2, nt, nullptr, nullptr, nullptr, 0, status, stream,
+                              n_targets > 0 ? target_ranges : &kNone, n_targets > 0 ? target_vels : &kNone,
+                              n_targets, snr_db);
+    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    cudaFree(nt);
+    return rc;
 }
