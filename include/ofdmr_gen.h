@@ -48,12 +48,18 @@ int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, int64_t firs
                      int32_t max_targets, int32_t* status, void* stream);
 
 /* run_pipeline's generator half (pipeline.cpp:65-71) for a fixed scenario, as the reference's
- * Monte-Carlo callers use it (metrics.cpp:92-120): frame i of the batch uses the run seed
+ * Monte-Carlo callers use it (metrics.cpp:92-143): frame i of the batch uses the run seed
  * derive_seed(seed, first + i); targets (host arrays, <= 16) and SNR are fixed.  y, x_tx,
- * sigma2, status as for ofdmr_gen_device.  Synchronous on `stream`. */
+ * sigma2, status as for ofdmr_gen_device; h_true (may be NULL): device c128 [count][N][M],
+ * true_channel of the realisation (channel.cpp:100-109).  Synchronous on `stream`. */
 int ofdmr_gen_device_explicit(const ofdmr_gen_params* p, uint64_t seed, int64_t first, int64_t count,
                               const double* target_ranges, const double* target_vels, int32_t n_targets,
-                              double snr_db, void* y, void* x_tx, double* sigma2, int32_t* status, void* stream);
+                              double snr_db, void* y, void* x_tx, double* sigma2, int32_t* status, void* h_true,
+                              void* stream);
+
+/* channel_mse (estimation.cpp:41-48) per frame: out[f] = mean |h_est - h_true|^2 with h_est
+ * device c64 and h_true device c128, `cells` = N*M per frame (fp64, tree-order sum). */
+int ofdmr_channel_mse(const void* h_est, const void* h_true, int64_t cells, int64_t frames, double* out, void* stream);
 
 #ifdef __cplusplus
 }

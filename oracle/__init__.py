@@ -93,6 +93,8 @@ def ref() -> C.CDLL:
         i64, d = C.c_int64, C.c_double
         _ref.ref_run_pipeline.argtypes = [i64, i64, i64, i64, d, d, i64, C.c_int, d, C.c_int, vp, vp, C.c_int32, d,
                                           C.c_uint64, vp, vp, vp, vp, vp]
+        _ref.ref_mse_sweep.argtypes = [i64, i64, i64, i64, d, d, i64, C.c_int, d, C.c_int, vp, vp, C.c_int32, vp,
+                                       C.c_int32, i64, C.c_uint64, vp]
         _ref.ref_rmse_sweep.argtypes = [i64, i64, i64, i64, d, d, i64, C.c_int, d, C.c_int, vp, vp, C.c_int32, vp,
                                         C.c_int32, i64, C.c_uint64, vp]
         _ref.ref_receive_frame.argtypes = [i64, i64, i64, i64, C.c_int, i64, C.c_int, d, vp, vp, d, i64, vp, vp, vp,
@@ -316,5 +318,15 @@ def ref_rmse_sweep(scn, snr_grid, trials: int, seed: int) -> np.ndarray:
     g = np.ascontiguousarray(snr_grid, np.float64)
     rows = np.zeros((len(g), 3))
     rc = ref().ref_rmse_sweep(*args, _p(g), len(g), trials, seed, _p(rows))
+    assert rc == 0
+    return rows
+
+
+def ref_mse_sweep(scn, snr_grid, trials: int, seed: int) -> np.ndarray:
+    """The reference's mse_sweep (metrics.cpp:122-143): per-SNR channel MSE."""
+    args, keep = ref_scenario_args(*scn)
+    g = np.ascontiguousarray(snr_grid, np.float64)
+    rows = np.zeros(len(g))
+    rc = ref().ref_mse_sweep(*args, _p(g), len(g), trials, seed, _p(rows))
     assert rc == 0
     return rows

@@ -348,4 +348,21 @@ int ref_rmse_sweep(int64_t n, int64_t m, int64_t np, int64_t mp, double df, doub
     }
 }
 
+/// The reference's mse_sweep (metrics.cpp:122-143) on the same scenario; rows[i] = MSE.
+int ref_mse_sweep(int64_t n, int64_t m, int64_t np, int64_t mp, double df, double fc, int64_t n_cp, int window,
+                  double pfa, int estimator, const double* ranges, const double* vels, int32_t count,
+                  const double* snr_grid, int32_t n_snr, int64_t trials, uint64_t seed, double* rows) {
+    try {
+        SimulationConfig cfg = scenario(n, m, np, mp, df, fc, n_cp, window, pfa, estimator, ranges, vels, count);
+        std::vector<double> grid(snr_grid, snr_grid + n_snr);
+        const auto out = mse_sweep(cfg, cfg.estimator.kind, grid, std::size_t(trials), seed);
+        for (std::size_t i = 0; i < out.size(); ++i) rows[i] = out[i].channel_mse;
+        return 0;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (...) {
+        return 3;
+    }
+}
+
 }  // extern "C"

@@ -107,7 +107,8 @@ RECEIVER_SYMBOLS = [
 DEVICE_GEN_SYMBOLS = [
     ("ofdmr_gen_device", i32, [C.POINTER(GenParams), u64, i64, i64, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp]),
     ("ofdmr_gen_device_explicit", i32, [C.POINTER(GenParams), u64, i64, i64, P_f64, P_f64, i32, f64, vp, vp, vp, vp,
-                                        vp]),
+                                        vp, vp]),
+    ("ofdmr_channel_mse", i32, [vp, vp, i64, i64, vp, vp]),
 ]
 
 GEN_SYMBOLS = [

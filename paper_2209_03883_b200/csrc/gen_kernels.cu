@@ -139,6 +139,7 @@ struct GenArgs {
     int lev_of_gray[16];    // Gray code -> level index
     double inv_sqrt2;
     uint32_t ring_mask;     // ring size - 1 (power of two >= bits per row + 312)
+    double2* h_true;        // optional: true_channel (channel.cpp:100-109) as c128 [count][N][M]
     int explicit_scene;     // 1: fixed targets / SNR below instead of the scene stream
     int exp_count;
     double exp_range[kMaxT], exp_vel[kMaxT];
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
                 xr = a.lev_d[ir];
                 xi = a.lev_d[iq];
             }
-            double yr = 0.0, yi = 0.0;
+            double yr = 0.0, yi = 0.0, hr = 0.0, hi = 0.0;
             for (int t = 0; t < T; ++t) {
                 // row = b * dph[k]; y += row * fph[l] * x  (std::complex products, left to right)
                 const double rr = s.b_re[t] * s.d_re[t] - s.b_im[t] * s.d_im[t];
@@ -369,7 +370,10 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
                 const double t2i = t1r * xi + t1i * xr;
                 yr = yr + t2r;
                 yi = yi + t2i;
+                hr = hr + t1r;  // true_channel: the same target term with x = 1 (exact)
+                hi = hi + t1i;
             }
+            if (a.h_true) a.h_true[((size_t)f * n + k) * m + l] = make_double2(hr, hi);
             if (noisy) {
                 const uint64_t v1 = ring[(consumed + 2u * l) & mask];
                 const uint64_t v2 = ring[(consumed + 2u * l + 1u) & mask];
@@ -405,7 +409,7 @@ namespace {
 int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int64_t count, void* y, void* x_tx,
                double* sigma2, int32_t* n_targets, double* ranges, double* vels, double* snr_db, int32_t max_targets,
                int32_t* status, void* stream, const double* exp_ranges, const double* exp_vels, int32_t exp_count,
-               double exp_snr) {
+               double exp_snr, void* h_true = nullptr) {
     using namespace ofdmr;
     if (!p || !y || !x_tx || !sigma2 || !n_targets || !status || count < 0) return 2;
     if (count == 0) return 0;
@@ -434,6 +438,7 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
     a.snr_db = snr_db;
     a.max_targets = max_targets;
     a.status = status;
+    a.h_true = static_cast<double2*>(h_true);
     a.bps = bps;
     // constellation axis levels exactly as gen.cpp constellation(): li = (L-1) - 2*gray_decode(g)
     const int half = bps / 2, levels = 1 << half;
@@ -481,15 +486,48 @@ extern "C" int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, i
 extern "C" int ofdmr_gen_device_explicit(const ofdmr_gen_params* p, uint64_t seed, int64_t first, int64_t count,
                                          const double* target_ranges, const double* target_vels, int32_t n_targets,
                                          double snr_db, void* y, void* x_tx, double* sigma2, int32_t* status,
-                                         void* stream) {
+                                         void* h_true, void* stream) {
     static const double kNone = 0.0;
     if (!p || n_targets < 0 || n_targets > 16) return 2;
     int32_t* nt = nullptr;
     if (cudaMalloc(&nt, sizeof(int32_t) * (size_t)(count > 0 ? count : 1)) != cudaSuccess) return 10;
     const int rc = gen_launch(p, seed, first, count, y, x_tx, sigma2, nt, nullptr, nullptr, nullptr, 0, status, stream,
                               n_targets > 0 ? target_ranges : &kNone, n_targets > 0 ? target_vels : &kNone,
-                              n_targets, snr_db);
+                              n_targets, snr_db, h_true);
     cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
     cudaFree(nt);
     return rc;
+}
+
+namespace {
+// channel_mse (estimation.cpp:41-48) per frame: mean |h_est - h_true|^2, h_est c64, h_true c128;
+// one CTA per frame, fp64 accumulation (tree order, not the CPU's sequential order).
+__global__ void __launch_bounds__(256) channel_mse_kernel(const float2* h, const double2* ht, int64_t cells,
+                                                          double* out) {
+    const size_t base = (size_t)blockIdx.x * cells;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < cells; i += 256) {
+        const float2 e = h[base + i];
+        const double2 t = ht[base + i];
+        const double dr = (double)e.x - t.x, di = (double)e.y - t.y;
+        acc += dr * dr + di * di;
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = red[0] / (double)cells;
+}
+}  // namespace
+
+extern "C" int ofdmr_channel_mse(const void* h_est, const void* h_true, int64_t cells, int64_t frames, double* out,
+                                 void* stream) {
+    if (!h_est || !h_true || !out || cells <= 0 || frames < 0 || frames > (int64_t)1 << 30) return 2;
+    if (frames == 0) return 0;
+    channel_mse_kernel<<<(unsigned)frames, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const float2*>(h_est), static_cast<const double2*>(h_true), cells, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 10;
 }

@@ -1,6 +1,7 @@
 """Monte-Carlo callers on the GPU receiver.
 
-`rmse_sweep` mirrors the reference's `rmse_sweep` (src/metrics.cpp:92-120): for every SNR of
+`rmse_sweep` mirrors the reference's `rmse_sweep` (src/metrics.cpp:92-120) and `mse_sweep` its
+`mse_sweep` (metrics.cpp:122-143).  rmse_sweep: for every SNR of
 the grid, `trials` runs of run_pipeline on a fixed scenario (run seed derive_seed(seed, t),
 max_targets = number of targets), detections matched to the truths by `match_detections`
 (metrics.cpp:36-72) and reduced to range / velocity RMSE and miss rate.  The frames come from
@@ -13,7 +14,7 @@ operation order.
 Differences from the reference: the frames are quantised to c64 and the receiver computes in
 fp32 (fp64 for σ_h² and η), so a trial's detections can differ from the fp64 reference only
 at fp32-unresolvable near-ties (SURVEY.md §8d parity rules); the host-side reduction is exact
-(tests/test_oracle_pins.py pins it against the reference's own rmse_sweep).
+(tests/test_montecarlo.py pins it against the reference's own rmse_sweep).
 """
 from __future__ import annotations
 
@@ -151,7 +152,8 @@ def rmse_sweep(cfg: RadarConfig, ranges, vels, snr_grid_db, trials: int, seed: i
                 stream = torch.cuda.current_stream(dev).cuda_stream
                 rc = lib.ofdmr_gen_device_explicit(C.byref(p), seed, t0, nb, ranges.ctypes.data_as(_native.P_f64),
                                                    vels.ctypes.data_as(_native.P_f64), T, float(snr), y.data_ptr(),
-                                                   x.data_ptr(), s2.data_ptr(), st.data_ptr(), C.c_void_p(stream))
+                                                   x.data_ptr(), s2.data_ptr(), st.data_ptr(), None,
+                                                   C.c_void_p(stream))
                 if rc:
                     raise RuntimeError(f"ofdmr_gen_device_explicit failed ({rc})")
                 if int(st[:nb].sum().item()):
@@ -164,4 +166,60 @@ def rmse_sweep(cfg: RadarConfig, ranges, vels, snr_grid_db, trials: int, seed: i
                     phys = [bins_to_physics(int(d[i, j]), int(v[i, j]), cfg) for j in range(int(c[i]))]
                     match_detections(phys, truths, res, stats)
             rows.append(finish_row(float(snr), est_name, stats, trials))
+    return rows
+
+
+@dataclass
+class MseRow:
+    snr_db: float
+    estimator: str
+    channel_mse: float
+
+
+def mse_sweep(cfg: RadarConfig, ranges, vels, snr_grid_db, trials: int, seed: int, batch: int = 512,
+              device=None) -> list[MseRow]:
+    """metrics.cpp:122-143 on the GPU: per trial, the generator's true channel (c128) against
+    estimate_channel on the GPU (LS or DFT-CE per cfg.estimator), channel_mse per trial on the
+    device, accumulated over trials in trial order on the host (as the reference does)."""
+    import torch
+
+    from . import gen
+    from .receiver import Receiver
+
+    if trials < 1:
+        raise ValueError("mse_sweep: trials must be >= 1")
+    ranges = np.ascontiguousarray(ranges, np.float64)
+    vels = np.ascontiguousarray(vels, np.float64)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    est_name = {0: "ls", 1: "dft-ce"}.get(cfg.estimator, "?")
+    p = gen.gen_params(cfg)
+    lib = _native.lib()
+    B = min(batch, trials)
+    y = torch.empty(B, cfg.n, cfg.m, dtype=torch.complex64, device=dev)
+    x = torch.empty(B, cfg.n, cfg.m, dtype=torch.complex64, device=dev)
+    ht = torch.empty(B, cfg.n, cfg.m, dtype=torch.complex128, device=dev)
+    s2 = torch.empty(B, dtype=torch.float64, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    mse = torch.empty(B, dtype=torch.float64, device=dev)
+    rows = []
+    with Receiver.from_config(cfg, device=dev.index) as rx:
+        for snr in snr_grid_db:
+            acc = 0.0
+            for t0 in range(0, trials, B):
+                nb = min(B, trials - t0)
+                stream = torch.cuda.current_stream(dev).cuda_stream
+                rc = lib.ofdmr_gen_device_explicit(C.byref(p), seed, t0, nb, ranges.ctypes.data_as(_native.P_f64),
+                                                   vels.ctypes.data_as(_native.P_f64), len(ranges), float(snr),
+                                                   y.data_ptr(), x.data_ptr(), s2.data_ptr(), st.data_ptr(),
+                                                   ht.data_ptr(), C.c_void_p(stream))
+                if rc or int(st[:nb].sum().item()):
+                    raise RuntimeError(f"ofdmr_gen_device_explicit failed ({rc})")
+                h = rx.estimate_channel(y[:nb], x[:nb])
+                rc = lib.ofdmr_channel_mse(h.data_ptr(), ht.data_ptr(), cfg.n * cfg.m, nb, mse.data_ptr(),
+                                           C.c_void_p(stream))
+                if rc:
+                    raise RuntimeError(f"ofdmr_channel_mse failed ({rc})")
+                for v in mse[:nb].cpu().numpy().tolist():
+                    acc += v
+            rows.append(MseRow(float(snr), est_name, acc / float(trials)))
     return rows

@@ -69,3 +69,20 @@ def test_gpu_rmse_sweep_matches_reference(cuda):
         # frames are c64 and the receiver fp32 on the GPU path: identical detections give
         # identical rows; a near-tie flip in one of the 72 truths moves a row by < 1 / 72
         assert np.allclose(got, ref, rtol=1e-9, atol=0), (row, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("estimator", [0, 1], ids=["ls", "dft-ce"])
+def test_gpu_mse_sweep_matches_reference(cuda, estimator):
+    """mse_sweep (metrics.cpp:122-143): GPU generator true channel (c128) vs GPU estimate_channel
+    (fp32 on c64 frames) against the reference's fp64 sweep.  The fp32 estimate error
+    (~1e-7 of |H|) is far below the estimation noise being measured: rtol 1e-4."""
+    cfg = configs.CFG1.replace(estimator=estimator)
+    ranges = np.array([8.0, 17.5, 31.0])
+    vels = np.array([-35.0, 12.0, 60.0])
+    grid = [-10.0, 0.0, 20.0]
+    trials, seed = 6, 99
+    rows = mc.mse_sweep(cfg, ranges, vels, grid, trials, seed)
+    ref = O.ref_mse_sweep(_scenario(cfg, ranges, vels), grid, trials, seed)
+    got = np.array([r.channel_mse for r in rows])
+    assert np.allclose(got, ref, rtol=1e-4, atol=0), (got, ref)
