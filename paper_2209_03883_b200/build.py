@@ -48,6 +48,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "fast_kernels": [],
         "fused_ce": [],
         "fused_pg": [],
+        "fused_pg2": [],
         "capi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions
         "sft_kernels": ["-fmad=false"],

@@ -49,6 +49,9 @@ cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStre
 cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_t st);
 int fused_pg_max_clusters();
 int fused_pg_cluster();
+cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st);
+int fused_pg2_max_groups();
+size_t fused_pg2_counter_ints(int groups);
 }  // namespace ofdmr
 
 using namespace ofdmr;
@@ -106,6 +109,9 @@ struct ofdmr_context {
     int pg_clusters = 0;              // fused periodogram: co-resident 8-CTA clusters
     float2* pg_scratch = nullptr;     // fused periodogram: per-cluster 1024 x 256 G (L2)
     int* pg_counters = nullptr;       // fused periodogram: per-group barrier counters
+    int pg2_groups = 0;               // warp-specialised periodogram: 16-CTA frame groups
+    float2* pg2_scratch = nullptr;    // per group 2 x 1024 x 256 G (L2)
+    int* pg2_counters = nullptr;      // per group progress counters
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
     float* fedges = nullptr;               // fused: per-CTA edge columns of P (16 steps x 2)
     unsigned long long* fpend = nullptr;   // fused: per-CTA pending edge candidates
@@ -645,6 +651,8 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->dscratch);
     cudaFree(c->pg_scratch);
     cudaFree(c->pg_counters);
+    cudaFree(c->pg2_scratch);
+    cudaFree(c->pg2_counters);
     cudaFree(c->fedges);
     cudaFree(c->fpend);
     cudaFree(c->fpend_loc);
@@ -795,8 +803,44 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
     // the general (non-shortcut) G layout is always N' rows; the chunk buffer holds g_rows rows
     const int64_t chunk = c->shortcut ? std::max<int64_t>(1, c->chunk * c->g_rows / g.n_prime) : c->chunk;
     (void)chunk;
-    if (c->fast && g.n_subcarriers == 1024 && g.n_symbols == 256 && g.n_prime == 1024 && g.m_prime == 256 &&
-        getenv("OFDMR_PG_PERSIST") == nullptr) {
+    const bool pg_shape = c->fast && g.n_subcarriers == 1024 && g.n_symbols == 256 && g.n_prime == 1024 &&
+                          g.m_prime == 256 && getenv("OFDMR_PG_PERSIST") == nullptr;
+    if (pg_shape && getenv("OFDMR_PG_V1") == nullptr) {
+        // warp-specialised single-launch periodogram (16-CTA frame groups, column and row
+        // warps concurrent, double-buffered G in L2)
+        if (!c->pg2_scratch) {
+            c->pg2_groups = fused_pg2_max_groups();
+            if (c->pg2_groups <= 0) return fail(OFDMR_ERR_CUDA, "fused periodogram: no co-resident frame group");
+            OFDMR_CUDA(cudaMalloc(&c->pg2_scratch, sizeof(float2) * 2 * 1024 * 256 * size_t(c->pg2_groups)));
+            OFDMR_CUDA(cudaMalloc(&c->pg2_counters, sizeof(int) * fused_pg2_counter_ints(c->pg2_groups)));
+        }
+        const size_t cnt_bytes = sizeof(int) * fused_pg2_counter_ints(c->pg2_groups);
+        Pg2Args pa{};
+        const bool win = g.window == OFDMR_WINDOW_HAMMING;
+        pa.wk = win ? c->wk : nullptr;
+        pa.wl = win ? c->wl : nullptr;
+        pa.tw1024_t = c->tw1024_t;
+        pa.tw256_t = c->tw256_t;
+        pa.gscratch = c->pg2_scratch;
+        pa.counters = c->pg2_counters;
+        pa.scale = c->scale;
+        for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 28) {
+            const int64_t nf = std::min<int64_t>((int64_t)1 << 28, frames - f0);
+            OFDMR_CUDA(cudaMemsetAsync(c->pg2_counters, 0, cnt_bytes, c->stream));
+            pa.h = static_cast<const float2*>(h) + fc * f0;
+            pa.p = p + pframe * f0;
+            pa.frames = int(nf);
+            cudaError_t e;
+            {
+                StageTimer t(c, 0, c->stream);
+                e = launch_fused_pg2(pa, win, int(std::min<int64_t>(c->pg2_groups, nf)), c->pg2_groups, c->stream);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "fused_pg2");
+            ++c->launches;
+        }
+        return OFDMR_OK;
+    }
+    if (pg_shape) {
         // fused single-launch periodogram (8-CTA cluster per frame, G in L2)
         if (!c->pg_scratch) {
             c->pg_clusters = fused_pg_max_clusters();
@@ -1178,5 +1222,6 @@ extern "C" long long ofdmr_debug_info(ofdmr_context* c, const char* key) {
     if (k == "pg_clusters") return c->pg_clusters;
     if (k == "fused_grid") return c->fused_grid;
     if (k == "pg_max_clusters") return ofdmr::fused_pg_max_clusters();
+    if (k == "pg2_max_groups") return ofdmr::fused_pg2_max_groups();
     return -1;
 }

@@ -53,4 +53,18 @@ struct PgArgs {
     float scale;               // 1 / (N M)
 };
 
+// Launch arguments of the warp-specialised batched periodogram (fused_pg2.cu).
+struct Pg2Args {
+    const float2* h;           // [frames][1024][256] channel estimates
+    float* p;                  // [frames][1024][256] periodogram (Doppler fftshifted)
+    const float* wk;           // subcarrier / symbol windows (Hamming only)
+    const float* wl;
+    const float2* tw1024_t;
+    const float2* tw256_t;
+    float2* gscratch;          // per group 2 x 256 x 1024 column-major G (L2 resident)
+    int* counters;             // per group col / row progress counters (zeroed before each launch)
+    int frames;
+    float scale;               // 1 / (N M)
+};
+
 }  // namespace ofdmr

@@ -1,0 +1,360 @@
+// Warp-specialised, TMA-fed persistent batched 2-D periodogram for N = N' = 1024,
+// M = M' = 256 (H in, P out):
+//   P[n][(m + M/2) mod M] = |FFT_M( IFFT_N( H .* w_k w_l ) )|^2 / (N M)
+// (periodogram.cpp:39-75; the map ofdmr_periodogram returns).
+//
+// Design driver: at this shape the kernel is bound by the SM's L1tex data pipe, which serves
+// every shared-memory wavefront AND every 128-B line a global LSU instruction touches.  So
+// the bulk data movement that would gather (H tiles, the G row blocks) goes through the TMA
+// engine instead, and every shared-memory exchange is laid out conflict-free.
+//
+// One CTA per SM (16 warps), frames handled by groups of kGrp = 16 CTAs; inside a CTA the two
+// passes run CONCURRENTLY on different warps:
+//
+//   column warps 0-7   tile = 1024 subcarriers x 8 symbols of H, loaded by ONE TMA box
+//                      (64-B swizzled rows; at step u the 16 CTAs of a group read 1 KiB of each
+//                      subcarrier row).  Each warp reads its symbol column (constant per-lane
+//                      offsets thanks to the swizzle) and, as soon as all 8 columns are in
+//                      registers, the next tile's TMA is in flight.  Window w_k w_l, register-
+//                      resident IFFT_1024 (32 x 32; transpose through a private padded slot),
+//                      then the column of G goes to the group's L2 scratch in COLUMN-major
+//                      order (256 B contiguous per store instruction).
+//   row warps 8-15     per frame 4 rounds of 16 delay rows: ONE TMA box (16 rows x 256
+//                      symbols of the column-major G, 128-B swizzled) per round, double-
+//                      buffered; each half-warp takes one row (conflict-free reads), FFT_256
+//                      with register twiddles and the transpose in the round buffer itself
+//                      (XOR layout), |.|^2 / (N M) with the Doppler fftshift streamed to P.
+//
+// Producer/consumer counters per group replace frame barriers: the column warps of all 16
+// CTAs bump col_cnt after a frame's G is complete; each CTA's row producer bumps row_cnt once
+// the last G box of a frame has landed in shared memory.  G is double-buffered per group
+// (4 MiB per group, 36 MiB in total, L2-resident).  All CTAs of the persistent grid are
+// co-resident (1 per SM).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+
+#include "fused_args.cuh"
+#include "radar_kernels.cuh"
+#include "warp_fft.cuh"
+
+namespace ofdmr {
+
+namespace {
+
+constexpr int kN = 1024, kM = 256;
+constexpr int kGrp = 16;        // CTAs per frame group
+constexpr int kVS = 1058;       // padded column-FFT scratch stride (float2)
+constexpr int kColWarps = 8, kRowWarps = 8;
+constexpr int kThreads = 32 * (kColWarps + kRowWarps);
+constexpr int kCntStride = 32;  // ints between counters (own 128-B line)
+constexpr int kRoundRows = 16;  // G rows per TMA round
+constexpr int kRounds = kN / kGrp / kRoundRows;         // rounds per frame per CTA (4)
+constexpr unsigned kTileBytes = 8u * kN * 8u;           // 64 KiB
+constexpr unsigned kRoundBytes = kRoundRows * kM * 8u;  // 32 KiB
+
+struct __align__(1024) Pg2Smem {
+    float2 htile[kN * 8];                 // [k][8 symbols], 64-B swizzle   (1024-B aligned)
+    float2 gbuf[2][kM * kRoundRows];      // [l][16 rows], 128-B swizzle    (1024-B aligned)
+    float2 cs[kColWarps][kVS];            // column-FFT transpose slots
+    float2 tw[1024];                      // tw[t1*32 + j] = W_1024^{j t1}
+    float wk[1024];
+    float wl[256];
+    unsigned long long mbar_h;
+    unsigned long long mbar_g[2];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bar_col() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kColWarps) : "memory"); }
+__device__ __forceinline__ void bar_row() { asm volatile("bar.sync 2, %0;" ::"n"(32 * kRowWarps) : "memory"); }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+}  // namespace
+
+#ifdef OFDMR_PHASE_TIMING
+__device__ unsigned long long g_pg2_phase[8];
+#define P2_INIT() long long _ph_t = clock64();
+#define P2(i)                                                            \
+    do {                                                                 \
+        if (lane == 0 && (warp == 0 || warp == kColWarps)) {             \
+            const long long _n = clock64();                              \
+            atomicAdd(&g_pg2_phase[i], (unsigned long long)(_n - _ph_t)); \
+            _ph_t = _n;                                                  \
+        }                                                                \
+    } while (0)
+#else
+#define P2_INIT()
+#define P2(i)
+#endif
+
+template <bool HAMMING>
+__global__ void __launch_bounds__(kThreads, 1)
+    fused_pg2_kernel(Pg2Args a, const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap gmap) {
+    extern __shared__ unsigned char smem_raw[];
+    Pg2Smem& s = *reinterpret_cast<Pg2Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = blockIdx.x / kGrp, rank = blockIdx.x % kGrp, ng = gridDim.x / kGrp;
+    for (int i = tid; i < 1024; i += kThreads) {
+        s.tw[i] = a.tw1024_t[i];
+        if (HAMMING) s.wk[i] = a.wk[i];
+    }
+    if (HAMMING && tid < 256) s.wl[tid] = a.wl[tid];
+    if (tid == 0) {
+        mbar_init(&s.mbar_h, 1);
+        mbar_init(&s.mbar_g[0], 1);
+        mbar_init(&s.mbar_g[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int nfr = a.frames > g ? (a.frames - g + ng - 1) / ng : 0;  // frames g, g + ng, ..
+    int* col_cnt = a.counters + (size_t)g * 2 * kCntStride;
+    int* row_cnt = col_cnt + kCntStride;
+    P2_INIT();
+
+    if (warp < kColWarps) {
+        // ------------------------------------------------------------ column warps
+        const int ntiles = 2 * nfr;  // tile t: frame g + (t/2) ng, symbols 128 (t&1) + 8 rank ..
+        if (tid == 0 && ntiles > 0) {
+            mbar_expect_tx(&s.mbar_h, kTileBytes);
+            tma_load_3d(s.htile, &hmap, 8 * rank, 0, 4 * g, &s.mbar_h);
+        }
+        // swizzled (k = lane + 32 r, symbol `warp`): float2 8k + 2((warp/2) ^ ((k/2)&3)) + (warp&1)
+        const int hoff = 8 * lane + 2 * ((warp >> 1) ^ ((lane >> 1) & 3)) + (warp & 1);
+        float2* col = s.cs[warp];
+        for (int t = 0; t < ntiles; ++t) {
+            const int i = t >> 1, u = t & 1;
+            const int c = 128 * u + 8 * rank + warp;
+            mbar_wait(&s.mbar_h, t & 1);
+            P2(0);
+            float2 v[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) v[r] = s.htile[hoff + 256 * r];
+            bar_col();  // every column is in registers: the tile buffer is free
+            if (tid == 0) {
+                if (t + 1 < ntiles) {
+                    const int tn = t + 1;
+                    mbar_expect_tx(&s.mbar_h, kTileBytes);
+                    tma_load_3d(s.htile, &hmap, 128 * (tn & 1) + 8 * rank, 0, 4 * (g + (tn >> 1) * ng), &s.mbar_h);
+                }
+                if (t >= 2 && u == 0) {
+                    __threadfence();
+                    atomicAdd(col_cnt, 1);  // G of frame i - 1 complete (every warp passed its stores)
+                }
+            }
+            if (HAMMING) {
+                const float wl = s.wl[c];
+#pragma unroll
+                for (int r = 0; r < 32; ++r) v[r] = cscale(v[r], s.wk[lane + 32 * r] * wl);
+            }
+            warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: G[t1 + 32 t2] in v[t2]
+            P2(1);
+            if (u == 0 && i >= 2) {
+                // G buffer (i & 1) last held frame i - 2: wait until every CTA of the group loaded it
+                if (lane == 0)
+                    while (ld_acquire(row_cnt) < kGrp * (i - 1)) __nanosleep(32);
+                __syncwarp();
+            }
+            P2(2);
+            float2* gcol = a.gscratch + ((size_t)(2 * g + (i & 1)) * kM + c) * kN + lane;
+#pragma unroll
+            for (int t2 = 0; t2 < 32; ++t2) __stcg(gcol + 32 * t2, v[t2]);
+            P2(3);
+        }
+        bar_col();
+        if (ntiles > 0 && tid == 0) {
+            __threadfence();
+            atomicAdd(col_cnt, 1);  // last frame
+        }
+    } else {
+        // ------------------------------------------------------------ row warps
+        const int wr = warp - kColWarps, h = lane >> 4, j = lane & 15;
+        const bool producer = tid == 32 * kColWarps;
+        const int nrounds = kRounds * nfr;
+        // round R: frame g + (R / kRounds) ng, rows 64 rank + 16 (R % kRounds) .. +15, buffer R & 1
+        int issued = 0;  // rounds whose TMA has been issued (producer only)
+        auto try_issue = [&](bool block) {
+            const int R = issued, i = R / kRounds, q = R % kRounds;
+            if (q == 0) {
+                if (block) {
+                    while (ld_acquire(col_cnt) < kGrp * (i + 1)) __nanosleep(32);
+                } else if (ld_acquire(col_cnt) < kGrp * (i + 1)) {
+                    return;
+                }
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // peers' generic G stores -> TMA reads
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic transposes -> TMA overwrite
+            mbar_expect_tx(&s.mbar_g[R & 1], kRoundBytes);
+            tma_load_2d(s.gbuf[R & 1], &gmap, 64 * rank + kRoundRows * q, (2 * g + (i & 1)) * kM, &s.mbar_g[R & 1]);
+            ++issued;
+        };
+        float2 twr[16];
+#pragma unroll
+        for (int t1 = 0; t1 < 16; ++t1) twr[t1] = a.tw256_t[t1 * 16 + j];
+        // swizzled (l = j + 16 r, row 2 wr + h): float2 16 l + 2 (wr ^ (l & 7)) + h
+        const int goff = 16 * j + 2 * (wr ^ (j & 7)) + h;
+        if (producer && nrounds > 0) try_issue(true);
+        for (int R = 0; R < nrounds; ++R) {
+            const int i = R / kRounds, q = R % kRounds;
+            if (producer && issued == R + 1 && R + 1 < nrounds) try_issue(false);  // look-ahead when G is ready
+            P2(5);
+            mbar_wait(&s.mbar_g[R & 1], (R >> 1) & 1);
+            if (producer && q == kRounds - 1) {
+                __threadfence();
+                atomicAdd(row_cnt, 1);  // every G box of frame i has landed: the G buffer may be reused
+            }
+            float2* gb = s.gbuf[R & 1];
+            float2 v[16];
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = gb[goff + 256 * r];
+            bar_row();  // the round buffer is now transpose scratch
+            // half-warp FFT_256 of row 2 wr + h; 16 x 16 transpose in its own 2 KiB slot, XOR layout
+            float2* sl = gb + (2 * wr + h) * 256;
+            dft16<false>(v);
+#pragma unroll
+            for (int t1 = 1; t1 < 16; ++t1) v[t1] = cmul(v[t1], twr[t1]);
+#pragma unroll
+            for (int t1 = 0; t1 < 16; ++t1) sl[t1 * 16 + (j ^ t1)] = v[t1];
+            __syncwarp();
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) v[jj] = sl[j * 16 + (jj ^ j)];
+            dft16<false>(v);
+            const int n = 64 * rank + kRoundRows * q + 2 * wr + h;
+            float* prow = a.p + ((size_t)(g + i * ng) * kN + n) * kM;
+#pragma unroll
+            for (int t2 = 0; t2 < 16; ++t2) __stcs(prow + ((j + 16 * t2 + 128) & 255), cnorm(v[t2]) * a.scale);
+            P2(6);
+            bar_row();  // transposes done: the buffer may be refilled
+            if (producer && issued == R + 1 && R + 1 < nrounds) try_issue(true);
+        }
+    }
+}
+
+}  // namespace ofdmr
+
+extern "C" int ofdmr_debug_pg2_phase_cycles(unsigned long long* out, int reset) {
+#ifdef OFDMR_PHASE_TIMING
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, ofdmr::g_pg2_phase, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(ofdmr::g_pg2_phase, z, sizeof(z));
+    }
+    return 8;
+#else
+    (void)out;
+    (void)reset;
+    return 0;
+#endif
+}
+
+namespace ofdmr {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+}  // namespace
+
+size_t fused_pg2_smem() { return sizeof(Pg2Smem) + 1024; }
+int fused_pg2_group() { return kGrp; }
+size_t fused_pg2_counter_ints(int groups) { return (size_t)groups * 2 * kCntStride; }
+
+// Frame groups of the persistent grid: one CTA per SM, kGrp CTAs per group.
+int fused_pg2_max_groups() {
+    const size_t smem = fused_pg2_smem();
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!encode_fn()) return 0;
+    if (cudaFuncSetAttribute(fused_pg2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_pg2_kernel<false>, kThreads, smem) !=
+        cudaSuccess)
+        return 0;
+    return per_sm * sms / kGrp;
+}
+
+cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st) {
+    auto enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap hmap, gmap;
+    // H: [frames][1024 k][256 l] c64 as a 3-D f64 tensor (l, k mod 256, 4 frame + k / 256);
+    // box = 8 symbols x all 1024 subcarriers, 64-B swizzle
+    {
+        const cuuint64_t dims[3] = {256, 256, 4ull * (cuuint64_t)a.frames};
+        const cuuint64_t strides[2] = {256 * 8, 256 * 256 * 8};
+        const cuuint32_t box[3] = {8, 256, 4};
+        const cuuint32_t es[3] = {1, 1, 1};
+        if (enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float2*>(a.h), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    // G scratch: per group 2 x [256 l][1024 n] c64 (column-major); box = 16 rows x 256 symbols, 128-B swizzle
+    {
+        const cuuint64_t dims[2] = {1024, 256ull * 2 * (cuuint64_t)scratch_groups};
+        const cuuint64_t strides[1] = {1024 * 8};
+        const cuuint32_t box[2] = {kRoundRows, 256};
+        const cuuint32_t es[2] = {1, 1};
+        if (enc(&gmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.gscratch, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    const size_t smem = fused_pg2_smem();
+    auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        kern<<<groups * kGrp, kThreads, smem, st>>>(a, hmap, gmap);
+        return cudaGetLastError();
+    };
+    return hamming ? go(fused_pg2_kernel<true>) : go(fused_pg2_kernel<false>);
+}
+
+}  // namespace ofdmr

@@ -398,3 +398,22 @@ def test_gpu_generator_matches_cpu_generator(cuda, cfg):
     u = _ulp_dist(y.view(np.float32), ref.y.view(np.float32))
     assert u.max() <= 2, u.max()
     assert (u > 0).mean() <= 1e-3, (u > 0).mean()
+
+
+@pytest.mark.parametrize("window,F", [(0, 5), (1, 300)])
+def test_fused_periodogram_matches_two_pass_kernel(cuda, window, F, monkeypatch):
+    """The warp-specialised TMA periodogram (default at 1024 x 256) against the previous
+    single-launch kernel (OFDMR_PG_V1) on every frame: fewer frames than frame groups, and
+    many frames per group (double-buffered G reused ~16 times)."""
+    n, m = 1024, 256
+    rng = np.random.default_rng(5 + F)
+    base = (rng.standard_normal((min(F, 37), n, m)) + 1j * rng.standard_normal((min(F, 37), n, m))).astype(np.complex64)
+    h = np.concatenate([base] * (-(-F // len(base))))[:F] * np.linspace(0.5, 2.0, F, dtype=np.float32)[:, None, None]
+    with Receiver(n, m, window=window) as rx:
+        p = rx.periodogram(h).cpu().numpy()
+        monkeypatch.setenv("OFDMR_PG_V1", "1")
+        q = rx.periodogram(h).cpu().numpy()
+    for f in range(F):
+        assert np.abs(p[f] - q[f]).max() / q[f].max() <= MAP_TOL, f
+    ref = O.periodogram(h[F - 1].astype(np.complex128), window, n, m)
+    assert np.abs(p[F - 1] - ref).max() / ref.max() <= MAP_TOL
