@@ -472,9 +472,10 @@ def main():
         per._stream()
         per._lib.ofdmr_periodogram(per._h, h.data_ptr(), pm.data_ptr(), pf)
         pst, _ = per.get_profile()
-        ptraffic = load_traffic("fused_pg1024", pf)
+        ptraffic = load_traffic("fused_pg2", pf)
         periodogram = {"frames": pf, "frames_per_s": pf / (pms / 1e3), "ms_per_step": pms,
-                       "kernel": "fused_pg1024 (persistent, 16-CTA frame groups, G in L2)",
+                       "kernel": "fused_pg2 (persistent, warp-specialised: column and row warps concurrent, "
+                                 "H tiles and G row blocks by TMA, 8-CTA frame groups, double-buffered G in L2)",
                        "algorithmic_bytes_per_frame": pbytes, "achieved_gbs": pach, "frac": pach / hbm,
                        "traffic": ptraffic["bytes_per_launch"] if ptraffic else None,
                        "traffic_source": ptraffic["source"] if ptraffic else None,

@@ -52,6 +52,7 @@ int fused_pg_cluster();
 cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st);
 int fused_pg2_max_groups();
 size_t fused_pg2_counter_ints(int groups);
+size_t fused_pg2_scratch_elems(int groups);
 }  // namespace ofdmr
 
 using namespace ofdmr;
@@ -811,7 +812,7 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
         if (!c->pg2_scratch) {
             c->pg2_groups = fused_pg2_max_groups();
             if (c->pg2_groups <= 0) return fail(OFDMR_ERR_CUDA, "fused periodogram: no co-resident frame group");
-            OFDMR_CUDA(cudaMalloc(&c->pg2_scratch, sizeof(float2) * 2 * 1024 * 256 * size_t(c->pg2_groups)));
+            OFDMR_CUDA(cudaMalloc(&c->pg2_scratch, sizeof(float2) * fused_pg2_scratch_elems(c->pg2_groups)));
             OFDMR_CUDA(cudaMalloc(&c->pg2_counters, sizeof(int) * fused_pg2_counter_ints(c->pg2_groups)));
         }
         const size_t cnt_bytes = sizeof(int) * fused_pg2_counter_ints(c->pg2_groups);

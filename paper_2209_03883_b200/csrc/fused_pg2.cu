@@ -3,33 +3,37 @@
 //   P[n][(m + M/2) mod M] = |FFT_M( IFFT_N( H .* w_k w_l ) )|^2 / (N M)
 // (periodogram.cpp:39-75; the map ofdmr_periodogram returns).
 //
-// Design driver: at this shape the kernel is bound by the SM's L1tex data pipe, which serves
-// every shared-memory wavefront AND every 128-B line a global LSU instruction touches.  So
-// the bulk data movement that would gather (H tiles, the G row blocks) goes through the TMA
-// engine instead, and every shared-memory exchange is laid out conflict-free.
+// Design driver: at this shape the kernel is bound by FP32 issue and by the SM's L1tex/LSU
+// data pipe, which serves every shared-memory wavefront AND every 128-B line a global LSU
+// instruction touches.  So the bulk data movement that would gather (H tiles, the G row
+// blocks) goes through the TMA engine instead, and the shared-memory exchanges are laid out
+// conflict-free (profiles/r01_pg2_*.txt).
 //
-// One CTA per SM (16 warps), frames handled by groups of kGrp = 16 CTAs; inside a CTA the two
-// passes run CONCURRENTLY on different warps:
+// One CTA per SM (16 warps); frames are handled by groups of kGrp = 8 CTAs; inside a CTA the
+// two passes of the 2-D transform run CONCURRENTLY on different warps:
 //
-//   column warps 0-7   tile = 1024 subcarriers x 8 symbols of H, loaded by ONE TMA box
-//                      (64-B swizzled rows; at step u the 16 CTAs of a group read 1 KiB of each
-//                      subcarrier row).  Each warp reads its symbol column (constant per-lane
-//                      offsets thanks to the swizzle) and, as soon as all 8 columns are in
-//                      registers, the next tile's TMA is in flight.  Window w_k w_l, register-
+//   column warps 0-7   tile = 1024 subcarriers x 8 symbols of H, ONE TMA box (64-B swizzled
+//                      rows; at step u the CTAs of a group read 8 kGrp symbols contiguous of
+//                      each subcarrier row).  Each warp reads its symbol column (constant
+//                      per-lane offsets thanks to the swizzle); as soon as all 8 columns are
+//                      in registers the next tile's TMA is issued.  Window w_k w_l, register-
 //                      resident IFFT_1024 (32 x 32; transpose through a private padded slot),
-//                      then the column of G goes to the group's L2 scratch in COLUMN-major
-//                      order (256 B contiguous per store instruction).
-//   row warps 8-15     per frame 4 rounds of 16 delay rows: ONE TMA box (16 rows x 256
-//                      symbols of the column-major G, 128-B swizzled) per round, double-
-//                      buffered; each half-warp takes one row (conflict-free reads), FFT_256
-//                      with register twiddles and the transpose in the round buffer itself
+//                      then the column of G goes to the group's L2 scratch column-major, in
+//                      the storage order pos = 64 b + 2 t1 + p for delay n = t1 + 32 (2b + p),
+//                      so each lane stores 16-B pairs (16 x 512 B per column).
+//   row warps 8-15     per frame 1024 / kGrp delay rows per CTA in rounds of 16: ONE TMA box
+//                      (16 storage rows x 256 symbols, 128-B swizzled) per round, double-
+//                      buffered; each 16-lane group takes one row (lane mapping chosen so each
+//                      64-bit shared-memory phase hits 16 distinct bank pairs), FFT_256 with
+//                      register twiddles and its 16 x 16 transpose in the round buffer itself
 //                      (XOR layout), |.|^2 / (N M) with the Doppler fftshift streamed to P.
 //
-// Producer/consumer counters per group replace frame barriers: the column warps of all 16
-// CTAs bump col_cnt after a frame's G is complete; each CTA's row producer bumps row_cnt once
-// the last G box of a frame has landed in shared memory.  G is double-buffered per group
-// (4 MiB per group, 36 MiB in total, L2-resident).  All CTAs of the persistent grid are
-// co-resident (1 per SM).
+// Producer/consumer counters per group and G buffer replace frame barriers: the column warps
+// of every CTA of the group bump col_cnt[b] after writing their part of a frame into G buffer
+// b; each CTA's row producer bumps row_cnt[b] once the last G box of that frame has landed in
+// shared memory.  G is double-buffered per group (18 groups x 2 x 2 MiB = 72 MiB, L2-resident;
+// 3 or 4 buffers and 16-CTA groups measured slower).  All CTAs of the persistent grid are
+// co-resident (1 per SM, 144 of 148 SMs).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -44,11 +48,20 @@ namespace ofdmr {
 namespace {
 
 constexpr int kN = 1024, kM = 256;
-constexpr int kGrp = 16;        // CTAs per frame group
+#ifndef PG2_GRP
+#define PG2_GRP 8
+#endif
+constexpr int kGrp = PG2_GRP;   // CTAs per frame group
+constexpr int kTpf = 32 / kGrp;  // column tiles (8 symbols each) per CTA per frame
+constexpr int kRowsPerCta = kN / kGrp;
 constexpr int kVS = 1058;       // padded column-FFT scratch stride (float2)
 constexpr int kColWarps = 8, kRowWarps = 8;
 constexpr int kThreads = 32 * (kColWarps + kRowWarps);
 constexpr int kCntStride = 32;  // ints between counters (own 128-B line)
+#ifndef PG2_GBUF
+#define PG2_GBUF 2
+#endif
+constexpr int kGBuf = PG2_GBUF;  // G buffers per group (frames in flight between the passes)
 constexpr int kRoundRows = 16;  // G rows per TMA round
 constexpr int kRounds = kN / kGrp / kRoundRows;         // rounds per frame per CTA (4)
 constexpr unsigned kTileBytes = 8u * kN * 8u;           // 64 KiB
@@ -80,20 +93,26 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         "r"(parity)
         : "memory");
 }
+// L2 policy for the TMA loads: H and G are read exactly once (evict first)
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            unsigned long long* bar) {
+                                            unsigned long long* bar, unsigned long long pol) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            unsigned long long* bar) {
+                                            unsigned long long* bar, unsigned long long pol) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void bar_col() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kColWarps) : "memory"); }
@@ -111,7 +130,7 @@ __device__ unsigned long long g_pg2_phase[8];
 #define P2_INIT() long long _ph_t = clock64();
 #define P2(i)                                                            \
     do {                                                                 \
-        if (lane == 0 && (warp == 0 || warp == kColWarps)) {             \
+        if (lane == 0 && ridx == 0) {                                    \
             const long long _n = clock64();                              \
             atomicAdd(&g_pg2_phase[i], (unsigned long long)(_n - _ph_t)); \
             _ph_t = _n;                                                  \
@@ -128,6 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ unsigned char smem_raw[];
     Pg2Smem& s = *reinterpret_cast<Pg2Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool is_col = warp < kColWarps;  // (interleaving the roles across schedulers measured slower)
+    const int ridx = is_col ? warp : warp - kColWarps;
     const int g = blockIdx.x / kGrp, rank = blockIdx.x % kGrp, ng = gridDim.x / kGrp;
     for (int i = tid; i < 1024; i += kThreads) {
         s.tw[i] = a.tw1024_t[i];
@@ -142,38 +163,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncthreads();
     const int nfr = a.frames > g ? (a.frames - g + ng - 1) / ng : 0;  // frames g, g + ng, ..
-    int* col_cnt = a.counters + (size_t)g * 2 * kCntStride;
-    int* row_cnt = col_cnt + kCntStride;
+    // per G buffer b: col_cnt[b] counts CTAs that finished writing a frame into b, row_cnt[b] CTAs
+    // whose row producer finished loading one out of it (per-buffer, not cumulative: a CTA
+    // running a frame ahead cannot stand in for a slower one)
+    int* col_cnt = a.counters + (size_t)g * 2 * kGBuf * kCntStride;
+    int* row_cnt = col_cnt + kGBuf * kCntStride;
     P2_INIT();
 
-    if (warp < kColWarps) {
+    // diagnostics: PG2_ROW_ONLY / PG2_COL_ONLY run one role alone (wrong results, rates only)
+#ifdef PG2_ROW_ONLY
+    if (is_col) return;
+#endif
+#ifdef PG2_COL_ONLY
+    if (!is_col) return;
+#endif
+    if (is_col) {
         // ------------------------------------------------------------ column warps
-        const int ntiles = 2 * nfr;  // tile t: frame g + (t/2) ng, symbols 128 (t&1) + 8 rank ..
-        if (tid == 0 && ntiles > 0) {
+        const int cw = ridx;
+        const bool cw0 = cw == 0 && lane == 0;
+        const int ntiles = kTpf * nfr;  // tile t: frame g + (t / kTpf) ng, symbols 8 kGrp (t % kTpf) + 8 rank ..
+        if (cw0 && ntiles > 0) {
             mbar_expect_tx(&s.mbar_h, kTileBytes);
-            tma_load_3d(s.htile, &hmap, 8 * rank, 0, 4 * g, &s.mbar_h);
+            tma_load_3d(s.htile, &hmap, 8 * rank, 0, 4 * g, &s.mbar_h, policy_evict_first());
         }
         // swizzled (k = lane + 32 r, symbol `warp`): float2 8k + 2((warp/2) ^ ((k/2)&3)) + (warp&1)
-        const int hoff = 8 * lane + 2 * ((warp >> 1) ^ ((lane >> 1) & 3)) + (warp & 1);
-        float2* col = s.cs[warp];
+        const int hoff = 8 * lane + 2 * ((cw >> 1) ^ ((lane >> 1) & 3)) + (cw & 1);
+        float2* col = s.cs[cw];
         for (int t = 0; t < ntiles; ++t) {
-            const int i = t >> 1, u = t & 1;
-            const int c = 128 * u + 8 * rank + warp;
+            const int i = t / kTpf, u = t % kTpf;
+            const int c = 8 * kGrp * u + 8 * rank + cw;
             mbar_wait(&s.mbar_h, t & 1);
             P2(0);
             float2 v[32];
 #pragma unroll
             for (int r = 0; r < 32; ++r) v[r] = s.htile[hoff + 256 * r];
             bar_col();  // every column is in registers: the tile buffer is free
-            if (tid == 0) {
+            if (cw0) {
                 if (t + 1 < ntiles) {
                     const int tn = t + 1;
                     mbar_expect_tx(&s.mbar_h, kTileBytes);
-                    tma_load_3d(s.htile, &hmap, 128 * (tn & 1) + 8 * rank, 0, 4 * (g + (tn >> 1) * ng), &s.mbar_h);
+                    tma_load_3d(s.htile, &hmap, 8 * kGrp * (tn % kTpf) + 8 * rank, 0, 4 * (g + (tn / kTpf) * ng), &s.mbar_h,
+                                policy_evict_first());
                 }
-                if (t >= 2 && u == 0) {
+                if (t >= kTpf && u == 0) {
                     __threadfence();
-                    atomicAdd(col_cnt, 1);  // G of frame i - 1 complete (every warp passed its stores)
+                    atomicAdd(col_cnt + ((i - 1) % kGBuf) * kCntStride, 1);  // G of frame i - 1 complete
                 }
             }
             if (HAMMING) {
@@ -183,43 +217,61 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: G[t1 + 32 t2] in v[t2]
             P2(1);
-            if (u == 0 && i >= 2) {
-                // G buffer (i & 1) last held frame i - 2: wait until every CTA of the group loaded it
+#ifdef PG2_COL_ONLY
+            if (false) {
+#else
+            if (u == 0 && i >= kGBuf) {
+#endif
+                // G buffer i % kGBuf last held frame i - kGBuf: wait until every CTA of the group loaded it
                 if (lane == 0)
-                    while (ld_acquire(row_cnt) < kGrp * (i - 1)) __nanosleep(32);
+                    while (ld_acquire(row_cnt + (i % kGBuf) * kCntStride) < kGrp * (i / kGBuf)) __nanosleep(32);
                 __syncwarp();
             }
             P2(2);
-            float2* gcol = a.gscratch + ((size_t)(2 * g + (i & 1)) * kM + c) * kN + lane;
+            // G column storage order: position 64 b + 2 t1 + p holds delay n = t1 + 32 (2 b + p), so lane
+            // t1 stores its pair (t2 = 2b, 2b + 1) as one 16-B vector (16 stores of 512 B per column)
+            float2* gcol = a.gscratch + ((size_t)(kGBuf * g + i % kGBuf) * kM + c) * kN;
 #pragma unroll
-            for (int t2 = 0; t2 < 32; ++t2) __stcg(gcol + 32 * t2, v[t2]);
+            for (int b = 0; b < 16; ++b)
+                __stcg(reinterpret_cast<float4*>(gcol + 64 * b) + lane,
+                       make_float4(v[2 * b].x, v[2 * b].y, v[2 * b + 1].x, v[2 * b + 1].y));
             P2(3);
         }
         bar_col();
-        if (ntiles > 0 && tid == 0) {
+        if (ntiles > 0 && cw0) {
             __threadfence();
-            atomicAdd(col_cnt, 1);  // last frame
+            atomicAdd(col_cnt + ((nfr - 1) % kGBuf) * kCntStride, 1);  // last frame
         }
     } else {
         // ------------------------------------------------------------ row warps
-        const int wr = warp - kColWarps, h = lane >> 4, j = lane & 15;
-        const bool producer = tid == 32 * kColWarps;
+        // lane -> (row h of the warp's pair, sub-lane j): the 16-lane phases of 64-bit shared
+        // accesses then hold 8 lanes of each row, so every phase hits 16 distinct bank pairs
+        const int wr = ridx, h = (lane >> 3) & 1, j = (lane & 7) | ((lane >> 4) << 3);
+        const int hx = 8 * h;  // XOR of the transpose layout of row h (disjoint bank halves)
+        const bool producer = wr == 0 && lane == 0;
         const int nrounds = kRounds * nfr;
         // round R: frame g + (R / kRounds) ng, rows 64 rank + 16 (R % kRounds) .. +15, buffer R & 1
         int issued = 0;  // rounds whose TMA has been issued (producer only)
         auto try_issue = [&](bool block) {
             const int R = issued, i = R / kRounds, q = R % kRounds;
             if (q == 0) {
+                const int* cc = col_cnt + (i % kGBuf) * kCntStride;
+#ifdef PG2_ROW_ONLY
+                const int need = 0;
+#else
+                const int need = kGrp * (i / kGBuf + 1);
+#endif
                 if (block) {
-                    while (ld_acquire(col_cnt) < kGrp * (i + 1)) __nanosleep(32);
-                } else if (ld_acquire(col_cnt) < kGrp * (i + 1)) {
+                    while (ld_acquire(cc) < need) __nanosleep(32);
+                } else if (ld_acquire(cc) < need) {
                     return;
                 }
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // peers' generic G stores -> TMA reads
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic transposes -> TMA overwrite
             mbar_expect_tx(&s.mbar_g[R & 1], kRoundBytes);
-            tma_load_2d(s.gbuf[R & 1], &gmap, 64 * rank + kRoundRows * q, (2 * g + (i & 1)) * kM, &s.mbar_g[R & 1]);
+            tma_load_2d(s.gbuf[R & 1], &gmap, kRowsPerCta * rank + kRoundRows * q, (kGBuf * g + i % kGBuf) * kM, &s.mbar_g[R & 1],
+                        policy_evict_first());
             ++issued;
         };
         float2 twr[16];
@@ -233,9 +285,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (producer && issued == R + 1 && R + 1 < nrounds) try_issue(false);  // look-ahead when G is ready
             P2(5);
             mbar_wait(&s.mbar_g[R & 1], (R >> 1) & 1);
+#ifndef PG2_NO_DISCARD
+            if (wr == 0) {
+                // the box's 256 lines of G (one 128-B line per symbol) are dead now: drop them from L2
+                // without write-back (G otherwise costs a DRAM write of 2 MiB per frame on eviction)
+                const float2* gl = a.gscratch + (size_t)(kGBuf * g + i % kGBuf) * kM * kN + kRowsPerCta * rank +
+                                   kRoundRows * q;
+#pragma unroll
+                for (int k = 0; k < kM / 32; ++k)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(gl + (size_t)(lane + 32 * k) * kN) : "memory");
+            }
+#endif
             if (producer && q == kRounds - 1) {
                 __threadfence();
-                atomicAdd(row_cnt, 1);  // every G box of frame i has landed: the G buffer may be reused
+                atomicAdd(row_cnt + (i % kGBuf) * kCntStride, 1);  // every G box of frame i landed: buffer reusable
             }
             float2* gb = s.gbuf[R & 1];
             float2 v[16];
@@ -248,12 +311,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int t1 = 1; t1 < 16; ++t1) v[t1] = cmul(v[t1], twr[t1]);
 #pragma unroll
-            for (int t1 = 0; t1 < 16; ++t1) sl[t1 * 16 + (j ^ t1)] = v[t1];
+            for (int t1 = 0; t1 < 16; ++t1) sl[t1 * 16 + (j ^ t1 ^ hx)] = v[t1];
             __syncwarp();
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) v[jj] = sl[j * 16 + (jj ^ j)];
+            for (int jj = 0; jj < 16; ++jj) v[jj] = sl[j * 16 + (jj ^ j ^ hx)];
             dft16<false>(v);
-            const int n = 64 * rank + kRoundRows * q + 2 * wr + h;
+            // storage position -> delay row n (see the column store): pos = 64 b + 2 t1 + p, n = t1 + 32 (2b + p)
+            const int pos = kRowsPerCta * rank + kRoundRows * q + 2 * wr + h;
+            const int n = ((pos & 63) >> 1) + 64 * (pos >> 6) + 32 * (pos & 1);
             float* prow = a.p + ((size_t)(g + i * ng) * kN + n) * kM;
 #pragma unroll
             for (int t2 = 0; t2 < 16; ++t2) __stcs(prow + ((j + 16 * t2 + 128) & 255), cnorm(v[t2]) * a.scale);
@@ -302,7 +367,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 size_t fused_pg2_smem() { return sizeof(Pg2Smem) + 1024; }
 int fused_pg2_group() { return kGrp; }
-size_t fused_pg2_counter_ints(int groups) { return (size_t)groups * 2 * kCntStride; }
+size_t fused_pg2_counter_ints(int groups) { return (size_t)groups * 2 * kGBuf * kCntStride; }
+size_t fused_pg2_scratch_elems(int groups) { return (size_t)groups * kGBuf * kN * kM; }
 
 // Frame groups of the persistent grid: one CTA per SM, kGrp CTAs per group.
 int fused_pg2_max_groups() {
@@ -338,7 +404,7 @@ cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scr
     }
     // G scratch: per group 2 x [256 l][1024 n] c64 (column-major); box = 16 rows x 256 symbols, 128-B swizzle
     {
-        const cuuint64_t dims[2] = {1024, 256ull * 2 * (cuuint64_t)scratch_groups};
+        const cuuint64_t dims[2] = {1024, 256ull * kGBuf * (cuuint64_t)scratch_groups};
         const cuuint64_t strides[1] = {1024 * 8};
         const cuuint32_t box[2] = {kRoundRows, 256};
         const cuuint32_t es[2] = {1, 1};
