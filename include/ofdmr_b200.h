@@ -107,6 +107,18 @@ int ofdmr_periodogram(ofdmr_context* ctx, const void* h, float* p, int64_t frame
  * k_per_frame may be NULL (= max_targets). */
 int ofdmr_detect(ofdmr_context* ctx, const float* p, const double* sigma2_h, const int32_t* k_per_frame,
                  int32_t* delay_bin, int32_t* doppler_bin, float* peak_power, int32_t* counts, int64_t frames);
+/* OFDM time-domain front end, waveform.cpp:133-166 (N = cfg.n_subcarriers, M = cfg.n_symbols,
+ * Ncp = cfg.n_cp; requires 0 <= Ncp <= N).  stream: [frames][M][Ncp + N] c64 samples; grid:
+ * [frames][N][M] c64 row-major.  ofdm_demodulate strips each symbol's cyclic prefix and takes
+ * the unscaled forward FFT_N (the receiver step in front of spectral_division); ofdm_modulate
+ * is its transmitter inverse (IFFT_N x 1/N, prefix = last Ncp samples). */
+int ofdmr_ofdm_demodulate(ofdmr_context* ctx, const void* stream, void* grid, int64_t frames);
+int ofdmr_ofdm_modulate(ofdmr_context* ctx, const void* grid, void* stream, int64_t frames);
+/* estimate_noise_power, periodogram.cpp:146-152 (the detector's estimate_noise mode,
+ * pipeline.cpp:86-87): sigma2_out[f] = P_f[count / 2] (nth_element order statistic of the
+ * N' x M' device map) / ln 2 / window power factor.  sigma2_out is a device array; feed it to
+ * ofdmr_detect as sigma2_h to run the reference's estimate-noise detection. */
+int ofdmr_estimate_noise_power(ofdmr_context* ctx, const float* p, double* sigma2_out, int64_t frames);
 /* threshold_mask + extract_peaks, periodogram.cpp:83-136, with the mask given by its
  * per-frame threshold eta[f] (mask = p >= eta). Same record layout as ofdmr_detect. */
 int ofdmr_extract_peaks(ofdmr_context* ctx, const float* p, const double* eta, const int32_t* k_per_frame,

@@ -77,6 +77,8 @@ def orc() -> C.CDLL:
         _orc.orc_make_window.argtypes = [C.c_int, sz, sz, vp, vp]
         _orc.orc_periodogram.argtypes = [vp, sz, sz, vp, vp, sz, sz, vp]
         _orc.orc_detection_threshold.argtypes = [C.c_double, C.c_double, C.c_double, vp]
+        _orc.orc_ofdm_modulate.argtypes = [vp, sz, sz, sz, vp]
+        _orc.orc_ofdm_demodulate.argtypes = [vp, sz, sz, sz, vp]
     return _orc
 
 
@@ -115,6 +117,10 @@ def ref() -> C.CDLL:
         _ref.ref_sft_batch_c64.argtypes = [vp, i64, i64, i64, i64, vp, vp, d, i64, i64, vp, vp, vp, vp, vp, C.c_int]
         _ref.ref_make_frame_pair.argtypes = [i64, i64, d, d, i64, C.c_int, vp, vp, i64, d, C.c_uint64, vp, vp, vp]
         _ref.ref_rng_u64.argtypes = [C.c_uint64, i64, vp]
+        _ref.ref_estimate_noise_power.restype = d
+        _ref.ref_estimate_noise_power.argtypes = [vp, i64, i64, d]
+        _ref.ref_ofdm_modulate.argtypes = [vp, i64, i64, i64, vp]
+        _ref.ref_ofdm_demodulate.argtypes = [vp, i64, i64, i64, vp]
     return _ref
 
 
@@ -199,6 +205,24 @@ def division_noise_power(sigma2: float, x: np.ndarray) -> float:
 def estimate_noise_power(p: np.ndarray, pf: float) -> float:
     p = np.ascontiguousarray(p, np.float64)
     return orc().orc_estimate_noise_power(_p(p), p.size, pf)
+
+
+def ofdm_modulate(x: np.ndarray, n_cp: int) -> np.ndarray:
+    """waveform.cpp:133-149 on an N x M grid -> stream [M][N_cp + N] (fp64)."""
+    x = np.ascontiguousarray(x, np.complex128)
+    n, m = x.shape
+    out = np.zeros((m, n + n_cp), np.complex128)
+    if orc().orc_ofdm_modulate(_p(x), n, m, n_cp, _p(out)) != 0:
+        raise ValueError("n_cp > N")
+    return out
+
+
+def ofdm_demodulate(stream: np.ndarray, n: int, m: int, n_cp: int) -> np.ndarray:
+    """waveform.cpp:152-166: stream [M][N_cp + N] -> N x M grid (fp64)."""
+    s = np.ascontiguousarray(stream, np.complex128).reshape(m, n + n_cp)
+    out = np.zeros((n, m), np.complex128)
+    orc().orc_ofdm_demodulate(_p(s), n, m, n_cp, _p(out))
+    return out
 
 
 def rx_config(n, m, n_prime, m_prime, estimator, n_cp, window, pfa) -> RxConfig:

@@ -135,6 +135,47 @@ static void fft_strided(cd* data, size_t n, size_t count, size_t stride, size_t 
     free(buf);
 }
 
+/* ------------------------------------------------------ OFDM front end -- */
+
+/* waveform.cpp:133-149 ofdm_modulate: per symbol l, unscaled inverse FFT_N of column l
+ * times 1/N; stream[l][0..ncp) = sym[n - ncp + i], stream[l][ncp..) = sym. */
+int orc_ofdm_modulate(const cd* x, size_t n, size_t m, size_t ncp, cd* stream) {
+    if (ncp > n) return 2;
+    const size_t ns = n + ncp;
+    const double inv_n = 1.0 / (double)n;
+    double* sym = (double*)malloc(sizeof(double) * 2 * n);
+    for (size_t l = 0; l < m; l++) {
+        for (size_t k = 0; k < n; k++) {
+            sym[2 * k] = creal(x[k * m + l]);
+            sym[2 * k + 1] = cimag(x[k * m + l]);
+        }
+        orc_fft(sym, n, +1);
+        cd* dst = stream + l * ns;
+        for (size_t i = 0; i < ncp; i++) dst[i] = CMPLX(sym[2 * (n - ncp + i)] * inv_n, sym[2 * (n - ncp + i) + 1] * inv_n);
+        for (size_t i = 0; i < n; i++) dst[ncp + i] = CMPLX(sym[2 * i] * inv_n, sym[2 * i + 1] * inv_n);
+    }
+    free(sym);
+    return 0;
+}
+
+/* waveform.cpp:152-166 ofdm_demodulate: strip the cyclic prefix of symbol l and take the
+ * unscaled forward FFT_N of the next N samples -> column l of the N x M grid. */
+int orc_ofdm_demodulate(const cd* stream, size_t n, size_t m, size_t ncp, cd* x) {
+    const size_t ns = n + ncp;
+    double* sym = (double*)malloc(sizeof(double) * 2 * n);
+    for (size_t l = 0; l < m; l++) {
+        const cd* src = stream + l * ns + ncp;
+        for (size_t i = 0; i < n; i++) {
+            sym[2 * i] = creal(src[i]);
+            sym[2 * i + 1] = cimag(src[i]);
+        }
+        orc_fft(sym, n, -1);
+        for (size_t k = 0; k < n; k++) x[k * m + l] = CMPLX(sym[2 * k], sym[2 * k + 1]);
+    }
+    free(sym);
+    return 0;
+}
+
 /* --------------------------------------------------------- estimation -- */
 
 /* estimation.cpp:10-21 spectral_division: H = Y / X, error 2 on a zero X cell. */

@@ -94,6 +94,34 @@ int ref_periodogram(const double* h, int64_t n, int64_t m, int window, int64_t n
     } catch (const ConfigError&) { return 2; }
 }
 
+double ref_estimate_noise_power(const double* p, int64_t rows, int64_t cols, double pf) {
+    RealGrid g(rows, cols);
+    for (int64_t i = 0; i < rows * cols; ++i) g.storage()[i] = p[i];
+    return estimate_noise_power(g, pf);
+}
+
+int ref_ofdm_modulate(const double* x, int64_t n, int64_t m, int64_t n_cp, double* stream) {
+    try {
+        const WaveformConfig w = make_wave(n, m, n, m, 1.0, 1.0, n_cp, 0, 0.01);
+        const std::vector<cplx> s = ofdm_modulate(grid_from(x, n, m), w);
+        for (std::size_t i = 0; i < s.size(); ++i) {
+            stream[2 * i] = s[i].real();
+            stream[2 * i + 1] = s[i].imag();
+        }
+        return 0;
+    } catch (const ConfigError&) { return 2; }
+}
+
+int ref_ofdm_demodulate(const double* stream, int64_t n, int64_t m, int64_t n_cp, double* x) {
+    try {
+        const WaveformConfig w = make_wave(n, m, n, m, 1.0, 1.0, n_cp, 0, 0.01);
+        std::vector<cplx> s(std::size_t(m * (n + n_cp)));
+        for (std::size_t i = 0; i < s.size(); ++i) s[i] = cplx(stream[2 * i], stream[2 * i + 1]);
+        grid_to(ofdm_demodulate(s, w), x);
+        return 0;
+    } catch (const ConfigError&) { return 2; }
+}
+
 double ref_window_power_factor(int window, int64_t n, int64_t m) {
     return make_window(window ? WindowKind::Hamming : WindowKind::Rectangular, n, m).power_factor();
 }

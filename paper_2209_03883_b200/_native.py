@@ -97,6 +97,9 @@ RECEIVER_SYMBOLS = [
     ("ofdmr_periodogram", i32, [vp, vp, vp, i64]),
     ("ofdmr_detect", i32, [vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_extract_peaks", i32, [vp, vp, vp, vp, vp, vp, vp, vp, i64]),
+    ("ofdmr_estimate_noise_power", i32, [vp, vp, vp, i64]),
+    ("ofdmr_ofdm_demodulate", i32, [vp, vp, vp, i64]),
+    ("ofdmr_ofdm_modulate", i32, [vp, vp, vp, i64]),
     ("ofdmr_pipeline", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_general", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_host", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),

@@ -49,6 +49,8 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "fused_ce": [],
         "fused_pg": [],
         "fused_pg2": [],
+        "noise_kernels": [],
+        "ofdm_kernels": [],
         "capi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions
         "sft_kernels": ["-fmad=false"],

@@ -49,6 +49,11 @@ cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStre
 cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_t st);
 int fused_pg_max_clusters();
 int fused_pg_cluster();
+size_t noise_select_scratch_bytes(int64_t frames);
+cudaError_t launch_ofdm(bool inverse, const float2* in, float2* out, int n, int m, int ncp, int64_t frames,
+                        const float2* tw, cudaStream_t st);
+cudaError_t launch_noise_select(const float* p, int64_t count, double pf, double* sigma2_out, int64_t frames,
+                                void* scratch, int sms, cudaStream_t st, int64_t* launches);
 cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st);
 int fused_pg2_max_groups();
 size_t fused_pg2_counter_ints(int groups);
@@ -113,6 +118,8 @@ struct ofdmr_context {
     int pg2_groups = 0;               // warp-specialised periodogram: 16-CTA frame groups
     float2* pg2_scratch = nullptr;    // per group 2 x 1024 x 256 G (L2)
     int* pg2_counters = nullptr;      // per group progress counters
+    void* noise_scratch = nullptr;    // estimate_noise_power radix-select histograms
+    int64_t noise_cap = 0;            // frames the scratch holds
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
     float* fedges = nullptr;               // fused: per-CTA edge columns of P (16 steps x 2)
     unsigned long long* fpend = nullptr;   // fused: per-CTA pending edge candidates
@@ -654,6 +661,7 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->pg_counters);
     cudaFree(c->pg2_scratch);
     cudaFree(c->pg2_counters);
+    cudaFree(c->noise_scratch);
     cudaFree(c->fedges);
     cudaFree(c->fpend);
     cudaFree(c->fpend_loc);
@@ -999,6 +1007,51 @@ static int detect_impl(ofdmr_context* c, const float* p, const double* sigma2_h,
     return OFDMR_OK;
 }
 
+static int ofdm_impl(ofdmr_context* c, bool inverse, const void* in, void* out, int64_t frames, const char* what) {
+    if (!c || !in || !out) return fail(OFDMR_ERR_CONFIG, std::string(what) + ": null argument");
+    if (frames <= 0) return OFDMR_OK;
+    const ofdmr_config& g = c->cfg;
+    if (g.n_cp < 0 || g.n_cp > g.n_subcarriers) return fail(OFDMR_ERR_CONFIG, "n_cp must lie in [0, N]");
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const cudaError_t e = ofdmr::launch_ofdm(inverse, static_cast<const float2*>(in), static_cast<float2*>(out),
+                                             g.n_subcarriers, g.n_symbols, g.n_cp, frames, c->tw, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    ++c->launches;
+    return OFDMR_OK;
+}
+
+int ofdmr_ofdm_demodulate(ofdmr_context* c, const void* stream, void* grid, int64_t frames) {
+    return ofdm_impl(c, false, stream, grid, frames, "ofdm_demodulate");
+}
+
+int ofdmr_ofdm_modulate(ofdmr_context* c, const void* grid, void* stream, int64_t frames) {
+    return ofdm_impl(c, true, grid, stream, frames, "ofdm_modulate");
+}
+
+int ofdmr_estimate_noise_power(ofdmr_context* c, const float* p, double* sigma2_out, int64_t frames) {
+    if (!c || !p || !sigma2_out) return fail(OFDMR_ERR_CONFIG, "estimate_noise_power: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const int64_t count = int64_t(c->cfg.n_prime) * int64_t(c->cfg.m_prime);
+    const int64_t chunk = std::min<int64_t>(frames, 4096);
+    if (c->noise_cap < chunk) {
+        cudaFree(c->noise_scratch);
+        c->noise_scratch = nullptr;
+        c->noise_cap = 0;
+        OFDMR_CUDA(cudaMalloc(&c->noise_scratch, ofdmr::noise_select_scratch_bytes(chunk)));
+        c->noise_cap = chunk;
+    }
+    int sms = 0;
+    OFDMR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    for (int64_t f0 = 0; f0 < frames; f0 += chunk) {
+        const int64_t nf = std::min<int64_t>(chunk, frames - f0);
+        const cudaError_t e = ofdmr::launch_noise_select(p + size_t(f0) * size_t(count), count, c->pf, sigma2_out + f0,
+                                                         nf, c->noise_scratch, sms, c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(e, "estimate_noise_power");
+    }
+    return OFDMR_OK;
+}
+
 int ofdmr_detect(ofdmr_context* c, const float* p, const double* sigma2_h, const int32_t* kpf, int32_t* d,
                  int32_t* dp, float* pw, int32_t* cnt, int64_t frames) {
     if (!c || !p || !sigma2_h || !d || !dp || !pw || !cnt) return fail(OFDMR_ERR_CONFIG, "detect: null argument");
@@ -1054,6 +1107,16 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
         for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
             const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);
             fa.frames = int(nf);
+            fa.y = static_cast<const float2*>(y) + fc * f0;
+            fa.x = static_cast<const float2*>(x) + fc * f0;
+            fa.sigma2 = sigma2 + f0;
+            fa.k_per_frame = kpf ? kpf + f0 : nullptr;
+            fa.det_delay = d + f0 * K;
+            fa.det_doppler = dp + f0 * K;
+            fa.det_power = pw + f0 * K;
+            fa.counts = cnt + f0;
+            fa.s2h_out = s2h_out ? s2h_out + f0 : nullptr;
+            fa.status = status ? status + f0 : nullptr;
             cudaError_t e;
             {
                 StageTimer t(c, 0, c->stream);

@@ -274,7 +274,10 @@ class Receiver:
         """detection_threshold + threshold_mask + extract_peaks (periodogram.cpp:77-136)."""
         p = self._p_batch(p)
         F = p.shape[0]
-        s2 = torch.as_tensor(np.broadcast_to(np.asarray(sigma2_h, np.float64), (F,)).copy()).to(self.device)
+        if isinstance(sigma2_h, torch.Tensor):
+            s2 = sigma2_h.to(self.device, torch.float64).reshape(-1).expand(F).contiguous()
+        else:
+            s2 = torch.as_tensor(np.broadcast_to(np.asarray(sigma2_h, np.float64), (F,)).copy()).to(self.device)
         if bool((s2 < 0).any()):
             raise ConfigError("threshold: sigma2 must be >= 0")
         k = self._k(k_per_frame, F)
@@ -284,6 +287,43 @@ class Receiver:
                                       d.delay_bin.data_ptr(), d.doppler_bin.data_ptr(), d.peak_power.data_ptr(),
                                       d.counts.data_ptr(), F))
         return d
+
+    def ofdm_demodulate(self, stream) -> torch.Tensor:
+        """ofdm_demodulate (waveform.cpp:152-166): stream of M (N_cp + N) samples per frame
+        -> N x M grid (CP strip + unscaled forward FFT_N per symbol)."""
+        n, m, ncp = self.cfg.n_subcarriers, self.cfg.n_symbols, self.cfg.n_cp
+        st = _as_grid(stream, self.device)
+        single = st.dim() == 1 or (st.dim() == 2 and st.shape == (m, n + ncp))
+        st = st.reshape(1 if single else st.shape[0], -1)
+        if st.shape[1] != m * (n + ncp):
+            raise ConfigError("stream length must be M*(N+Ncp)")
+        st = st.contiguous()
+        out = torch.empty(st.shape[0], n, m, dtype=torch.complex64, device=self.device)
+        self._stream()
+        _check(self._lib.ofdmr_ofdm_demodulate(self._h, st.data_ptr(), out.data_ptr(), st.shape[0]))
+        return out[0] if single else out
+
+    def ofdm_modulate(self, x) -> torch.Tensor:
+        """ofdm_modulate (waveform.cpp:133-149): N x M grid -> M x (N_cp + N) stream per frame
+        (IFFT_N x 1/N per symbol, cyclic prefix = last N_cp samples)."""
+        n, m, ncp = self.cfg.n_subcarriers, self.cfg.n_symbols, self.cfg.n_cp
+        x, single = _batched(_as_grid(x, self.device))
+        if tuple(x.shape[1:]) != (n, m):
+            raise ConfigError("grid shape does not match config")
+        out = torch.empty(x.shape[0], m, n + ncp, dtype=torch.complex64, device=self.device)
+        self._stream()
+        _check(self._lib.ofdmr_ofdm_modulate(self._h, x.data_ptr(), out.data_ptr(), x.shape[0]))
+        return out[0] if single else out
+
+    def estimate_noise_power(self, p) -> torch.Tensor:
+        """estimate_noise_power (periodogram.cpp:146-152) per frame: the order statistic
+        P[count / 2] of the map / ln 2 / window power factor (fp64, device)."""
+        p = self._p_batch(p)
+        F = p.shape[0]
+        out = torch.empty(F, dtype=torch.float64, device=self.device)
+        self._stream()
+        _check(self._lib.ofdmr_estimate_noise_power(self._h, p.data_ptr(), out.data_ptr(), F))
+        return out
 
     def extract_peaks(self, p, eta, k_per_frame=None) -> Detections:
         """extract_peaks (periodogram.cpp:89-136) on the mask p >= eta."""
@@ -298,14 +338,25 @@ class Receiver:
                                              d.doppler_bin.data_ptr(), d.peak_power.data_ptr(), d.counts.data_ptr(), F))
         return d
 
-    def pipeline(self, y, x_tx, sigma2, k_per_frame=None, want_map: bool = False, check: bool = True):
-        """Receiver half of run_pipeline (pipeline.cpp:72-96).  Returns (Detections, map|None)."""
+    def pipeline(self, y, x_tx, sigma2, k_per_frame=None, want_map: bool = False, check: bool = True,
+                 estimate_noise: bool = False):
+        """Receiver half of run_pipeline (pipeline.cpp:72-96).  Returns (Detections, map|None).
+        estimate_noise=True is the detector's estimate_noise mode (pipeline.cpp:86-87): the
+        threshold uses estimate_noise_power(P) instead of sigma2 (which is then ignored);
+        Detections.sigma2_h holds the estimate (the reference's sigma2_used)."""
         y, _ = _batched(_as_grid(y, self.device))
         x, _ = _batched(_as_grid(x_tx, self.device))
         if y.shape != x.shape:
             raise ConfigError("spectral_division: shape mismatch")
         self._shape_check(y)
         F = y.shape[0]
+        if estimate_noise:
+            h = self.estimate_channel(y, x, check=check)
+            pm = self.periodogram(h)
+            s2e = self.estimate_noise_power(pm)
+            d = self.detect(pm, s2e, k_per_frame)
+            d.sigma2_h = s2e
+            return d, (pm if want_map else None)
         s2 = torch.as_tensor(np.broadcast_to(np.asarray(sigma2, np.float64), (F,)).copy()).to(self.device) \
             if not isinstance(sigma2, torch.Tensor) else sigma2.to(self.device, torch.float64).contiguous()
         k = self._k(k_per_frame, F)

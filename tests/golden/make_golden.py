@@ -144,6 +144,31 @@ def frame_fixture(R):
                         vels=vels, snr_db=5.0, seed=4242, y=y, x=x, sigma2=s2.value)
 
 
+def ofdm_fixtures(R):
+    """ofdm_modulate / ofdm_demodulate (waveform.cpp:133-166) on seeded grids / streams."""
+    rng = np.random.default_rng(1333)
+    for i, (n, m, ncp) in enumerate([(64, 12, 16), (256, 6, 0), (48, 5, 12)]):
+        x = np.ascontiguousarray(rng.normal(size=(n, m)) + 1j * rng.normal(size=(n, m)))
+        stream = np.empty((m, n + ncp), np.complex128)
+        assert R.ref_ofdm_modulate(p(x), n, m, ncp, p(stream)) == 0
+        noisy = np.ascontiguousarray(stream + 0.1 * (rng.normal(size=stream.shape) + 1j * rng.normal(size=stream.shape)))
+        grid = np.empty((n, m), np.complex128)
+        assert R.ref_ofdm_demodulate(p(noisy), n, m, ncp, p(grid)) == 0
+        np.savez_compressed(OUT / f"ofdm_{i}.npz", kind="ofdm", x=x, n_cp=ncp, stream=stream, noisy=noisy, grid=grid)
+
+
+def noise_fixtures(R):
+    """estimate_noise_power (periodogram.cpp:146-152): maps with odd/even counts and ties."""
+    rng = np.random.default_rng(146)
+    maps = [rng.exponential(size=(32, 16)), rng.exponential(size=(7, 9)),
+            np.round(rng.exponential(size=(16, 16)) * 4) / 4, np.zeros((8, 8))]
+    for i, mp_ in enumerate(maps):
+        mp_ = np.ascontiguousarray(mp_)
+        pf = 0.3968 if i % 2 else 1.0
+        s2 = R.ref_estimate_noise_power(p(mp_), mp_.shape[0], mp_.shape[1], pf)
+        np.savez_compressed(OUT / f"noise_{i}.npz", kind="noise", p=mp_, pf=pf, sigma2=s2)
+
+
 if __name__ == "__main__":
     R = O.ref()
     periodogram_fixtures(R)
@@ -151,5 +176,7 @@ if __name__ == "__main__":
     receive_fixtures(R)
     sft_fixture(R)
     frame_fixture(R)
+    ofdm_fixtures(R)
+    noise_fixtures(R)
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

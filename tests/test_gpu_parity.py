@@ -417,3 +417,93 @@ def test_fused_periodogram_matches_two_pass_kernel(cuda, window, F, monkeypatch)
         assert np.abs(p[f] - q[f]).max() / q[f].max() <= MAP_TOL, f
     ref = O.periodogram(h[F - 1].astype(np.complex128), window, n, m)
     assert np.abs(p[F - 1] - ref).max() / ref.max() <= MAP_TOL
+
+
+@pytest.mark.parametrize("n,m,np_,mp,window", [(1024, 256, 1024, 256, 1), (64, 32, 128, 64, 0), (2048, 512, 4096, 2048, 1),
+                                               (16, 16, 16, 16, 0)])
+def test_estimate_noise_power(cuda, n, m, np_, mp, window):
+    """estimate_noise_power (periodogram.cpp:146-152): the radix select returns exactly the
+    nth_element order statistic P[count/2] of the device map (bit-exact sigma2 from it), and
+    matches the oracle's fp64 estimate on its own map."""
+    F = 2 if np_ * mp > 2**20 else 5
+    h = np.stack([gen.noise_grid(n, m, 0.3 + f, 300 + f) for f in range(F)]).astype(np.complex64)
+    pf = O.power_factor(window, n, m)
+    with Receiver(n, m, np_, mp, window=window) as rx:
+        p = rx.periodogram(h)
+        s2 = rx.estimate_noise_power(p).cpu().numpy()
+        pz = torch.zeros_like(p[:1])
+        assert rx.estimate_noise_power(pz).cpu().numpy()[0] == 0.0
+        pc = torch.full_like(p[:1], 0.25)  # all ties
+        assert rx.estimate_noise_power(pc).cpu().numpy()[0] == 0.25 / 0.6931471805599453 / pf
+    p = p.cpu().numpy()
+    mid = np_ * mp // 2
+    for f in range(F):
+        v = float(np.partition(p[f].ravel(), mid)[mid])
+        assert s2[f] == v / 0.6931471805599453 / pf, f
+        ref = O.estimate_noise_power(O.periodogram(h[f].astype(np.complex128), window, np_, mp), pf)
+        assert abs(s2[f] - ref) <= 1e-4 * ref, (f, s2[f], ref)
+
+
+def test_pipeline_estimate_noise_mode(cuda):
+    """run_pipeline with detector.estimate_noise (pipeline.cpp:86-87) on LS frames (cfg0 and a
+    Hamming variant): the threshold from the estimated noise; detections equal the oracle
+    composition on the same frames (periodogram -> estimate_noise_power -> threshold ->
+    extract_peaks).  (With DFT-CE the median cell is an algebraic zero, so the estimate is
+    fp roundoff in both implementations and is not compared.)"""
+    _estimate_noise_parity(configs.CFG0)
+    _estimate_noise_parity(configs.CFG0.replace(window=1, snr_lo_db=0.0, snr_hi_db=0.0))
+
+
+def _estimate_noise_parity(cfg):
+    fb = gen.frames(cfg, 0, 8)
+    with Receiver.from_config(cfg) as rx:
+        dets, pm = rx.pipeline(fb.y, fb.x, fb.sigma2, want_map=True, estimate_noise=True)
+        s2e = dets.sigma2_h.cpu().numpy()
+    pfac = O.power_factor(cfg.window, cfg.n, cfg.m)
+    for f in range(8):
+        h = O.spectral_division(fb.y[f].astype(np.complex128), fb.x[f].astype(np.complex128))
+        ref_map = O.periodogram(h, cfg.window, cfg.n_prime, cfg.m_prime)
+        ref_s2 = O.estimate_noise_power(ref_map, pfac)
+        assert abs(s2e[f] - ref_s2) <= 1e-4 * ref_s2
+        eta = O.detection_threshold(ref_s2, cfg.pfa, pfac)
+        ref = O.extract_peaks(ref_map, eta, cfg.max_targets)
+        got = dets.frame(f)
+        assert classify(got, ref, ref_map, eta, cfg.max_targets) != "fail", (f, got, ref)
+        assert powers_close(got, ref)
+
+
+@pytest.mark.parametrize("n,m,ncp", [(1024, 256, 128), (2048, 16, 256), (4096, 16, 1024), (16, 16, 0), (64, 16, 64),
+                                     (256, 32, 7)])
+def test_ofdm_front_end_matches_oracle(cuda, n, m, ncp):
+    """§8(f) item 3, the OFDM time-domain front end (waveform.cpp:133-166): GPU ofdm_modulate
+    and ofdm_demodulate against the oracle restatement on identical c64 inputs (fp32 FFT:
+    1e-5 of the frame's peak magnitude), the modulate -> demodulate round trip, batching."""
+    F = 3
+    rng = np.random.default_rng(n + m + ncp)
+    x = (rng.standard_normal((F, n, m)) + 1j * rng.standard_normal((F, n, m))).astype(np.complex64)
+    noise = (0.05 * (rng.standard_normal((F, m, n + ncp)) + 1j * rng.standard_normal((F, m, n + ncp))))
+    with Receiver(n, m, n_cp=ncp, window="rectangular") as rx:
+        st = rx.ofdm_modulate(x)
+        assert tuple(st.shape) == (F, m, n + ncp)
+        st_np = st.cpu().numpy()
+        noisy = (st_np + noise).astype(np.complex64)
+        gr = rx.ofdm_demodulate(noisy).cpu().numpy()
+        rt = rx.ofdm_demodulate(st).cpu().numpy()
+        single = rx.ofdm_demodulate(noisy[1].reshape(-1)).cpu().numpy()
+        with pytest.raises(ConfigError):
+            rx.ofdm_demodulate(noisy[:, :, 1:])
+        with pytest.raises(ConfigError):
+            rx.ofdm_modulate(x[:, :, 1:])
+    for f in range(F):
+        ref_st = O.ofdm_modulate(x[f].astype(np.complex128), ncp)
+        assert np.abs(st_np[f] - ref_st).max() <= 1e-5 * np.abs(ref_st).max()
+        ref_gr = O.ofdm_demodulate(noisy[f].astype(np.complex128), n, m, ncp)
+        assert np.abs(gr[f] - ref_gr).max() <= 1e-5 * np.abs(ref_gr).max()
+        assert np.abs(rt[f] - x[f]).max() <= 1e-5 * np.abs(x[f]).max()
+    assert np.array_equal(single, gr[1])
+
+
+def test_ofdm_cp_longer_than_symbol_rejected(cuda):
+    with Receiver(64, 16, n_cp=65, window="rectangular") as rx:
+        with pytest.raises(ConfigError):
+            rx.ofdm_modulate(np.zeros((64, 16), np.complex64))
