@@ -113,6 +113,37 @@ int main() {
     std::printf("sft_iterate: reference %zu entries, b200 %zu entries, same support = %d, iterations %zu/%zu\n",
                 s1.entries.size(), s2.entries.size(), int(a1 == a2), s1.iterations, s2.iterations);
     fails += a1 != a2;
+    // estimate_noise_power on the reference's own periodogram
+    {
+        const double pfw = w.power_factor();
+        const double e1 = estimate_noise_power(pr, pfw), e2 = b200::estimate_noise_power(pr, pfw);
+        const bool ok = std::abs(e1 - e2) <= 1e-6 * e1;
+        std::printf("estimate_noise_power: reference %.9g, b200 %.9g, ok = %d\n", e1, e2, int(ok));
+        fails += !ok;
+    }
+    // OFDM front end: b200 modulate -> reference demodulate, reference modulate -> b200 demodulate
+    {
+        WaveformConfig ow = wc;
+        ow.n_subcarriers = 256;
+        ow.n_symbols = 16;
+        ow.n_cp = 32;
+        ComplexGrid xg(256, 16, AxisTag::SubcarrierSymbol);
+        for (std::size_t a = 0; a < 256; ++a)
+            for (std::size_t b = 0; b < 16; ++b) xg.at(a, b) = std::polar(1.0, 0.7 * double(a * 16 + b));
+        const auto st_ref = ofdm_modulate(xg, ow), st_b200 = b200::ofdm_modulate(xg, ow);
+        double e_mod = 0, peak = 0;
+        for (std::size_t i = 0; i < st_ref.size(); ++i) {
+            e_mod = std::max(e_mod, std::abs(st_ref[i] - st_b200[i]));
+            peak = std::max(peak, std::abs(st_ref[i]));
+        }
+        const ComplexGrid d_ref = ofdm_demodulate(st_ref, ow), d_b200 = b200::ofdm_demodulate(st_ref, ow);
+        double e_dem = 0;
+        for (std::size_t a = 0; a < 256; ++a)
+            for (std::size_t b = 0; b < 16; ++b) e_dem = std::max(e_dem, std::abs(d_ref.at(a, b) - d_b200.at(a, b)));
+        const bool ok = e_mod <= 1e-5 * peak && e_dem <= 1e-5;
+        std::printf("ofdm_modulate/demodulate: max err %.3g / %.3g, ok = %d\n", e_mod / peak, e_dem, int(ok));
+        fails += !ok;
+    }
     std::printf("%s\n", fails ? "FAIL" : "OK");
     return fails ? 1 : 0;
 }

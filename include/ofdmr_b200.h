@@ -114,6 +114,10 @@ int ofdmr_detect(ofdmr_context* ctx, const float* p, const double* sigma2_h, con
  * is its transmitter inverse (IFFT_N x 1/N, prefix = last Ncp samples). */
 int ofdmr_ofdm_demodulate(ofdmr_context* ctx, const void* stream, void* grid, int64_t frames);
 int ofdmr_ofdm_modulate(ofdmr_context* ctx, const void* grid, void* stream, int64_t frames);
+/* write_map_pgm's pixel values (io.cpp:94-110) for a batch of device maps: out[f] holds the
+ * N' x M' row-major 8-bit image (rows = delay bin, columns = fft-shifted Doppler bin) that the
+ * reference writes after its "P5\n<cols> <rows>\n255\n" header.  out is device memory. */
+int ofdmr_map_to_pgm(ofdmr_context* ctx, const float* p, uint8_t* out, int64_t frames);
 /* estimate_noise_power, periodogram.cpp:146-152 (the detector's estimate_noise mode,
  * pipeline.cpp:86-87): sigma2_out[f] = P_f[count / 2] (nth_element order statistic of the
  * N' x M' device map) / ln 2 / window power factor.  sigma2_out is a device array; feed it to

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -187,6 +188,62 @@ inline std::vector<Detection> extract_peaks(const RealGrid& p, const std::vector
         out[i].peak_power = p.at(std::size_t(dh[i]), std::size_t(vh[i] + mp / 2));  // exact fp64 value of the cell
         bins_to_physics(out[i], cfg);  // reference host formula (periodogram.cpp:138-144)
     }
+    return out;
+}
+
+// periodogram.hpp (estimate_noise_power, periodogram.cpp:146-152) — median cell / ln 2 /
+// window power factor.  The map is quantised to fp32 on the device, so the selected order
+// statistic is the fp32 rounding of the reference's (relative difference <= 2^-24).
+inline double estimate_noise_power(const RealGrid& p, double window_power_factor) {
+    using namespace detail;
+    const int32_t np = int32_t(p.rows()), mp = int32_t(p.cols());
+    ofdmr_context* c = context(np, mp, np, mp, OFDMR_WINDOW_RECT, OFDMR_EST_LS, 0, 1, 1e-2);  // pf = 1
+    std::vector<float> ph(p.size());
+    for (std::size_t i = 0; i < p.size(); ++i) ph[i] = static_cast<float>(p.storage()[i]);
+    DevBuf<float> pd(ph.size());
+    DevBuf<double> sd(1);
+    cuda(cudaMemcpy(pd.p, ph.data(), sizeof(float) * ph.size(), cudaMemcpyHostToDevice));
+    check(ofdmr_estimate_noise_power(c, pd.p, sd.p, 1));
+    double s2 = 0.0;
+    cuda(cudaMemcpy(&s2, sd.p, sizeof(double), cudaMemcpyDeviceToHost));
+    return s2 / window_power_factor;  // (v / ln 2 / 1) / pf == v / ln 2 / pf
+}
+
+// waveform.hpp:81 — CP strip + forward DFT per symbol.
+inline ComplexGrid ofdm_demodulate(std::span<const cplx> stream, const WaveformConfig& cfg) {
+    using namespace detail;
+    const std::size_t n = cfg.n_subcarriers, m = cfg.n_symbols, ns = cfg.samples_per_symbol();
+    if (stream.size() != m * ns) throw ConfigError("stream length must be M*(N+Ncp)");
+    ofdmr_context* c = context(int32_t(n), int32_t(m), int32_t(n), int32_t(m), OFDMR_WINDOW_RECT, OFDMR_EST_LS,
+                               int32_t(cfg.n_cp), 1, 1e-2);
+    std::vector<float> sh(2 * stream.size());
+    for (std::size_t i = 0; i < stream.size(); ++i) {
+        sh[2 * i] = static_cast<float>(stream[i].real());
+        sh[2 * i + 1] = static_cast<float>(stream[i].imag());
+    }
+    DevBuf<float> sd(sh.size()), gd(2 * n * m);
+    cuda(cudaMemcpy(sd.p, sh.data(), sizeof(float) * sh.size(), cudaMemcpyHostToDevice));
+    check(ofdmr_ofdm_demodulate(c, sd.p, gd.p, 1));
+    std::vector<float> gh(2 * n * m);
+    cuda(cudaMemcpy(gh.data(), gd.p, sizeof(float) * gh.size(), cudaMemcpyDeviceToHost));
+    return from_c64(gh, n, m, AxisTag::SubcarrierSymbol);
+}
+
+// waveform.hpp:78 — per-symbol inverse DFT (1/N) with cyclic prefix.
+inline std::vector<cplx> ofdm_modulate(const ComplexGrid& x, const WaveformConfig& cfg) {
+    using namespace detail;
+    const std::size_t n = cfg.n_subcarriers, m = cfg.n_symbols, ns = cfg.samples_per_symbol();
+    if (x.rows() != n || x.cols() != m) throw ConfigError("grid shape does not match config");
+    ofdmr_context* c = context(int32_t(n), int32_t(m), int32_t(n), int32_t(m), OFDMR_WINDOW_RECT, OFDMR_EST_LS,
+                               int32_t(cfg.n_cp), 1, 1e-2);
+    const auto xh = to_c64(x);
+    DevBuf<float> xd(xh.size()), sd(2 * m * ns);
+    cuda(cudaMemcpy(xd.p, xh.data(), sizeof(float) * xh.size(), cudaMemcpyHostToDevice));
+    check(ofdmr_ofdm_modulate(c, xd.p, sd.p, 1));
+    std::vector<float> sh(2 * m * ns);
+    cuda(cudaMemcpy(sh.data(), sd.p, sizeof(float) * sh.size(), cudaMemcpyDeviceToHost));
+    std::vector<cplx> out(m * ns);
+    for (std::size_t i = 0; i < out.size(); ++i) out[i] = cplx(sh[2 * i], sh[2 * i + 1]);
     return out;
 }
 

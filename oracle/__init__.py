@@ -82,6 +82,24 @@ def orc() -> C.CDLL:
     return _orc
 
 
+REF_IO_SO = HERE / "_ref" / "libofdmref_io.so"
+_ref_io = None
+
+
+def ref_io() -> C.CDLL:
+    """The reference's own output writers (io.cpp) behind oracle/ref_shim/ref_io_capi.cpp."""
+    global _ref_io
+    if _ref_io is None:
+        if not REF_IO_SO.exists():
+            raise ImportError(f"{REF_IO_SO} missing (built from /root/reference by `make -f oracle/Makefile ref`)")
+        _ref_io = C.CDLL(str(REF_IO_SO))
+        i64 = C.c_int64
+        _ref_io.ref_write_map_csv.argtypes = [vp, i64, i64, C.c_char_p]
+        _ref_io.ref_write_map_pgm.argtypes = [vp, i64, i64, C.c_char_p]
+        _ref_io.ref_write_detections_csv.argtypes = [vp, vp, vp, vp, vp, i64, C.c_char_p]
+    return _ref_io
+
+
 def ref_available() -> bool:
     return REF_SO.exists()
 

@@ -100,6 +100,7 @@ RECEIVER_SYMBOLS = [
     ("ofdmr_estimate_noise_power", i32, [vp, vp, vp, i64]),
     ("ofdmr_ofdm_demodulate", i32, [vp, vp, vp, i64]),
     ("ofdmr_ofdm_modulate", i32, [vp, vp, vp, i64]),
+    ("ofdmr_map_to_pgm", i32, [vp, vp, vp, i64]),
     ("ofdmr_pipeline", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_general", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_host", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),

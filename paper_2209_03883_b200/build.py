@@ -51,6 +51,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "fused_pg2": [],
         "noise_kernels": [],
         "ofdm_kernels": [],
+        "io_kernels": [],
         "capi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions
         "sft_kernels": ["-fmad=false"],

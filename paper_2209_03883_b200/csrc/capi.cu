@@ -50,6 +50,8 @@ cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_
 int fused_pg_max_clusters();
 int fused_pg_cluster();
 size_t noise_select_scratch_bytes(int64_t frames);
+cudaError_t launch_map_pgm(const float* p, int64_t count, uint8_t* out, int64_t frames, double* scratch,
+                           cudaStream_t st, int64_t* launches);
 cudaError_t launch_ofdm(bool inverse, const float2* in, float2* out, int n, int m, int ncp, int64_t frames,
                         const float2* tw, cudaStream_t st);
 cudaError_t launch_noise_select(const float* p, int64_t count, double pf, double* sigma2_out, int64_t frames,
@@ -1004,6 +1006,19 @@ static int detect_impl(ofdmr_context* c, const float* p, const double* sigma2_h,
         if (e != cudaSuccess) return cuda_fail(e, "merge");
         ++c->launches;
     }
+    return OFDMR_OK;
+}
+
+int ofdmr_map_to_pgm(ofdmr_context* c, const float* p, uint8_t* out, int64_t frames) {
+    if (!c || !p || !out) return fail(OFDMR_ERR_CONFIG, "map_to_pgm: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const int64_t count = int64_t(c->cfg.n_prime) * int64_t(c->cfg.m_prime);
+    double* peak = nullptr;
+    OFDMR_CUDA(cudaMallocAsync(&peak, sizeof(double) * size_t(std::min<int64_t>(frames, 65535)), c->stream));
+    const cudaError_t e = ofdmr::launch_map_pgm(p, count, out, frames, peak, c->stream, &c->launches);
+    cudaFreeAsync(peak, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "map_to_pgm");
     return OFDMR_OK;
 }
 

@@ -315,6 +315,15 @@ class Receiver:
         _check(self._lib.ofdmr_ofdm_modulate(self._h, x.data_ptr(), out.data_ptr(), x.shape[0]))
         return out[0] if single else out
 
+    def map_to_pgm(self, p) -> torch.Tensor:
+        """write_map_pgm's pixels (io.cpp:94-110) for a batch of maps, on the device: uint8
+        (F, N', M'); io.write_pgm_bytes adds the header."""
+        p = self._p_batch(p)
+        out = torch.empty(p.shape, dtype=torch.uint8, device=self.device)
+        self._stream()
+        _check(self._lib.ofdmr_map_to_pgm(self._h, p.data_ptr(), out.data_ptr(), p.shape[0]))
+        return out
+
     def estimate_noise_power(self, p) -> torch.Tensor:
         """estimate_noise_power (periodogram.cpp:146-152) per frame: the order statistic
         P[count / 2] of the map / ln 2 / window power factor (fp64, device)."""

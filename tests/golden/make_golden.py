@@ -169,6 +169,32 @@ def noise_fixtures(R):
         np.savez_compressed(OUT / f"noise_{i}.npz", kind="noise", p=mp_, pf=pf, sigma2=s2)
 
 
+def io_fixture():
+    """The reference's own writers (io.cpp:28-110, oracle/_ref/libofdmref_io.so) on a small map
+    with zeros, sub-floor cells and a wide dynamic range, and on a detection list."""
+    import tempfile
+    W = O.ref_io()
+    rng = np.random.default_rng(28)
+    pm = rng.exponential(size=(16, 8)) * 10.0 ** rng.uniform(-40, 3, size=(16, 8))
+    pm[0, 0] = 0.0
+    pm[3, 5] = 1e-290
+    pm = np.ascontiguousarray(pm)
+    d = np.array([328, 1, 17], np.int64)
+    v = np.array([45, -1, -128], np.int64)
+    pw = np.array([12.5, 3.3e-7, 0.0])
+    rg = np.array([100.0982666015625, 0.30517578125, 5.18798828125])
+    vl = np.array([30.057, -0.6679, -85.5])
+    with tempfile.TemporaryDirectory() as td:
+        files = {}
+        assert W.ref_write_map_csv(p(pm), 16, 8, f"{td}/map.csv".encode()) == 0
+        assert W.ref_write_map_pgm(p(pm), 16, 8, f"{td}/map.pgm".encode()) == 0
+        assert W.ref_write_detections_csv(p(d), p(v), p(pw), p(rg), p(vl), 3, f"{td}/det.csv".encode()) == 0
+        for k in ("map.csv", "map.pgm", "det.csv"):
+            files[k] = np.frombuffer(open(f"{td}/{k}", "rb").read(), np.uint8)
+    np.savez_compressed(OUT / "io_0.npz", kind="io", p=pm, d=d, v=v, pw=pw, rg=rg, vl=vl, map_csv=files["map.csv"],
+                        map_pgm=files["map.pgm"], det_csv=files["det.csv"])
+
+
 if __name__ == "__main__":
     R = O.ref()
     periodogram_fixtures(R)
@@ -178,5 +204,6 @@ if __name__ == "__main__":
     frame_fixture(R)
     ofdm_fixtures(R)
     noise_fixtures(R)
+    io_fixture()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -507,3 +507,25 @@ def test_ofdm_cp_longer_than_symbol_rejected(cuda):
     with Receiver(64, 16, n_cp=65, window="rectangular") as rx:
         with pytest.raises(ConfigError):
             rx.ofdm_modulate(np.zeros((64, 16), np.complex64))
+
+
+def test_map_to_pgm_matches_reference_writer(cuda, tmp_path):
+    """§8(f) item 4: write_map_pgm pixels (io.cpp:94-110) computed on the GPU for a batch of
+    device maps equal the host restatement byte for byte, and (where the reference's writer
+    library was built) the reference's own file for the same map."""
+    from paper_2209_03883_b200 import io as W
+    n, m = 1024, 256
+    h = np.stack([gen.noise_grid(n, m, 1.0, 900 + f) for f in range(3)]).astype(np.complex64)
+    h[1] += 4.0 * np.exp(1j * TWO_PI * (-np.arange(n)[:, None] * 9 / n + np.arange(m)[None, :] * 5 / m))
+    with Receiver(n, m, window=1) as rx:
+        p = rx.periodogram(h)
+        p[2] = 0.0  # degenerate map: peak 0 -> 1 (io.cpp:99)
+        px = rx.map_to_pgm(p).cpu().numpy()
+    pn = p.cpu().numpy()
+    for f in range(3):
+        assert np.array_equal(px[f], W.pgm_pixels(pn[f])), f
+    W.write_pgm_bytes(tmp_path / "g.pgm", px[1])
+    if O.REF_IO_SO.exists():
+        pd = np.ascontiguousarray(pn[1], np.float64)
+        assert O.ref_io().ref_write_map_pgm(pd.ctypes.data, n, m, str(tmp_path / "r.pgm").encode()) == 0
+        assert (tmp_path / "g.pgm").read_bytes() == (tmp_path / "r.pgm").read_bytes()
