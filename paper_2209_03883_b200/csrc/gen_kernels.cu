@@ -23,8 +23,12 @@
 // mean_power(x) is summed sequentially in cell order by one thread, as the CPU does.
 // Pass 1 writes x_tx (and the running |x|^2 sum); pass 2 re-reads x_tx (exact decode of the
 // c64 value back to its fp64 constellation point), applies the channel and adds the noise.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include <cuda_runtime.h>
 
@@ -144,6 +148,12 @@ struct GenArgs {
     int exp_count;
     double exp_range[kMaxT], exp_vel[kMaxT];
     double exp_snr;
+    // ZC-precoded frames (zadoffchu.cpp:58-87,133-136) run as three launches:
+    //   mode 1: scene + pilots + payload -> fp64 x in xd (no channel),
+    //   (precode_kernel: x_tx = Z x per column, fp64),
+    //   mode 2: scene again (same streams), mean_power of the fp64 x_tx, channel + noise.
+    int mode;               // 0: unprecoded single pass
+    double2* xd;            // mode 1: fp64 x out; mode 2: fp64 x_tx in ([count][N][M])
 };
 
 struct GenShared {
@@ -239,6 +249,8 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
 
     // ---- pilots: n draws of uniform_int(4) (warp 0)
     const uint32_t mask = a.ring_mask;
+    double2* xdf = a.xd ? a.xd + (size_t)f * n * m : nullptr;
+    if (a.mode != 2) {
     if (w == 0) {
         if (tid == 0) mt_seed(s.mt, splitmix(fx, 0ull));
         __syncwarp();
@@ -290,18 +302,38 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
                 xr = a.lev_d[a.lev_of_gray[gi]];
                 xi = a.lev_d[a.lev_of_gray[gq]];
             }
-            xo[(size_t)k * m + l] = make_float2((float)xr, (float)xi);
-            nr[l] = xr * xr + xi * xi;
+            if (a.mode == 1) {
+                xdf[(size_t)k * m + l] = make_double2(xr, xi);
+            } else {
+                xo[(size_t)k * m + l] = make_float2((float)xr, (float)xi);
+                nr[l] = xr * xr + xi * xi;
+            }
         }
         consumed += need;
         __syncthreads();
-        if (tid == 32) {  // sequential sum of this row (gen.cpp mean_power order)
+        if (tid == 32 && a.mode == 0) {  // sequential sum of this row (gen.cpp mean_power order)
             double acc = s.mp;
             for (int l = 0; l < m; ++l) acc += nr[l];
             s.mp = acc;
         }
     }
     __syncthreads();
+    if (a.mode == 1) {
+        if (tid == 0) a.status[f] = s.rej ? 1 : 0;
+        return;
+    }
+    } else {
+        // mode 2: mean_power of the precoded fp64 x_tx, sequentially in cell order (gen.cpp)
+        if (tid == 32) {
+            double acc = 0.0;
+            for (size_t i = 0; i < (size_t)n * m; ++i) {
+                const double2 v = xdf[i];
+                acc += v.x * v.x + v.y * v.y;
+            }
+            s.mp = acc;
+        }
+        __syncthreads();
+    }
 
     // ---- sigma2 (channel.cpp:86-89) and the noise stream
     const bool noisy = isfinite(s.snr_db);
@@ -322,8 +354,7 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
     __syncthreads();
 
     // ---- pass 2: channel + noise, row by row
-    produced = 0;
-    consumed = 0;
+    uint32_t produced = 0, consumed = 0;
     const uint32_t need2 = noisy ? 2u * (uint32_t)m : 0u;
     const double sd = s.sd;
     for (int k = 0; k < n; ++k) {
@@ -343,10 +374,14 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
         }
         __syncthreads();
         for (int l = tid; l < m; l += 256) {
-            // exact fp64 x from the stored c64 value
-            const float2 xf = xo[(size_t)k * m + l];
+            // exact fp64 x from the stored c64 value (or the precoded fp64 x_tx in mode 2)
             double xr, xi;
-            if (l == 0) {
+            if (a.mode == 2) {
+                const double2 xv = xdf[(size_t)k * m + l];
+                xr = xv.x;
+                xi = xv.y;
+                xo[(size_t)k * m + l] = make_float2((float)xr, (float)xi);
+            } else if (const float2 xf = xo[(size_t)k * m + l]; l == 0) {
                 xr = xf.x < 0.f ? -a.inv_sqrt2 : a.inv_sqrt2;
                 xi = xf.y < 0.f ? -a.inv_sqrt2 : a.inv_sqrt2;
             } else {
@@ -393,7 +428,77 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
         consumed += need2;
         __syncthreads();
     }
-    if (tid == 0) a.status[f] = s.rej ? 1 : 0;
+    if (tid == 0) a.status[f] = a.mode == 2 ? (a.status[f] | (s.rej ? 1 : 0)) : (s.rej ? 1 : 0);
+}
+
+// zadoffchu.cpp:98-119 sequence of length D^2 (D = N), reshaped row-major into the D x D
+// matrix (gen.cpp zc_matrix): the same fp64 expressions, GPU sincos.
+__global__ void zc_matrix_kernel(int n, long long root, double2* z) {
+    const long long l = (long long)n * (long long)n;
+    const double rl = double(root) / double(l);
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < l; k += (long long)gridDim.x * blockDim.x) {
+        const double kk = double(k);
+        double cycles;
+        if (l % 2 == 0) cycles = rl * (kk * kk / 2.0 + 0.0 * kk);
+        else cycles = rl * (kk * (kk + 1.0) / 2.0 + 0.0 * kk);
+        cycles -= floor(cycles);
+        double sn, cs;
+        sincos(kTwoPiG * cycles, &sn, &cs);
+        z[k] = make_double2(1.0 * cs, 1.0 * sn);
+    }
+}
+
+// x_tx[:, l] = Z x[:, l] (gen.cpp precode_direct / zadoffchu.cpp apply_matrix, d == n): every
+// output is the sequential sum over mm = 0..n-1 of std::complex products (re = ac - bd,
+// im = ad + bc, no FMA: this unit is built with -fmad=false).  64 x 64 output tiles, 4 x 4
+// per thread, K chunks of 16 through shared memory.
+__global__ void __launch_bounds__(256) zc_precode_kernel(const double2* __restrict__ z, const double2* __restrict__ x,
+                                                         double2* __restrict__ out, int n, int m) {
+    __shared__ double2 zs[64][17];
+    __shared__ double2 xs[16][65];
+    const int tiles_l = (m + 63) / 64;
+    const int i0 = (blockIdx.x / tiles_l) * 64, l0 = (blockIdx.x % tiles_l) * 64;
+    const size_t fo = (size_t)blockIdx.y * n * m;
+    const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;  // outputs i0 + ty + 16 a, l0 + tx + 16 b
+    double ar[4][4], ai[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) ar[u][v] = ai[u][v] = 0.0;
+    for (int k0 = 0; k0 < n; k0 += 16) {
+        for (int idx = threadIdx.x; idx < 64 * 16; idx += 256) {
+            const int r = idx / 16, c = idx % 16;
+            zs[r][c] = (i0 + r < n) ? z[(size_t)(i0 + r) * n + k0 + c] : make_double2(0.0, 0.0);
+            const int r2 = idx / 64, c2 = idx % 64;
+            xs[r2][c2] = (l0 + c2 < m) ? x[fo + (size_t)(k0 + r2) * m + l0 + c2] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < 16; ++kk) {
+            double2 zv[4], xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) zv[u] = zs[ty + 16 * u][kk];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) xv[v] = xs[kk][tx + 16 * v];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const double pr = zv[u].x * xv[v].x - zv[u].y * xv[v].y;
+                    const double pi = zv[u].x * xv[v].y + zv[u].y * xv[v].x;
+                    ar[u][v] = ar[u][v] + pr;
+                    ai[u][v] = ai[u][v] + pi;
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = i0 + ty + 16 * u, l = l0 + tx + 16 * v;
+            if (i < n && l < m) out[fo + (size_t)i * m + l] = make_double2(ar[u][v], ai[u][v]);
+        }
 }
 
 int gray_decode_h(unsigned g) {
@@ -406,6 +511,24 @@ int gray_decode_h(unsigned g) {
 }  // namespace ofdmr
 
 namespace {
+// Device ZC matrices, built once per (device, N, root) and kept for the process.
+double2* zc_device_matrix(int n, long long root, cudaStream_t st) {
+    static std::mutex mtx;
+    static std::map<std::tuple<int, int, long long>, double2*> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mtx);
+    const auto key = std::make_tuple(dev, n, root);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    double2* z = nullptr;
+    if (cudaMalloc(&z, sizeof(double2) * (size_t)n * n) != cudaSuccess) return nullptr;
+    ofdmr::zc_matrix_kernel<<<1184, 256, 0, st>>>(n, root, z);
+    if (cudaGetLastError() != cudaSuccess) return nullptr;
+    cache.emplace(key, z);
+    return z;
+}
+
 int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int64_t count, void* y, void* x_tx,
                double* sigma2, int32_t* n_targets, double* ranges, double* vels, double* snr_db, int32_t max_targets,
                int32_t* status, void* stream, const double* exp_ranges, const double* exp_vels, int32_t exp_count,
@@ -421,8 +544,8 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
         case 256: bps = 8; break;
         default: return 2;
     }
-    if (p->zc_precode || p->n <= 0 || p->m < 2 || p->m > kMaxM || p->targets_max > kMaxT || p->targets_min < 0 ||
-        p->targets_max < p->targets_min || count > (int64_t)1 << 30)
+    if (p->n <= 0 || p->m < 2 || p->m > kMaxM || p->targets_max > kMaxT || p->targets_min < 0 ||
+        p->targets_max < p->targets_min || count > (int64_t)1 << 30 || (p->zc_precode && p->n > 4096))
         return 2;
     GenArgs a{};
     a.p = *p;
@@ -471,7 +594,45 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
                         sizeof(double) * 2 * p->m + sizeof(uint64_t) * ring + (size_t)p->n;
     cudaError_t e = cudaFuncSetAttribute(gen_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return 10;
-    gen_frame_kernel<<<(unsigned)count, 256, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!p->zc_precode) {
+        gen_frame_kernel<<<(unsigned)count, 256, smem, st>>>(a);
+        return cudaGetLastError() == cudaSuccess ? 0 : 10;
+    }
+    // ZC precode (D = N): x (fp64) -> Z x per column -> channel, in chunks of frames
+    const size_t cells = (size_t)p->n * p->m;
+    double2* z = zc_device_matrix(p->n, p->zc_root, st);
+    if (!z) return 10;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(count, ((int64_t)512 << 20) / (int64_t)(cells * 16)));
+    double2 *xb = nullptr, *tb = nullptr;
+    if (cudaMallocAsync(&xb, sizeof(double2) * cells * chunk, st) != cudaSuccess ||
+        cudaMallocAsync(&tb, sizeof(double2) * cells * chunk, st) != cudaSuccess)
+        return 10;
+    const int tiles = ((p->n + 63) / 64) * ((p->m + 63) / 64);
+    for (int64_t c0 = 0; c0 < count; c0 += chunk) {
+        const int64_t nc = std::min<int64_t>(chunk, count - c0);
+        GenArgs b = a;
+        b.first = first + c0;
+        b.count = (int)nc;
+        b.y = a.y + c0 * cells;
+        b.x = a.x + c0 * cells;
+        b.sigma2 = a.sigma2 + c0;
+        b.n_targets = a.n_targets + c0;
+        b.status = a.status + c0;
+        if (a.ranges) b.ranges = a.ranges + c0 * a.max_targets;
+        if (a.vels) b.vels = a.vels + c0 * a.max_targets;
+        if (a.snr_db) b.snr_db = a.snr_db + c0;
+        if (a.h_true) b.h_true = a.h_true + c0 * cells;
+        b.mode = 1;
+        b.xd = xb;
+        gen_frame_kernel<<<(unsigned)nc, 256, smem, st>>>(b);
+        zc_precode_kernel<<<dim3((unsigned)tiles, (unsigned)nc), 256, 0, st>>>(z, xb, tb, p->n, p->m);
+        b.mode = 2;
+        b.xd = tb;
+        gen_frame_kernel<<<(unsigned)nc, 256, smem, st>>>(b);
+    }
+    cudaFreeAsync(xb, st);
+    cudaFreeAsync(tb, st);
     return cudaGetLastError() == cudaSuccess ? 0 : 10;
 }
 }  // namespace

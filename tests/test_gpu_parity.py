@@ -529,3 +529,23 @@ def test_map_to_pgm_matches_reference_writer(cuda, tmp_path):
         pd = np.ascontiguousarray(pn[1], np.float64)
         assert O.ref_io().ref_write_map_pgm(pd.ctypes.data, n, m, str(tmp_path / "r.pgm").encode()) == 0
         assert (tmp_path / "g.pgm").read_bytes() == (tmp_path / "r.pgm").read_bytes()
+
+
+@pytest.mark.parametrize("cfg,F", [(configs.CFG2.replace(n=256, m=64, n_prime=512, m_prime=128, n_cp=32), 6),
+                                   (configs.CFG2, 1)], ids=["zc256x64", "cfg2"])
+def test_gpu_generator_zc_precoded(cuda, cfg, F):
+    """§8(f) item 1, ZC precode (zadoffchu.cpp:58-87,133-136, D = N): the device generator's
+    fp64 x -> Z x -> channel path against the CPU generator.  The ZC matrix uses the GPU's
+    sincos, so precoded cells may differ in the last c64 bit; symbols' scene, counts exact."""
+    ref = gen.frames(cfg, 3, F)
+    d = gen.frames_device(cfg, 3, F)
+    assert d["regenerated_on_cpu"] == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(d["n_targets"].cpu().numpy(), ref.n_targets)
+    assert np.array_equal(d["snr_db"].cpu().numpy(), ref.snr_db)
+    s2 = d["sigma2"].cpu().numpy()
+    assert np.all(np.abs(s2 - ref.sigma2) <= 1e-12 * ref.sigma2), (s2, ref.sigma2)
+    for name, got, want in (("x", d["x"].cpu().numpy(), ref.x), ("y", d["y"].cpu().numpy(), ref.y)):
+        u = _ulp_dist(got.view(np.float32), want.view(np.float32))
+        assert u.max() <= 4, (name, u.max())
+        assert (u > 0).mean() <= 0.05, (name, (u > 0).mean())
