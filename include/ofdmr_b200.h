@@ -169,6 +169,13 @@ int ofdmr_sft(ofdmr_context* ctx, const void* h, int32_t n, int32_t m, const ofd
               int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged,
               double* residual, int64_t frames);
 
+/* estimate_noise_from_slice, pipeline.cpp:26-43 (run_pipeline's FPS-SFT estimate-noise mode,
+ * pipeline.cpp:97-98): per frame, Rng(seeds[f]) draws the admissible slope, the slice of
+ * length Q = lcm(N, M) through (0, 0) is FFT'd, sigma2_out[f] = median(|S|^2 / Q^2) * Q / ln 2.
+ * seeds on the host, h and sigma2_out on the device (power-of-two N, M, Q <= 2048). */
+int ofdmr_sft_estimate_noise(ofdmr_context* ctx, const void* h, int32_t n, int32_t m, const uint64_t* seeds,
+                             double* sigma2_out, int64_t frames);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,8 @@ def orc() -> C.CDLL:
         _orc.orc_periodogram.argtypes = [vp, sz, sz, vp, vp, sz, sz, vp]
         _orc.orc_detection_threshold.argtypes = [C.c_double, C.c_double, C.c_double, vp]
         _orc.orc_ofdm_modulate.argtypes = [vp, sz, sz, sz, vp]
+        _orc.orc_estimate_noise_from_slice.restype = C.c_double
+        _orc.orc_estimate_noise_from_slice.argtypes = [vp, sz, sz, C.c_uint64]
         _orc.orc_ofdm_demodulate.argtypes = [vp, sz, sz, sz, vp]
     return _orc
 
@@ -135,6 +137,7 @@ def ref() -> C.CDLL:
         _ref.ref_sft_batch_c64.argtypes = [vp, i64, i64, i64, i64, vp, vp, d, i64, i64, vp, vp, vp, vp, vp, C.c_int]
         _ref.ref_make_frame_pair.argtypes = [i64, i64, d, d, i64, C.c_int, vp, vp, i64, d, C.c_uint64, vp, vp, vp]
         _ref.ref_rng_u64.argtypes = [C.c_uint64, i64, vp]
+        _ref.ref_sft_noise_case.argtypes = [i64, i64, d, d, i64, vp, vp, C.c_int32, d, C.c_uint64, vp, vp]
         _ref.ref_estimate_noise_power.restype = d
         _ref.ref_estimate_noise_power.argtypes = [vp, i64, i64, d]
         _ref.ref_ofdm_modulate.argtypes = [vp, i64, i64, i64, vp]
@@ -223,6 +226,12 @@ def division_noise_power(sigma2: float, x: np.ndarray) -> float:
 def estimate_noise_power(p: np.ndarray, pf: float) -> float:
     p = np.ascontiguousarray(p, np.float64)
     return orc().orc_estimate_noise_power(_p(p), p.size, pf)
+
+
+def estimate_noise_from_slice(h: np.ndarray, seed: int) -> float:
+    """pipeline.cpp:26-43 (FPS-SFT estimate-noise mode) on an N x M grid (fp64)."""
+    h = np.ascontiguousarray(h, np.complex128)
+    return orc().orc_estimate_noise_from_slice(_p(h), h.shape[0], h.shape[1], seed)
 
 
 def ofdm_modulate(x: np.ndarray, n_cp: int) -> np.ndarray:

@@ -551,6 +551,39 @@ int orc_slope_admissible(long v1, long v2, size_t n, size_t m) {
 }
 
 /* sft.cpp:73-83 tone_bin. */
+/* pipeline.cpp:26-43 estimate_noise_from_slice (FPS-SFT estimate-noise mode): admissible
+ * slope from Rng(seed) (v1 = 1 + U(N-1), v2 = 1 + U(M-1) until admissible), the slice
+ * through (0, 0) of length Q = lcm(N, M), forward FFT, p = |s|^2 / Q^2, the order statistic
+ * p[Q/2] (nth_element) * Q / ln 2.  Output also the slope (for the GPU path's host draws). */
+static int cmp_d(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
+double orc_estimate_noise_from_slice(const cd* h, size_t n, size_t m, uint64_t seed) {
+    const size_t q = lcm_sz(n, m);
+    orc_rng r;
+    orc_rng_seed(&r, seed);
+    long v1 = 1, v2 = 1;
+    do {
+        v1 = (long)(1 + orc_rng_uniform_int(&r, n > 1 ? n - 1 : 1));
+        v2 = (long)(1 + orc_rng_uniform_int(&r, m > 1 ? m - 1 : 1));
+    } while (!orc_slope_admissible(v1, v2, n, m));
+    double* s = (double*)malloc(sizeof(double) * 2 * q);
+    double* p = (double*)malloc(sizeof(double) * q);
+    for (size_t t = 0; t < q; t++) {
+        const size_t k = (size_t)(((unsigned long long)v1 * t) % n), l = (size_t)(((unsigned long long)v2 * t) % m);
+        s[2 * t] = creal(h[k * m + l]);
+        s[2 * t + 1] = cimag(h[k * m + l]);
+    }
+    orc_fft(s, q, -1);
+    for (size_t i = 0; i < q; i++) p[i] = (s[2 * i] * s[2 * i] + s[2 * i + 1] * s[2 * i + 1]) / ((double)q * (double)q);
+    qsort(p, q, sizeof(double), cmp_d);
+    const double out = p[q / 2] * (double)q / 0.6931471805599453;
+    free(s);
+    free(p);
+    return out;
+}
+
 static size_t tone_bin(long k, long l, long v1, long v2, size_t n, size_t m, size_t q) {
     const unsigned long long qn = q / n, qm = q / m;
     const unsigned long long f = ((unsigned long long)v1 * (unsigned long long)k * qn +

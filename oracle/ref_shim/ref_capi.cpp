@@ -352,6 +352,33 @@ int ref_run_pipeline(int64_t n, int64_t m, int64_t np, int64_t mp, double df, do
     }
 }
 
+/// run_pipeline (pipeline.cpp:60-115) with the FPS-SFT detector in estimate-noise mode: the
+/// reference's own sigma2_used (= estimate_noise_from_slice(h, derive_seed(seed, 0x6e6573)),
+/// an anonymous-namespace function) and the channel estimate h it was computed from, rebuilt
+/// with the same public calls run_pipeline makes (pipeline.cpp:65-72).
+int ref_sft_noise_case(int64_t n, int64_t m, double df, double fc, int64_t n_cp, const double* ranges,
+                       const double* vels, int32_t count, double snr_db, uint64_t seed, double* h_out,
+                       double* sigma2_used) {
+    try {
+        SimulationConfig cfg = scenario(n, m, n, m, df, fc, n_cp, 0, 0.01, 0, ranges, vels, count);
+        cfg.channel.snr_db = snr_db;
+        cfg.detector.kind = DetectorKind::FpsSft;
+        cfg.detector.estimate_noise = true;
+        const auto res = run_pipeline(cfg, seed);
+        *sigma2_used = res.sigma2_used;
+        const WaveformConfig& w = cfg.waveform;
+        const ComplexGrid x = make_random_frame(w, derive_seed(seed, 0x667261));
+        auto [y, realization] = apply_channel(x, cfg.targets, w, cfg.channel.snr_db, seed, cfg.channel.amplitude_mode);
+        (void)realization;
+        grid_to(estimate_channel(y, x, cfg), h_out);
+        return 0;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (...) {
+        return 3;
+    }
+}
+
 /// The reference's own Monte-Carlo RMSE sweep (metrics.cpp:92-120) on a scenario built from
 /// plain parameters: QPSK, normalized gains, random phases, targets (ranges, vels),
 /// estimator 0 LS / 1 DFT-CE.  rows[i] = {range_rmse_m, velocity_rmse_mps, miss_rate}.

@@ -105,6 +105,7 @@ RECEIVER_SYMBOLS = [
     ("ofdmr_pipeline_general", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_host", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_sft", i32, [vp, vp, i32, i32, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
+    ("ofdmr_sft_estimate_noise", i32, [vp, vp, i32, i32, vp, vp, i64]),
 ]
 
 # include/ofdmr_gen.h, device side (in the CUDA library)

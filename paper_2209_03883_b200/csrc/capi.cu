@@ -1276,6 +1276,18 @@ int ofdmr_pipeline_host(ofdmr_context* c, const void* y, const void* x, const do
     return OFDMR_OK;
 }
 
+int ofdmr_sft_estimate_noise(ofdmr_context* c, const void* h, int32_t n, int32_t m, const uint64_t* seeds,
+                             double* sigma2_out, int64_t frames) {
+    if (!c || !h || !seeds || !sigma2_out) return fail(OFDMR_ERR_CONFIG, "estimate_noise_from_slice: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    std::string err;
+    const int rc = sft_slice_noise(c->sft, c->stream, static_cast<const float2*>(h), n, m, seeds, sigma2_out, frames,
+                                   &c->launches, err);
+    if (rc) return fail(rc, err);
+    return OFDMR_OK;
+}
+
 int ofdmr_sft(ofdmr_context* c, const void* h, int32_t n, int32_t m, const ofdmr_sft_config* cfg,
               const uint64_t* seeds, const double* sigma2, int32_t* k_out, int32_t* l_out, double* amp_out,
               int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged, double* residual,

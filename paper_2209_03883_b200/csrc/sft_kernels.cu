@@ -519,6 +519,46 @@ uint64_t uniform_int(std::mt19937_64& e, uint64_t n) {
     return v % n;
 }
 
+// pipeline.cpp:26-43 estimate_noise_from_slice: one CTA per frame; the slice through (0, 0)
+// along the host-drawn slope, the oracle's radix-2 fp64 FFT (bit-identical spectrum),
+// p = |s|^2 / Q^2, bitonic sort, p[Q/2] * Q / ln 2.
+__global__ void __launch_bounds__(kSftNT) slice_noise_kernel(const float2* __restrict__ hall, int n, int m, int q,
+                                                             int logq, const int32_t* __restrict__ slopes,
+                                                             const double2* __restrict__ tw, double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* sp = reinterpret_cast<double2*>(smem_raw);  // [q]
+    double* pw = reinterpret_cast<double*>(sp + q);       // [q]
+    const int fr = blockIdx.x;
+    const float2* h = hall + (size_t)fr * n * m;
+    const long long v1 = slopes[2 * fr], v2 = slopes[2 * fr + 1];
+    for (int t = threadIdx.x; t < q; t += kSftNT) {
+        const int r = (int)((v1 * t) % n), c = (int)((v2 * t) % m);
+        const float2 v = h[(size_t)r * m + c];
+        sp[t] = make_double2((double)v.x, (double)v.y);
+    }
+    __syncthreads();
+    fft_r2(sp, q, logq, tw);
+    const double qq = (double)q * (double)q;
+    for (int t = threadIdx.x; t < q; t += kSftNT) pw[t] = dnorm(sp[t]) / qq;
+    __syncthreads();
+    for (int k = 2; k <= q; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < q; i += kSftNT) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const double a0 = pw[i], a1 = pw[ixj];
+                    const bool up = (i & k) == 0;
+                    if (up ? (a0 > a1) : (a0 < a1)) {
+                        pw[i] = a1;
+                        pw[ixj] = a0;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    if (threadIdx.x == 0) out[fr] = pw[q / 2] * (double)q / 0.6931471805599453;
+}
+
 template <typename T>
 cudaError_t ensure(T** p, int64_t& cap, int64_t need) {
     if (*p && cap >= need) return cudaSuccess;
@@ -531,6 +571,48 @@ cudaError_t ensure(T** p, int64_t& cap, int64_t need) {
 }
 
 }  // namespace
+
+int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const uint64_t* seeds,
+                    double* sigma2_out, int64_t frames, int64_t* launches, std::string& err) {
+    auto pow2 = [](int v) { return v >= 2 && (v & (v - 1)) == 0; };
+    if (!pow2(n) || !pow2(m)) { err = "estimate_noise_from_slice: N and M must be powers of two on the GPU path"; return OFDMR_ERR_CONFIG; }
+    const int q = int(lcm_ll(n, m));
+    if (q > 2048 || q < 16) { err = "estimate_noise_from_slice: Q = lcm(N, M) must lie in [16, 2048]"; return OFDMR_ERR_CONFIG; }
+    if (frames > 0x7fffffff) { err = "estimate_noise_from_slice: too many frames"; return OFDMR_ERR_CONFIG; }
+    std::vector<int32_t> slopes(size_t(frames) * 2);
+    for (int64_t f = 0; f < frames; ++f) {  // Rng(seed), pipeline.cpp:31-35
+        std::mt19937_64 e(seeds[f]);
+        long long v1, v2;
+        do {
+            v1 = (long long)(1 + uniform_int(e, n > 1 ? n - 1 : 1));
+            v2 = (long long)(1 + uniform_int(e, m > 1 ? m - 1 : 1));
+        } while (!slope_admissible(v1, v2, n, m));
+        slopes[2 * f] = int32_t(v1);
+        slopes[2 * f + 1] = int32_t(v2);
+    }
+    std::vector<double2> twf(q / 2);
+    for (int k = 0; k < q / 2; ++k) {
+        const double ang = (double)(-1) * kTwoPiD * (double)k / (double)q;
+        twf[k] = make_double2(std::cos(ang), std::sin(ang));
+    }
+    int64_t cap_q = s.cap_q;
+    cudaError_t e = ensure(&s.draws, s.cap_draws, int64_t(slopes.size()));
+    if (e == cudaSuccess) e = ensure(&s.tw_fft, cap_q, q);
+    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    s.cap_q = int(std::min<int64_t>(cap_q, s.cap_q ? s.cap_q : cap_q));
+    e = cudaMemcpyAsync(s.draws, slopes.data(), sizeof(int32_t) * slopes.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(s.tw_fft, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host vectors go out of scope
+    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    int logq = 0;
+    while ((1 << logq) < q) ++logq;
+    const size_t smem = sizeof(double2) * q + sizeof(double) * q;
+    slice_noise_kernel<<<unsigned(frames), kSftNT, smem, st>>>(h, n, m, q, logq, s.draws, s.tw_fft, sigma2_out);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    if (launches) ++*launches;
+    return OFDMR_OK;
+}
 
 void sft_free(SftScratch& s) {
     cudaFree(s.draws);

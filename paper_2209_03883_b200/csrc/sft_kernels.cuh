@@ -30,4 +30,9 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
             int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged, double* residual,
             int64_t frames, int64_t* launches, std::string& err);
 
+// pipeline.cpp:26-43 estimate_noise_from_slice for a batch of N x M c64 grids; seeds on the
+// host (the Rng seed, i.e. derive_seed(run seed, 0x6e6573) in run_pipeline); output on device.
+int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const uint64_t* seeds,
+                    double* sigma2_out, int64_t frames, int64_t* launches, std::string& err);
+
 }  // namespace ofdmr

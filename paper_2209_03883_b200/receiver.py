@@ -463,6 +463,17 @@ class Receiver:
                                    out["residual"].data_ptr(), F))
         return out
 
+    def estimate_noise_from_slice(self, h, seeds) -> torch.Tensor:
+        """estimate_noise_from_slice (pipeline.cpp:26-43), the FPS-SFT detector's estimate-noise
+        mode: seeds[f] is the Rng seed (run_pipeline passes derive_seed(seed, 0x6e6573))."""
+        h, single = _batched(_as_grid(h, self.device))
+        F, n, m = h.shape
+        seeds = np.ascontiguousarray(np.broadcast_to(np.asarray(seeds, np.uint64), (F,)))
+        out = torch.empty(F, dtype=torch.float64, device=self.device)
+        self._stream()
+        _check(self._lib.ofdmr_sft_estimate_noise(self._h, h.data_ptr(), n, m, seeds.ctypes.data, out.data_ptr(), F))
+        return out[0] if single else out
+
 
 # ---------------------------------------------------------------------------------
 # Module-level functions with the reference's names (single frame, value semantics).

@@ -195,6 +195,21 @@ def io_fixture():
                         map_pgm=files["map.pgm"], det_csv=files["det.csv"])
 
 
+def sft_noise_fixtures(R):
+    """run_pipeline with the FPS-SFT detector in estimate-noise mode: the reference's
+    sigma2_used and the channel estimate it came from (estimate_noise_from_slice is internal
+    to pipeline.cpp, so it is pinned through run_pipeline)."""
+    cases = [(64, 32, 16, 2, 10.0, 77), (48, 20, 12, 1, 0.0, 1234), (128, 64, 32, 3, -5.0, 99)]
+    for i, (n, m, ncp, cnt, snr, seed) in enumerate(cases):
+        df = 491.5e6 / n
+        ranges = np.array([1.0, 2.5, 3.3][:cnt])
+        vels = np.array([3.0, -5.5, 7.25][:cnt])
+        h = np.empty((n, m), np.complex128)
+        s2 = C.c_double()
+        assert R.ref_sft_noise_case(n, m, df, 77e9, ncp, p(ranges), p(vels), cnt, snr, seed, p(h), C.byref(s2)) == 0
+        np.savez_compressed(OUT / f"sft_noise_{i}.npz", kind="sft_noise", h=h, seed=seed, sigma2=s2.value)
+
+
 if __name__ == "__main__":
     R = O.ref()
     periodogram_fixtures(R)
@@ -205,5 +220,6 @@ if __name__ == "__main__":
     ofdm_fixtures(R)
     noise_fixtures(R)
     io_fixture()
+    sft_noise_fixtures(R)
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

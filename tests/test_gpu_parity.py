@@ -549,3 +549,19 @@ def test_gpu_generator_zc_precoded(cuda, cfg, F):
         u = _ulp_dist(got.view(np.float32), want.view(np.float32))
         assert u.max() <= 4, (name, u.max())
         assert (u > 0).mean() <= 0.05, (name, (u > 0).mean())
+
+
+@pytest.mark.parametrize("n,m", [(64, 32), (1024, 1024), (256, 16), (16, 2048)])
+def test_sft_estimate_noise_from_slice(cuda, n, m):
+    """estimate_noise_from_slice (pipeline.cpp:26-43): same host slope draws, the oracle's
+    radix-2 FFT schedule in fp64 and an exact median, so the GPU value equals the oracle's
+    bit for bit on identical c64 grids (the oracle itself is pinned to the reference's
+    run_pipeline sigma2_used, tests/golden/sft_noise_*.npz)."""
+    F = 4
+    h = np.stack([gen.noise_grid(n, m, 0.5 + f, 40 + f) for f in range(F)]).astype(np.complex64)
+    seeds = np.array([O.derive_seed(7 + f, 0x6E6573) for f in range(F)], np.uint64)
+    with Receiver(16, 16) as rx:
+        got = rx.estimate_noise_from_slice(h, seeds).cpu().numpy()
+    for f in range(F):
+        ref = O.estimate_noise_from_slice(h[f].astype(np.complex128), int(seeds[f]))
+        assert got[f] == ref, (f, got[f], ref)
