@@ -99,6 +99,10 @@ def ref_io() -> C.CDLL:
         _ref_io.ref_write_map_csv.argtypes = [vp, i64, i64, C.c_char_p]
         _ref_io.ref_write_map_pgm.argtypes = [vp, i64, i64, C.c_char_p]
         _ref_io.ref_write_detections_csv.argtypes = [vp, vp, vp, vp, vp, i64, C.c_char_p]
+        i32, d = C.c_int32, C.c_double
+        _ref_io.ref_write_run_manifest.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, i64, i64, d, d, i64, i32, i64,
+                                                   i64, i32, d, i32, i32, i64, i32, i64, vp, vp, vp, i32, d, vp, vp,
+                                                   i32, d]
     return _ref_io
 
 

@@ -210,6 +210,38 @@ def sft_noise_fixtures(R):
         np.savez_compressed(OUT / f"sft_noise_{i}.npz", kind="sft_noise", h=h, seed=seed, sigma2=s2.value)
 
 
+MANIFEST_CASES = [
+    # (command, seed, n, m, df, fc, ncp, qam, np, mp, window, pfa, est, det, K, est_noise, i_max,
+    #  ranges, vels, phases, snr, extra, wall_ms)
+    ("run", 7, 1024, 256, 491.5e6 / 1024, 77e9, 256, 4, 1024, 256, 0, 0.01, 0, 0, 3, 0, 10,
+     [100.0, 31.25], [30.0, -12.5], None, 10.0, [], 12.5),
+    ("rmse", 20220908, 2048, 512, 491.5e6 / 2048, 77e9, 256, 16, 4096, 2048, 1, 1e-05, 1, 1, 8, 1, 8,
+     [5.5], [-80.0], [0.25], float("inf"), [("snr_db", "-10:20:5"), ("trials", "200")], 123456.789),
+]
+
+
+def manifest_fixtures():
+    import tempfile
+    W = O.ref_io()
+    for i, c in enumerate(MANIFEST_CASES):
+        (cmd, seed, n, m, df, fc, ncp, qam, np_, mp, win, pfa, est, det, K, en, imax, rg, vl, ph, snr, extra,
+         wall) = c
+        rg_a = np.ascontiguousarray(rg, np.float64)
+        vl_a = np.ascontiguousarray(vl, np.float64)
+        ph_a = np.ascontiguousarray(ph, np.float64) if ph is not None else None
+        ks = (C.c_char_p * max(1, len(extra)))(*[k.encode() for k, _ in extra])
+        vs = (C.c_char_p * max(1, len(extra)))(*[v.encode() for _, v in extra])
+        with tempfile.TemporaryDirectory() as td:
+            path = f"{td}/run.json"
+            rc = W.ref_write_run_manifest(path.encode(), cmd.encode(), seed, n, m, df, fc, ncp, qam, np_, mp, win, pfa,
+                                          est, det, K, en, imax, p(rg_a), p(vl_a),
+                                          p(ph_a) if ph_a is not None else None, len(rg), snr, ks, vs, len(extra),
+                                          wall)
+            assert rc == 0
+            data = np.frombuffer(open(path, "rb").read(), np.uint8)
+        np.savez_compressed(OUT / f"manifest_{i}.npz", kind="manifest", case=i, run_json=data)
+
+
 if __name__ == "__main__":
     R = O.ref()
     periodogram_fixtures(R)
@@ -221,5 +253,6 @@ if __name__ == "__main__":
     noise_fixtures(R)
     io_fixture()
     sft_noise_fixtures(R)
+    manifest_fixtures()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
