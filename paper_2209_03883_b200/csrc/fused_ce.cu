@@ -451,9 +451,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         // this step's edge columns for the partner's end-of-frame tests
         {
             const float* pb = reinterpret_cast<const float*>(s.cols);
-            for (int i = tid; i < 2 * kN; i += 256) {
-                const int e = i >> 10, r = i & (kN - 1);
-                __stcg(my_edges + ((size_t)u * 2 + e) * kN + r, pb[(e ? 7 : 0) * (2 * kVS) + r]);
+#pragma unroll
+            for (int i = tid; i < 2 * kN / 4; i += 256) {  // 16-B vectors (column bases are 16-B aligned)
+                const int e = i >> 8, r4 = (i & 255) * 4;
+                const float4 v4 = *reinterpret_cast<const float4*>(pb + (e ? 7 : 0) * (2 * kVS) + r4);
+                __stcg(reinterpret_cast<float4*>(my_edges + ((size_t)u * 2 + e) * kN + r4), v4);
             }
         }
         __syncthreads();
