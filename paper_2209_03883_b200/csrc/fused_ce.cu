@@ -221,9 +221,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             const int k = idx >> 2, c = (idx & 3) * 2;
             const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
             const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
-            zero_cell |= (n0 == 0.f) | (n1 == 0.f);
-            const float i0 = n0 == 0.f ? 0.f : rcp_approx(n0);
-            const float i1 = n1 == 0.f ? 0.f : rcp_approx(n1);
+            // a zero (or flushed-denormal) |x|^2 gives rcp = +inf, caught once per tile below
+            const float i0 = rcp_approx(n0);
+            const float i1 = rcp_approx(n1);
             inv_tile += i0 + i1;
             const int pk = k + (k >> 5);
             const float2 r0 = make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
@@ -233,6 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             // refill the slot (its values were consumed above) with the stage kRing ahead
             a_issue();
         }
+        zero_cell |= isinf(inv_tile);  // estimation.cpp:17 zero-cell check (frame flagged, status bit 0)
         inv_acc += (double)inv_tile;  // fp32 within a tile (32 terms), fp64 across tiles
         __syncthreads();
         PH(0);
