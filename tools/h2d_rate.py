@@ -1,0 +1,16 @@
+"""Raw pinned host -> device copy bandwidth (the ceiling of the e2e path)."""
+import torch
+
+n = 1 << 30
+h = torch.empty(n, dtype=torch.uint8).pin_memory()
+d = torch.empty(n, dtype=torch.uint8, device="cuda")
+for _ in range(3):
+    d.copy_(h, non_blocking=True)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    d.copy_(h, non_blocking=True)
+e1.record()
+torch.cuda.synchronize()
+print(f"pinned H2D: {10 * n / e0.elapsed_time(e1) / 1e6:.1f} GB/s")
