@@ -289,8 +289,15 @@ cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_
     auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
+#if PG_SW
+        // software frame-group barriers: every CTA must be co-resident (cooperative launch)
+        PgArgs aa = a;
+        void* args[] = {&aa};
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(grid), dim3(256), args, smem, st);
+#else
         kern<<<grid, 256, smem, st>>>(a);
         return cudaGetLastError();
+#endif
     };
     return hamming ? go(fused_pg1024_kernel<true>) : go(fused_pg1024_kernel<false>);
 }

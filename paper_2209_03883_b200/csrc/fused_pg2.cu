@@ -417,8 +417,12 @@ cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scr
     auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        kern<<<groups * kGrp, kThreads, smem, st>>>(a, hmap, gmap);
-        return cudaGetLastError();
+        // cooperative launch: the frame groups spin on each other's counters, so every CTA of
+        // the persistent grid must be co-resident (guaranteed, or the launch fails loudly)
+        Pg2Args aa = a;
+        void* args[] = {&aa, &hmap, &gmap};
+        return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(groups * kGrp), dim3(kThreads),
+                                           args, smem, st);
     };
     return hamming ? go(fused_pg2_kernel<true>) : go(fused_pg2_kernel<false>);
 }
