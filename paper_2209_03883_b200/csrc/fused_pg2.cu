@@ -52,29 +52,43 @@ constexpr int kN = 1024, kM = 256;
 #define PG2_GRP 8
 #endif
 constexpr int kGrp = PG2_GRP;   // CTAs per frame group
-constexpr int kTpf = 32 / kGrp;  // column tiles (8 symbols each) per CTA per frame
+#ifndef PG2_TC
+#define PG2_TC 8  // symbols per column tile = column warps per CTA (8: 64-B swizzle, 4: 32-B swizzle)
+#endif
+#ifndef PG2_RW
+#define PG2_RW 8  // row warps per CTA; a TMA round is 2 x PG2_RW storage rows
+#endif
+#ifndef PG2_CPS
+#define PG2_CPS 1  // resident CTAs per SM
+#endif
+#ifndef PG2_HBUF
+#define PG2_HBUF 1  // H tile buffers (2: the tile two ahead is in flight while one is consumed)
+#endif
+constexpr int kTC = PG2_TC;
+constexpr int kHBuf = PG2_HBUF;
+constexpr int kTpf = 256 / (kTC * kGrp);  // column tiles per CTA per frame
 constexpr int kRowsPerCta = kN / kGrp;
 constexpr int kVS = 1058;       // padded column-FFT scratch stride (float2)
-constexpr int kColWarps = 8, kRowWarps = 8;
+constexpr int kColWarps = kTC, kRowWarps = PG2_RW;
 constexpr int kThreads = 32 * (kColWarps + kRowWarps);
 constexpr int kCntStride = 32;  // ints between counters (own 128-B line)
 #ifndef PG2_GBUF
 #define PG2_GBUF 2
 #endif
 constexpr int kGBuf = PG2_GBUF;  // G buffers per group (frames in flight between the passes)
-constexpr int kRoundRows = 16;  // G rows per TMA round
+constexpr int kRoundRows = 2 * kRowWarps;  // G storage rows per TMA round (16 or 8)
 constexpr int kRounds = kN / kGrp / kRoundRows;         // rounds per frame per CTA (4)
-constexpr unsigned kTileBytes = 8u * kN * 8u;           // 64 KiB
+constexpr unsigned kTileBytes = kTC * kN * 8u;         // 64 / 32 KiB
 constexpr unsigned kRoundBytes = kRoundRows * kM * 8u;  // 32 KiB
 
 struct __align__(1024) Pg2Smem {
-    float2 htile[kN * 8];                 // [k][8 symbols], 64-B swizzle   (1024-B aligned)
-    float2 gbuf[2][kM * kRoundRows];      // [l][16 rows], 128-B swizzle    (1024-B aligned)
+    float2 htile[kHBuf][kN * kTC];        // [k][kTC symbols], 64/32-B swizzle   (1024-B aligned)
+    float2 gbuf[2][kM * kRoundRows];      // [l][round rows], 128/64-B swizzle   (1024-B aligned)
     float2 cs[kColWarps][kVS];            // column-FFT transpose slots
     float2 tw[1024];                      // tw[t1*32 + j] = W_1024^{j t1}
     float wk[1024];
     float wl[256];
-    unsigned long long mbar_h;
+    unsigned long long mbar_h[kHBuf];
     unsigned long long mbar_g[2];
 };
 
@@ -142,7 +156,7 @@ __device__ unsigned long long g_pg2_phase[8];
 #endif
 
 template <bool HAMMING>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, PG2_CPS)
     fused_pg2_kernel(Pg2Args a, const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap gmap) {
     extern __shared__ unsigned char smem_raw[];
     Pg2Smem& s = *reinterpret_cast<Pg2Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -156,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (HAMMING && tid < 256) s.wl[tid] = a.wl[tid];
     if (tid == 0) {
-        mbar_init(&s.mbar_h, 1);
+        for (int b = 0; b < kHBuf; ++b) mbar_init(&s.mbar_h[b], 1);
         mbar_init(&s.mbar_g[0], 1);
         mbar_init(&s.mbar_g[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -181,30 +195,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------ column warps
         const int cw = ridx;
         const bool cw0 = cw == 0 && lane == 0;
-        const int ntiles = kTpf * nfr;  // tile t: frame g + (t / kTpf) ng, symbols 8 kGrp (t % kTpf) + 8 rank ..
-        if (cw0 && ntiles > 0) {
-            mbar_expect_tx(&s.mbar_h, kTileBytes);
-            tma_load_3d(s.htile, &hmap, 8 * rank, 0, 4 * g, &s.mbar_h, policy_evict_first());
-        }
+        const int ntiles = kTpf * nfr;  // tile t: frame g + (t / kTpf) ng, symbols kTC (kGrp (t % kTpf) + rank) ..
+        auto issue_tile = [&](int tn) {
+            const int b = tn % kHBuf;
+            mbar_expect_tx(&s.mbar_h[b], kTileBytes);
+            tma_load_3d(s.htile[b], &hmap, kTC * (kGrp * (tn % kTpf) + rank), 0, 4 * (g + (tn / kTpf) * ng), &s.mbar_h[b],
+                        policy_evict_first());
+        };
+        if (cw0)
+            for (int tn = 0; tn < kHBuf && tn < ntiles; ++tn) issue_tile(tn);
         // swizzled (k = lane + 32 r, symbol `warp`): float2 8k + 2((warp/2) ^ ((k/2)&3)) + (warp&1)
-        const int hoff = 8 * lane + 2 * ((cw >> 1) ^ ((lane >> 1) & 3)) + (cw & 1);
+        // kTC = 4 (32-B rows, SW32): 4k + 2((cw/2) ^ ((k/4)&1)) + (cw&1)
+        const int hoff = kTC == 8 ? 8 * lane + 2 * ((cw >> 1) ^ ((lane >> 1) & 3)) + (cw & 1)
+                                  : 4 * lane + 2 * ((cw >> 1) ^ ((lane >> 2) & 1)) + (cw & 1);
         float2* col = s.cs[cw];
         for (int t = 0; t < ntiles; ++t) {
             const int i = t / kTpf, u = t % kTpf;
-            const int c = 8 * kGrp * u + 8 * rank + cw;
-            mbar_wait(&s.mbar_h, t & 1);
+            const int c = kTC * (kGrp * u + rank) + cw;
+            mbar_wait(&s.mbar_h[t % kHBuf], (t / kHBuf) & 1);
             P2(0);
             float2 v[32];
 #pragma unroll
-            for (int r = 0; r < 32; ++r) v[r] = s.htile[hoff + 256 * r];
+            for (int r = 0; r < 32; ++r) v[r] = s.htile[t % kHBuf][hoff + 32 * kTC * r];
             bar_col();  // every column is in registers: the tile buffer is free
             if (cw0) {
-                if (t + 1 < ntiles) {
-                    const int tn = t + 1;
-                    mbar_expect_tx(&s.mbar_h, kTileBytes);
-                    tma_load_3d(s.htile, &hmap, 8 * kGrp * (tn % kTpf) + 8 * rank, 0, 4 * (g + (tn / kTpf) * ng), &s.mbar_h,
-                                policy_evict_first());
-                }
+                if (t + kHBuf < ntiles) issue_tile(t + kHBuf);  // into the buffer just read
                 if (t >= kTpf && u == 0) {
                     __threadfence();
                     atomicAdd(col_cnt + ((i - 1) % kGBuf) * kCntStride, 1);  // G of frame i - 1 complete
@@ -278,7 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t1 = 0; t1 < 16; ++t1) twr[t1] = a.tw256_t[t1 * 16 + j];
         // swizzled (l = j + 16 r, row 2 wr + h): float2 16 l + 2 (wr ^ (l & 7)) + h
-        const int goff = 16 * j + 2 * (wr ^ (j & 7)) + h;
+        // kRoundRows = 8 (64-B rows, SW64): 8 l + 2 (wr ^ ((l/2)&3)) + h
+        const int goff = kRoundRows == 16 ? 16 * j + 2 * (wr ^ (j & 7)) + h : 8 * j + 2 * (wr ^ ((j >> 1) & 3)) + h;
         if (producer && nrounds > 0) try_issue(true);
         for (int R = 0; R < nrounds; ++R) {
             const int i = R / kRounds, q = R % kRounds;
@@ -286,11 +302,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             P2(5);
             mbar_wait(&s.mbar_g[R & 1], (R >> 1) & 1);
 #ifndef PG2_NO_DISCARD
-            if (wr == 0) {
-                // the box's 256 lines of G (one 128-B line per symbol) are dead now: drop them from L2
-                // without write-back (G otherwise costs a DRAM write of 2 MiB per frame on eviction)
+            if (wr == 0 && (kRoundRows == 16 || (q & 1))) {
+                // the 256 lines of G (one 128-B line = 16 storage rows per symbol) read so far are dead:
+                // drop them from L2 without write-back (G otherwise costs a DRAM write on eviction);
+                // with 8-row rounds a line is complete after every second round
                 const float2* gl = a.gscratch + (size_t)(kGBuf * g + i % kGBuf) * kM * kN + kRowsPerCta * rank +
-                                   kRoundRows * q;
+                                   16 * (kRoundRows * q / 16);
 #pragma unroll
                 for (int k = 0; k < kM / 32; ++k)
                     asm volatile("discard.global.L2 [%0], 128;" ::"l"(gl + (size_t)(lane + 32 * k) * kN) : "memory");
@@ -303,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float2* gb = s.gbuf[R & 1];
             float2 v[16];
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = gb[goff + 256 * r];
+            for (int r = 0; r < 16; ++r) v[r] = gb[goff + 16 * kRoundRows * r];
             bar_row();  // the round buffer is now transpose scratch
             // half-warp FFT_256 of row 2 wr + h; 16 x 16 transpose in its own 2 KiB slot, XOR layout
             float2* sl = gb + (2 * wr + h) * 256;
@@ -395,10 +412,11 @@ cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scr
     {
         const cuuint64_t dims[3] = {256, 256, 4ull * (cuuint64_t)a.frames};
         const cuuint64_t strides[2] = {256 * 8, 256 * 256 * 8};
-        const cuuint32_t box[3] = {8, 256, 4};
+        const cuuint32_t box[3] = {(cuuint32_t)kTC, 256, 4};
         const cuuint32_t es[3] = {1, 1, 1};
         if (enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float2*>(a.h), dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, kTC == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
@@ -409,7 +427,8 @@ cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scr
         const cuuint32_t box[2] = {kRoundRows, 256};
         const cuuint32_t es[2] = {1, 1};
         if (enc(&gmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a.gscratch, dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, kRoundRows == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
