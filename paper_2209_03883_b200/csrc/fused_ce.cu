@@ -486,7 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         // per-CTA top-K of the frame's candidates (> kTileList / kFusedPend candidates in one
         // half-frame sets status bit 1 so the host recomputes the frame on the general path)
         if (tid == 0 && (s.tcnt > kTileList || s.pcnt > kFusedPend)) s.overflow = 1;
-        block_topk<256>(tl, min(s.tcnt, kTileList), K, s.run, s.sbest, s.sidx);
+        block_topk_reg<256, kTileList / 256>(tl, min(s.tcnt, kTileList), K, s.run, s.sbest);
         __syncthreads();
         cluster.sync();  // both per-CTA lists final
         if (rank == 0) {

@@ -120,6 +120,49 @@ __device__ __forceinline__ void block_topk(unsigned long long* list, int cnt, in
     }
 }
 
+// Same selection with the list read ONCE into registers (PER entries per thread, cnt <= PER *
+// NT): keys are unique (cell index in the low word), so the round's winner is retired by value
+// without tracking its position; two barriers per round and no re-reads of the list.
+template <int NT, int PER>
+__device__ __forceinline__ void block_topk_reg(const unsigned long long* list, int cnt, int K, unsigned long long* out,
+                                               unsigned long long* s_best) {
+    // `out` is in shared memory: the round's winner is broadcast through out[round]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long v[PER];
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+        const int i = threadIdx.x + p * NT;
+        v[p] = i < cnt ? list[i] : 0ull;
+    }
+    for (int round = 0; round < K; ++round) {
+        unsigned long long best = 0;
+#pragma unroll
+        for (int p = 0; p < PER; ++p) best = v[p] > best ? v[p] : best;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+            best = ob > best ? ob : best;
+        }
+        if (lane == 0) s_best[w] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long b = 0;
+            for (int i = 0; i < NT / 32; ++i) b = s_best[i] > b ? s_best[i] : b;
+            out[round] = b;
+        }
+        __syncthreads();
+        const unsigned long long b = out[round];
+        if (b == 0) {
+            for (int r = round + 1 + threadIdx.x; r < K; r += NT) out[r] = 0;
+            break;
+        }
+#pragma unroll
+        for (int p = 0; p < PER; ++p)
+            if (v[p] == b) v[p] = 0ull;
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void block_topk_smem(unsigned long long* list, int cnt, int K, unsigned long long* out,
                                                 unsigned long long* s_best, int* s_idx) {
     block_topk<256>(list, cnt, K, out, s_best, s_idx);
