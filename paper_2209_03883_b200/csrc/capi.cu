@@ -1119,8 +1119,8 @@ int ofdmr_pipeline(ofdmr_context* c, const void* y, const void* x, const double*
         fa.pend = c->fpend;
         fa.pend_loc = c->fpend_loc;
         fa.tlist = c->ftlist;
-        for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
-            const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);
+        for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 28) {
+            const int64_t nf = std::min<int64_t>((int64_t)1 << 28, frames - f0);
             fa.frames = int(nf);
             fa.y = static_cast<const float2*>(y) + fc * f0;
             fa.x = static_cast<const float2*>(x) + fc * f0;
