@@ -53,7 +53,7 @@ constexpr int kN = 1024, kM = 256;
 #endif
 constexpr int kGrp = PG2_GRP;   // CTAs per frame group
 #ifndef PG2_TC
-#define PG2_TC 8  // symbols per column tile = column warps per CTA (8: 64-B swizzle, 4: 32-B swizzle)
+#define PG2_TC 4  // symbols per column tile = column warps per CTA (8: 64-B swizzle, 4: 32-B swizzle)
 #endif
 #ifndef PG2_RW
 #define PG2_RW 8  // row warps per CTA; a TMA round is 2 x PG2_RW storage rows
@@ -76,7 +76,12 @@ constexpr int kCntStride = 32;  // ints between counters (own 128-B line)
 #define PG2_GBUF 2
 #endif
 constexpr int kGBuf = PG2_GBUF;  // G buffers per group (frames in flight between the passes)
-constexpr int kRoundRows = 2 * kRowWarps;  // G storage rows per TMA round (16 or 8)
+#ifndef PG2_RPG
+#define PG2_RPG 2  // rows per 16-lane group per round (2: a round is two 16-row halves, 3-D TMA box)
+#endif
+constexpr int kHalves = PG2_RPG;
+static_assert(kHalves == 1 || kRowWarps == 8, "two rows per group needs 8 row warps");
+constexpr int kRoundRows = 2 * kRowWarps * kHalves;  // G storage rows per TMA round (8, 16 or 32)
 constexpr int kRounds = kN / kGrp / kRoundRows;         // rounds per frame per CTA (4)
 constexpr unsigned kTileBytes = kTC * kN * 8u;         // 64 / 32 KiB
 constexpr unsigned kRoundBytes = kRoundRows * kM * 8u;  // 32 KiB
@@ -86,8 +91,6 @@ struct __align__(1024) Pg2Smem {
     float2 gbuf[2][kM * kRoundRows];      // [l][round rows], 128/64-B swizzle   (1024-B aligned)
     float2 cs[kColWarps][kVS];            // column-FFT transpose slots
     float2 tw[1024];                      // tw[t1*32 + j] = W_1024^{j t1}
-    float wk[1024];
-    float wl[256];
     unsigned long long mbar_h[kHBuf];
     unsigned long long mbar_g[2];
 };
@@ -166,9 +169,7 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
     const int g = blockIdx.x / kGrp, rank = blockIdx.x % kGrp, ng = gridDim.x / kGrp;
     for (int i = tid; i < 1024; i += kThreads) {
         s.tw[i] = a.tw1024_t[i];
-        if (HAMMING) s.wk[i] = a.wk[i];
     }
-    if (HAMMING && tid < 256) s.wl[tid] = a.wl[tid];
     if (tid == 0) {
         for (int b = 0; b < kHBuf; ++b) mbar_init(&s.mbar_h[b], 1);
         mbar_init(&s.mbar_g[0], 1);
@@ -209,6 +210,9 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
         const int hoff = kTC == 8 ? 8 * lane + 2 * ((cw >> 1) ^ ((lane >> 1) & 3)) + (cw & 1)
                                   : 4 * lane + 2 * ((cw >> 1) ^ ((lane >> 2) & 1)) + (cw & 1);
         float2* col = s.cs[cw];
+        float wkr[HAMMING ? 32 : 1];  // w_k[lane + 32 r]
+#pragma unroll
+        for (int r = 0; r < (HAMMING ? 32 : 1); ++r) wkr[r] = HAMMING ? a.wk[lane + 32 * r] : 1.f;
         for (int t = 0; t < ntiles; ++t) {
             const int i = t / kTpf, u = t % kTpf;
             const int c = kTC * (kGrp * u + rank) + cw;
@@ -225,10 +229,9 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
                     atomicAdd(col_cnt + ((i - 1) % kGBuf) * kCntStride, 1);  // G of frame i - 1 complete
                 }
             }
-            if (HAMMING) {
-                const float wl = s.wl[c];
+            if (HAMMING) {  // w_k here (register copy), w_l on the row side
 #pragma unroll
-                for (int r = 0; r < 32; ++r) v[r] = cscale(v[r], s.wk[lane + 32 * r] * wl);
+                for (int r = 0; r < 32; ++r) v[r] = cscale(v[r], wkr[r]);
             }
             warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: G[t1 + 32 t2] in v[t2]
             P2(1);
@@ -285,16 +288,23 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic transposes -> TMA overwrite
             mbar_expect_tx(&s.mbar_g[R & 1], kRoundBytes);
-            tma_load_2d(s.gbuf[R & 1], &gmap, kRowsPerCta * rank + kRoundRows * q, (kGBuf * g + i % kGBuf) * kM, &s.mbar_g[R & 1],
-                        policy_evict_first());
+            if (kHalves == 2)
+                tma_load_3d(s.gbuf[R & 1], &gmap, 0, (kGBuf * g + i % kGBuf) * kM, (kRowsPerCta * rank + kRoundRows * q) / 16,
+                            &s.mbar_g[R & 1], policy_evict_first());
+            else
+                tma_load_2d(s.gbuf[R & 1], &gmap, kRowsPerCta * rank + kRoundRows * q, (kGBuf * g + i % kGBuf) * kM,
+                            &s.mbar_g[R & 1], policy_evict_first());
             ++issued;
         };
         float2 twr[16];
 #pragma unroll
         for (int t1 = 0; t1 < 16; ++t1) twr[t1] = a.tw256_t[t1 * 16 + j];
+        float wlr[HAMMING ? 16 : 1];  // w_l[j + 16 r]: the symbol window, applied to the rows' inputs
+#pragma unroll
+        for (int r = 0; r < (HAMMING ? 16 : 1); ++r) wlr[r] = HAMMING ? a.wl[j + 16 * r] : 1.f;
         // swizzled (l = j + 16 r, row 2 wr + h): float2 16 l + 2 (wr ^ (l & 7)) + h
         // kRoundRows = 8 (64-B rows, SW64): 8 l + 2 (wr ^ ((l/2)&3)) + h
-        const int goff = kRoundRows == 16 ? 16 * j + 2 * (wr ^ (j & 7)) + h : 8 * j + 2 * (wr ^ ((j >> 1) & 3)) + h;
+        const int goff = kRoundRows >= 16 ? 16 * j + 2 * (wr ^ (j & 7)) + h : 8 * j + 2 * (wr ^ ((j >> 1) & 3)) + h;
         if (producer && nrounds > 0) try_issue(true);
         for (int R = 0; R < nrounds; ++R) {
             const int i = R / kRounds, q = R % kRounds;
@@ -302,15 +312,18 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
             P2(5);
             mbar_wait(&s.mbar_g[R & 1], (R >> 1) & 1);
 #ifndef PG2_NO_DISCARD
-            if (wr == 0 && (kRoundRows == 16 || (q & 1))) {
+            if (wr == 0 && (kRoundRows >= 16 || (q & 1))) {
                 // the 256 lines of G (one 128-B line = 16 storage rows per symbol) read so far are dead:
                 // drop them from L2 without write-back (G otherwise costs a DRAM write on eviction);
                 // with 8-row rounds a line is complete after every second round
                 const float2* gl = a.gscratch + (size_t)(kGBuf * g + i % kGBuf) * kM * kN + kRowsPerCta * rank +
                                    16 * (kRoundRows * q / 16);
 #pragma unroll
-                for (int k = 0; k < kM / 32; ++k)
-                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(gl + (size_t)(lane + 32 * k) * kN) : "memory");
+                for (int hh = 0; hh < kHalves; ++hh)
+#pragma unroll
+                    for (int k = 0; k < kM / 32; ++k)
+                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(gl + 16 * hh + (size_t)(lane + 32 * k) * kN)
+                                     : "memory");
             }
 #endif
             if (producer && q == kRounds - 1) {
@@ -318,27 +331,45 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
                 atomicAdd(row_cnt + (i % kGBuf) * kCntStride, 1);  // every G box of frame i landed: buffer reusable
             }
             float2* gb = s.gbuf[R & 1];
-            float2 v[16];
+            constexpr int kHalfElems = kHalves == 2 ? 16 * kM : 0;  // [half][l][16 rows] with 2 halves
+            constexpr int kLStride = kHalves == 2 ? 16 : kRoundRows;
+            float2 v[kHalves][16];
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = gb[goff + 16 * kRoundRows * r];
+            for (int hh = 0; hh < kHalves; ++hh)
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    v[hh][r] = gb[hh * kHalfElems + goff + 16 * kLStride * r];
+                    if (HAMMING) v[hh][r] = cscale(v[hh][r], wlr[r]);
+                }
             bar_row();  // the round buffer is now transpose scratch
-            // half-warp FFT_256 of row 2 wr + h; 16 x 16 transpose in its own 2 KiB slot, XOR layout
-            float2* sl = gb + (2 * wr + h) * 256;
-            dft16<false>(v);
+            // 16-lane FFT_256 of each of the group's rows; 16 x 16 transposes in own 2 KiB slots, XOR layout
 #pragma unroll
-            for (int t1 = 1; t1 < 16; ++t1) v[t1] = cmul(v[t1], twr[t1]);
+            for (int hh = 0; hh < kHalves; ++hh) {
+                dft16<false>(v[hh]);
 #pragma unroll
-            for (int t1 = 0; t1 < 16; ++t1) sl[t1 * 16 + (j ^ t1 ^ hx)] = v[t1];
+                for (int t1 = 1; t1 < 16; ++t1) v[hh][t1] = cmul(v[hh][t1], twr[t1]);
+                float2* sl = gb + (hh * 16 + 2 * wr + h) * 256;
+#pragma unroll
+                for (int t1 = 0; t1 < 16; ++t1) sl[t1 * 16 + (j ^ t1 ^ hx)] = v[hh][t1];
+            }
             __syncwarp();
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) v[jj] = sl[j * 16 + (jj ^ j ^ hx)];
-            dft16<false>(v);
-            // storage position -> delay row n (see the column store): pos = 64 b + 2 t1 + p, n = t1 + 32 (2b + p)
-            const int pos = kRowsPerCta * rank + kRoundRows * q + 2 * wr + h;
-            const int n = ((pos & 63) >> 1) + 64 * (pos >> 6) + 32 * (pos & 1);
-            float* prow = a.p + ((size_t)(g + i * ng) * kN + n) * kM;
+            for (int hh = 0; hh < kHalves; ++hh) {
+                float2* sl = gb + (hh * 16 + 2 * wr + h) * 256;
 #pragma unroll
-            for (int t2 = 0; t2 < 16; ++t2) __stcs(prow + ((j + 16 * t2 + 128) & 255), cnorm(v[t2]) * a.scale);
+                for (int jj = 0; jj < 16; ++jj) v[hh][jj] = sl[j * 16 + (jj ^ j ^ hx)];
+                dft16<false>(v[hh]);
+            }
+#pragma unroll
+            for (int hh = 0; hh < kHalves; ++hh) {
+                // storage position -> delay row n (see the column store): pos = 64 b + 2 t1 + p, n = t1 + 32 (2b + p)
+                const int pos = kRowsPerCta * rank + kRoundRows * q + 16 * hh + 2 * wr + h;
+                const int n = ((pos & 63) >> 1) + 64 * (pos >> 6) + 32 * (pos & 1);
+                float* prow = a.p + ((size_t)(g + i * ng) * kN + n) * kM;
+#pragma unroll
+                for (int t2 = 0; t2 < 16; ++t2)
+                    __stcs(prow + ((j + 16 * t2 + 128) & 255), cnorm(v[hh][t2]) * a.scale);
+            }
             P2(6);
             bar_row();  // transposes done: the buffer may be refilled
             if (producer && issued == R + 1 && R + 1 < nrounds) try_issue(true);
@@ -420,8 +451,18 @@ cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scr
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    // G scratch: per group 2 x [256 l][1024 n] c64 (column-major); box = 16 rows x 256 symbols, 128-B swizzle
-    {
+    // G scratch: per group kGBuf x [256 l][1024 n] c64 (column-major); box = round rows x 256 symbols
+    // (two rows per group: 3-D view (16 rows, l, 16-row block) with a [2][256][16] box)
+    if (kHalves == 2) {
+        const cuuint64_t dims[3] = {16, 256ull * kGBuf * (cuuint64_t)scratch_groups, 1024 / 16};
+        const cuuint64_t strides[2] = {1024 * 8, 16 * 8};
+        const cuuint32_t box[3] = {16, 256, 2};
+        const cuuint32_t es[3] = {1, 1, 1};
+        if (enc(&gmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.gscratch, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    } else {
         const cuuint64_t dims[2] = {1024, 256ull * kGBuf * (cuuint64_t)scratch_groups};
         const cuuint64_t strides[1] = {1024 * 8};
         const cuuint32_t box[2] = {kRoundRows, 256};
