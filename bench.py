@@ -475,11 +475,26 @@ def main():
         ptraffic = load_traffic("fused_pg2", pf)
         periodogram = {"frames": pf, "frames_per_s": pf / (pms / 1e3), "ms_per_step": pms,
                        "kernel": "fused_pg2 (persistent, warp-specialised: column and row warps concurrent, "
-                                 "H tiles and G row blocks by TMA, 8-CTA frame groups, double-buffered G in L2)",
+                                 "H tiles and G row blocks by TMA (3-D 32-row rounds), 8-CTA frame groups, double-buffered G in L2)",
                        "algorithmic_bytes_per_frame": pbytes, "achieved_gbs": pach, "frac": pach / hbm,
                        "traffic": ptraffic["bytes_per_launch"] if ptraffic else None,
                        "traffic_source": ptraffic["source"] if ptraffic else None,
-                       "stage_ms": {"fused_pg": pst[0]}}
+                       "stage_ms": {"fused_pg": pst[0]}, "window": "rectangular (cfg0's window)"}
+        # the same with the Hamming window of cfg1/2/4 (w_k, w_l applied inside the kernel)
+        perh = Receiver(cfg.n, cfg.m, cfg.n, cfg.m, window="hamming", device=local)
+        perh._stream()
+        for _ in range(3):
+            perh._lib.ofdmr_periodogram(perh._h, h.data_ptr(), pm.data_ptr(), pf)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            perh._lib.ofdmr_periodogram(perh._h, h.data_ptr(), pm.data_ptr(), pf)
+        e1.record()
+        torch.cuda.synchronize()
+        hms = e0.elapsed_time(e1) / args.steps
+        periodogram["hamming"] = {"frames_per_s": pf / (hms / 1e3), "ms_per_step": hms,
+                                  "frac": pf * pbytes / (hms / 1e3) / 1e9 / hbm}
+        perh.close()
         del pm
         per.close()
 
