@@ -18,7 +18,7 @@ cudaError_t launch_colpass(const ColArgs& a, int n, int np, int frames, cudaStre
 cudaError_t launch_rowpass(const RowArgs& a, int mp, int frames, cudaStream_t st);
 cudaError_t launch_merge(const MergeArgs& a, int frames, cudaStream_t st);
 int colpass_tile_cols(int np);
-int rowpass_rows(int mp, int np);
+int rowpass_rows(int mp, int np, int m);
 size_t rowpass_smem(int mp, int rows);
 struct FastRowArgs {
     RowArgs r;
@@ -528,7 +528,7 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
     c->g_rows = c->shortcut ? cfg->n_cp : np;
     if (c->shortcut && c->g_rows == 0) c->g_rows = 1;  // L = 0: all-zero estimate, keep one zero row
     c->ntiles = m / colpass_tile_cols(np);
-    c->rows_per_block = rowpass_rows(mp, np);
+    c->rows_per_block = rowpass_rows(mp, np, m);
     c->nblk = (np + c->rows_per_block - 1) / c->rows_per_block;
     c->log_pfa = std::log(cfg->pfa);
     c->pf = power_factor_d(cfg->window, n, m);
@@ -946,7 +946,7 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
         r.n_prime = g.n_prime;
         r.g_rows = g.n_prime;
         r.m = g.n_symbols;
-        r.rows_per_block = rowpass_rows(g.m_prime, g.n_prime);
+        r.rows_per_block = rowpass_rows(g.m_prime, g.n_prime, g.n_symbols);
         r.kmax = g.max_targets;
         r.detect = 0;
         cudaError_t e;

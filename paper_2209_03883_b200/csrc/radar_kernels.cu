@@ -373,7 +373,13 @@ cudaError_t launch_colpass(const ColArgs& a, int n, int np, int frames, cudaStre
 
 template <int MP> constexpr int row_chunk() { return MP >= 4096 ? 1 : MP >= 2048 ? 2 : MP >= 1024 ? 4 : 8; }
 
-int rowpass_rows(int mp, int np) {
+bool rowpass_zp_applies(const RowArgs& a, int mp);
+int rowpass_zp_rows();
+cudaError_t launch_rowpass_zp(const RowArgs& a, int frames, cudaStream_t st);
+
+int rowpass_rows(int mp, int np, int m) {
+    // M = 512 -> M' = 2048 (cfg2): rows per block of the zero-padded row pass (rowpass_zp.cu)
+    if (mp == 2048 && m == 512 && np >= rowpass_zp_rows()) return rowpass_zp_rows();
     int r = mp >= 4096 ? 4 : mp >= 2048 ? 6 : mp >= 1024 ? 14 : 30;  // R + 2 a multiple of the chunk
     if (r > np) r = np;
     return r;
@@ -400,6 +406,7 @@ cudaError_t launch_rowpass_t(const RowArgs& a, int frames, cudaStream_t st) {
 }
 
 cudaError_t launch_rowpass(const RowArgs& a, int mp, int frames, cudaStream_t st) {
+    if (rowpass_zp_applies(a, mp)) return launch_rowpass_zp(a, frames, st);
     switch (mp) {
         case 16: return launch_rowpass_t<16>(a, frames, st);
         case 32: return launch_rowpass_t<32>(a, frames, st);

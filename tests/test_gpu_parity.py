@@ -565,3 +565,18 @@ def test_sft_estimate_noise_from_slice(cuda, n, m):
     for f in range(F):
         ref = O.estimate_noise_from_slice(h[f].astype(np.complex128), int(seeds[f]))
         assert got[f] == ref, (f, got[f], ref)
+
+
+def test_rowpass_zp_matches_generic_rowpass(cuda):
+    # cfg2's zero-padded row pass (rowpass_zp.cu: 4 x FFT_512 per row, K <= 8) against the generic
+    # shared-memory row pass (taken for K > 8) on the same 12 ZC-precoded frames
+    cfg = configs.CFG2
+    fb = gen.frames(cfg, 0, 12)
+    with Receiver.from_config(cfg) as rx:
+        d8, _ = rx.pipeline(fb.y, fb.x, fb.sigma2)
+    with Receiver.from_config(cfg.replace(max_targets=9)) as rx:
+        d9, _ = rx.pipeline(fb.y, fb.x, fb.sigma2)
+    for f in range(12):
+        a, b = d8.frame(f), d9.frame(f)[:8]
+        assert [(x, y) for x, y, _ in a] == [(x, y) for x, y, _ in b]
+        assert all(abs(p - q) <= 1e-4 * q for (_, _, p), (_, _, q) in zip(a, b))
