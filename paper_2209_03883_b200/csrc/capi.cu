@@ -94,6 +94,7 @@ struct ofdmr_context {
     cudaStream_t stream = nullptr;
     int device = 0;
     float2* tw = nullptr;        // 4096-entry e^{-j2pi t/4096}
+    float2* zp_tw = nullptr;     // rowpass_zp twiddles (entries of tw): [4][32][16] W_2048^{j(4k1+m1)}, [128] W_128^q
     float* wk = nullptr;         // Hamming windows (fp32) or null for rectangular
     float* wk_s = nullptr;       // w_k * sqrt(1 / (N M)) for the fused kernel
     float* wl = nullptr;
@@ -359,6 +360,7 @@ int run_pipeline_chunk(ofdmr_context* c, int si, const float2* y, const float2* 
     r.inv_count = c->inv_count;
     r.scale = c->scale;
     r.tw = c->tw;
+    r.zp_tw = c->zp_tw;
     r.n_prime = g.n_prime;
     r.g_rows = c->g_rows;
     r.m = g.n_symbols;
@@ -558,6 +560,16 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
     }
     cudaError_t e = cudaMalloc(&c->tw, sizeof(float2) * kTwLenHost);
     if (e == cudaSuccess) e = cudaMemcpy(c->tw, tw.data(), sizeof(float2) * kTwLenHost, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        std::vector<float2> zt(4 * 512 + 128);
+        for (int i = 0; i < 4 * 512; ++i) {
+            const int m1 = i >> 9, k1 = (i >> 4) & 31, j = i & 15;
+            zt[i] = tw[(2 * j * (4 * k1 + m1)) & (kTwLenHost - 1)];
+        }
+        for (int q = 0; q < 128; ++q) zt[4 * 512 + q] = tw[32 * q];
+        e = cudaMalloc(&c->zp_tw, sizeof(float2) * zt.size());
+        if (e == cudaSuccess) e = cudaMemcpy(c->zp_tw, zt.data(), sizeof(float2) * zt.size(), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess && cfg->window == OFDMR_WINDOW_HAMMING) {
         std::vector<double> wk(n), wl(m);
         make_window_d(cfg->window, n, m, wk.data(), wl.data());
@@ -646,6 +658,7 @@ void ofdmr_destroy(ofdmr_context* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaFree(c->tw);
+    cudaFree(c->zp_tw);
     cudaFree(c->wk);
     cudaFree(c->wk_s);
     cudaFree(c->wl);
@@ -943,6 +956,7 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
         r.p_out = p + pframe * f0;
         r.scale = c->scale;
         r.tw = c->tw;
+        r.zp_tw = c->zp_tw;
         r.n_prime = g.n_prime;
         r.g_rows = g.n_prime;
         r.m = g.n_symbols;
@@ -981,6 +995,7 @@ static int detect_impl(ofdmr_context* c, const float* p, const double* sigma2_h,
         r.log_pfa = c->log_pfa;
         r.power_factor = c->pf;
         r.tw = c->tw;
+        r.zp_tw = c->zp_tw;
         r.n_prime = g.n_prime;
         r.g_rows = g.n_prime;
         r.m = g.n_symbols;

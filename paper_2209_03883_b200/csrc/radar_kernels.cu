@@ -44,16 +44,6 @@ __device__ double block_sum_d(double v, double* scratch) {
     return s;
 }
 
-// sigma_h^2 exactly as pipeline.cpp:18-23 composes it, partials summed in fixed order.
-__device__ __forceinline__ double sigma_h2(const double* inv_partial, int ntiles, int f, double sigma2,
-                                           double inv_count) {
-    if (inv_partial == nullptr) return sigma2;  // caller passed sigma_h^2 directly
-    if (sigma2 <= 0.0) return 0.0;
-    double acc = 0.0;
-    for (int t = 0; t < ntiles; ++t) acc += inv_partial[(size_t)f * ntiles + t];
-    return sigma2 * acc * inv_count;
-}
-
 // ---------------------------------------------------------------- colpass --
 
 template <int N, int NP, int C>
@@ -257,7 +247,7 @@ __global__ void __launch_bounds__(kNT) rowpass_kernel(RowArgs a) {
     if (a.eta_in != nullptr) {
         eta = a.eta_in[f];
     } else {
-        const double s2h = sigma_h2(a.inv_partial, a.ntiles, f, a.sigma2[f], a.inv_count);
+        const double s2h = sigma_h2_warp(a.inv_partial, a.ntiles, f, a.sigma2[f], a.inv_count);
         eta = -s2h * a.log_pfa * a.power_factor;  // periodogram.cpp:80
     }
     if (threadIdx.x == 0) s_cnt = 0;
@@ -300,6 +290,9 @@ __global__ void __launch_bounds__(kNT) merge_kernel(MergeArgs a) {
     const int kf = a.k_per_frame ? min(a.k_per_frame[f], a.kmax) : a.kmax;
     block_topk<kNT>(list, total, kf, s_top, s_best, s_idx);
     __syncthreads();
+    const double s2h = (a.s2h_out != nullptr || a.eta_out != nullptr)
+                           ? sigma_h2_warp(a.inv_partial, a.ntiles, f, a.sigma2[f], a.inv_count)
+                           : 0.0;
     if (threadIdx.x == 0) {
         int n = 0;
         for (int i = 0; i < a.kmax; ++i) {
@@ -319,7 +312,6 @@ __global__ void __launch_bounds__(kNT) merge_kernel(MergeArgs a) {
         }
         a.counts[f] = n;
         if (a.s2h_out != nullptr || a.eta_out != nullptr) {
-            const double s2h = sigma_h2(a.inv_partial, a.ntiles, f, a.sigma2[f], a.inv_count);
             if (a.s2h_out) a.s2h_out[f] = s2h;
             if (a.eta_out) a.eta_out[f] = -s2h * a.log_pfa * a.power_factor;
         }

@@ -53,6 +53,7 @@ struct RowArgs {
     int kmax;               // candidates kept per block
     unsigned long long* cand;  // [frame][nblk][kmax] packed keys
     int detect;             // 0 = map only
+    const float2* zp_tw;    // rowpass_zp twiddles: W_2048^{j (4 k1 + m1)} [4][32][16], then W_128^q [128]
 };
 
 struct MergeArgs {
@@ -72,6 +73,21 @@ struct MergeArgs {
     double* s2h_out;        // optional per-frame sigma_h^2
     double* eta_out;        // optional per-frame threshold
 };
+
+// sigma_h^2 (pipeline.cpp:18-23: sigma^2 * mean(1/|x|^2)) from the per-(frame, tile) partial
+// sums: lane i adds tiles i, i + 32, .. in order, then a fixed xor-shuffle tree (every lane ends
+// with the same value).  Call with all 32 lanes of a warp; every kernel that thresholds or
+// reports sigma_h^2 from the partials uses this one order.
+__device__ __forceinline__ double sigma_h2_warp(const double* inv_partial, int ntiles, int f, double sigma2,
+                                                double inv_count) {
+    if (inv_partial == nullptr) return sigma2;  // caller passed sigma_h^2 directly
+    if (sigma2 <= 0.0) return 0.0;
+    double acc = 0.0;
+    for (int t = threadIdx.x & 31; t < ntiles; t += 32) acc += inv_partial[(size_t)f * ntiles + t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return sigma2 * acc * inv_count;
+}
 
 // Packed detection key: larger key = larger power, ties -> smaller row-major index
 // (extract_peaks ordering, periodogram.cpp:98-102).  P >= 0 so the float bit pattern

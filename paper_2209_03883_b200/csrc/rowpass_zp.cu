@@ -21,6 +21,8 @@
 #include "radar_kernels.cuh"
 #include "warp_fft.cuh"
 
+#include <math.h>
+
 namespace ofdmr {
 
 namespace {
@@ -36,17 +38,14 @@ struct ZpSmem {
     unsigned long long best[kZW];
     int idx[kZW];
     unsigned long long top[kMaxK];
+    float eta_f;  // smallest float >= eta: (double)v >= eta  <=>  v >= eta_f (exact)
 };
 static_assert(2 * kZW * 32 * 16 * sizeof(float2) >= kZThreads * kZK * sizeof(unsigned long long), "key list");
 
-__device__ __forceinline__ double zp_sigma_h2(const double* inv_partial, int ntiles, int f, double sigma2,
-                                              double inv_count) {
-    if (inv_partial == nullptr) return sigma2;
-    if (sigma2 <= 0.0) return 0.0;
-    double acc = 0.0;
-    for (int t = 0; t < ntiles; ++t) acc += inv_partial[(size_t)f * ntiles + t];
-    return sigma2 * acc * inv_count;
-}
+// P tile column swizzle: flips bit 1 when bit 5 is set, so the 32 lanes of one |.|^2 store
+// (m = m1 + 4 j + .., m1 in {a, a + 1}) hit 32 distinct banks; an aligned float4 of the tile
+// holds logical columns c0 + (u ^ 2 * bit5(c0))
+__device__ __forceinline__ int zp_phys(int m) { return m ^ (((m >> 5) & 1) << 1); }
 
 }  // namespace
 
@@ -58,11 +57,25 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
     const int f = blockIdx.y, rb = blockIdx.x, np = a.n_prime, r0 = rb * kZR;
     const int nrows = min(kZR, np - r0), TR = nrows + 2;
 
-    for (int i = tid; i < 4 * 512; i += kZThreads) {
-        const int m1 = i >> 9, k1 = (i >> 4) & 31, jj = i & 15;
-        s.post[m1][k1 * 16 + jj] = a.tw[(2 * jj * (4 * k1 + m1)) & (kTwLen - 1)];
+    // twiddle tables (host-built, zp_tw layout: post[4][512] then pre[128])
+    {
+        const float4* src = reinterpret_cast<const float4*>(a.zp_tw);
+        float4* dst = reinterpret_cast<float4*>(&s.post[0][0]);
+        for (int i = tid; i < (4 * 512 + 128) / 2; i += kZThreads) dst[i] = __ldg(src + i);
     }
-    for (int i = tid; i < 128; i += kZThreads) s.pre[i] = a.tw[32 * i];
+    if (warp == 0 && a.detect) {
+        // threshold once per CTA (sigma_h^2 in the order the merge kernel reports it)
+        double eta;
+        if (a.eta_in != nullptr) {
+            eta = a.eta_in[f];
+        } else {
+            const double s2h = sigma_h2_warp(a.inv_partial, a.ntiles, f, a.sigma2[f], a.inv_count);
+            eta = -s2h * a.log_pfa * a.power_factor;  // periodogram.cpp:80
+        }
+        float e = (float)eta;
+        if ((double)e < eta) e = nextafterf(e, INFINITY);
+        if (lane == 0) s.eta_f = e;
+    }
     __syncthreads();
 
     // ---- 1. P tile: rows (r0 - 1 + t) mod N', t < TR
@@ -104,7 +117,7 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
                 // X[m1 + 4 (k1 + 32 k2)], fft-shifted by M'/2
                 const int base = m1 + 4 * k1 + kZMP / 2;
 #pragma unroll
-                for (int k2 = 0; k2 < 16; ++k2) prow[(base + 128 * k2) & (kZMP - 1)] = cnorm(w[k2]) * a.scale;
+                for (int k2 = 0; k2 < 16; ++k2) prow[zp_phys((base + 128 * k2) & (kZMP - 1))] = cnorm(w[k2]) * a.scale;
             }
             __syncwarp();  // the slot is rewritten by the next pass
         }
@@ -116,40 +129,43 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
         float* po = a.p_out + (size_t)f * np * kZMP + (size_t)r0 * kZMP;
         for (int i = tid; i < nrows * (kZMP / 4); i += kZThreads) {
             const int r = i / (kZMP / 4), q = i % (kZMP / 4);
-            __stcs(reinterpret_cast<float4*>(po + (size_t)r * kZMP) + q,
-                   reinterpret_cast<const float4*>(s.ptile + (r + 1) * kZMP)[q]);
+            float4 v = reinterpret_cast<const float4*>(s.ptile + (r + 1) * kZMP)[q];
+            if ((q >> 3) & 1) v = make_float4(v.z, v.w, v.x, v.y);  // undo zp_phys
+            __stcs(reinterpret_cast<float4*>(po + (size_t)r * kZMP) + q, v);
         }
     }
     if (!a.detect) return;
 
     // ---- 3. threshold + strict wrapped 3x3 local maxima, per-thread top-8 (periodogram.cpp:77-136)
-    double eta;
-    if (a.eta_in != nullptr) {
-        eta = a.eta_in[f];
-    } else {
-        const double s2h = zp_sigma_h2(a.inv_partial, a.ntiles, f, a.sigma2[f], a.inv_count);
-        eta = -s2h * a.log_pfa * a.power_factor;  // periodogram.cpp:80
-    }
+    const float eta_f = s.eta_f;
     unsigned long long top[kZK];
 #pragma unroll
     for (int i = 0; i < kZK; ++i) top[i] = 0ull;
-    for (int i = tid; i < nrows * kZMP; i += kZThreads) {
-        const int tr = i / kZMP + 1, c = i % kZMP;
+    for (int i = tid; i < nrows * (kZMP / 4); i += kZThreads) {
+        const int tr = i / (kZMP / 4) + 1, c0 = 4 * (i % (kZMP / 4));
         const float* mid = s.ptile + tr * kZMP;
-        const float v = mid[c];
-        if (!((double)v >= eta)) continue;
-        const int cl = (c - 1) & (kZMP - 1), cr = (c + 1) & (kZMP - 1);
-        const float* up = mid - kZMP;
-        const float* dn = mid + kZMP;
-        if (up[cl] >= v || up[c] >= v || up[cr] >= v || mid[cl] >= v || mid[cr] >= v || dn[cl] >= v ||
-            dn[c] >= v || dn[cr] >= v)
-            continue;
-        unsigned long long key = make_key(v, (uint32_t)((r0 + tr - 1) * kZMP + c));
+        const float4 q4 = *reinterpret_cast<const float4*>(mid + c0);
+        if (!(q4.x >= eta_f || q4.y >= eta_f || q4.z >= eta_f || q4.w >= eta_f)) continue;
+        const float qv[4] = {q4.x, q4.y, q4.z, q4.w};
+        const int sw = ((c0 >> 5) & 1) << 1;
 #pragma unroll
-        for (int q = 0; q < kZK; ++q) {  // sorted insert (descending), keys unique
-            const unsigned long long t = top[q];
-            top[q] = key > t ? key : t;
-            key = key > t ? t : key;
+        for (int u = 0; u < 4; ++u) {
+            const float v = qv[u];
+            if (!(v >= eta_f)) continue;
+            const int c = c0 + (u ^ sw);  // logical column; physical c0 + u
+            const int pc = c0 + u, pl = zp_phys((c - 1) & (kZMP - 1)), pr = zp_phys((c + 1) & (kZMP - 1));
+            const float* up = mid - kZMP;
+            const float* dn = mid + kZMP;
+            if (up[pl] >= v || up[pc] >= v || up[pr] >= v || mid[pl] >= v || mid[pr] >= v || dn[pl] >= v ||
+                dn[pc] >= v || dn[pr] >= v)
+                continue;
+            unsigned long long key = make_key(v, (uint32_t)((r0 + tr - 1) * kZMP + c));
+#pragma unroll
+            for (int q = 0; q < kZK; ++q) {  // sorted insert (descending), keys unique
+                const unsigned long long t = top[q];
+                top[q] = key > t ? key : t;
+                key = key > t ? t : key;
+            }
         }
     }
     unsigned long long* list = reinterpret_cast<unsigned long long*>(&s.sc[0][0]);  // slots are free
