@@ -14,6 +14,7 @@
 #include <cstring>
 #include <numeric>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "sft_kernels.cuh"
@@ -638,21 +639,32 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
     const int i_max = cfg.i_max;
     // host-side data-independent draws (sft.cpp:191, 212-218)
     std::vector<int32_t> draws(size_t(frames) * size_t(i_max > 0 ? i_max : 1) * 4);
-    for (int64_t f = 0; f < frames; ++f) {
-        std::mt19937_64 e(derive_seed(seeds[f], 0x73667421));
-        for (int it = 0; it < i_max; ++it) {
-            long long v1, v2;
-            do {
-                v1 = (long long)(1 + uniform_int(e, n > 1 ? n - 1 : 1));
-                v2 = (long long)(1 + uniform_int(e, m > 1 ? m - 1 : 1));
-            } while (!slope_admissible(v1, v2, n, m));
-            const long long a1 = (long long)uniform_int(e, n), a2 = (long long)uniform_int(e, m);
-            int32_t* d = &draws[(size_t(f) * i_max + it) * 4];
-            d[0] = int32_t(v1);
-            d[1] = int32_t(v2);
-            d[2] = int32_t(a1);
-            d[3] = int32_t(a2);
+    auto draw_frames = [&](int64_t f0, int64_t f1) {
+        for (int64_t f = f0; f < f1; ++f) {
+            std::mt19937_64 e(derive_seed(seeds[f], 0x73667421));
+            for (int it = 0; it < i_max; ++it) {
+                long long v1, v2;
+                do {
+                    v1 = (long long)(1 + uniform_int(e, n > 1 ? n - 1 : 1));
+                    v2 = (long long)(1 + uniform_int(e, m > 1 ? m - 1 : 1));
+                } while (!slope_admissible(v1, v2, n, m));
+                const long long a1 = (long long)uniform_int(e, n), a2 = (long long)uniform_int(e, m);
+                int32_t* d = &draws[(size_t(f) * i_max + it) * 4];
+                d[0] = int32_t(v1);
+                d[1] = int32_t(v2);
+                d[2] = int32_t(a1);
+                d[3] = int32_t(a2);
+            }
         }
+    };
+    // one engine per frame (seeding + first twist dominate): frames split over host threads,
+    // every frame's draws are independent of the split
+    {
+        const int64_t nt = std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), frames / 64 + 1);
+        std::vector<std::thread> pool;
+        for (int64_t t = 1; t < nt; ++t) pool.emplace_back(draw_frames, frames * t / nt, frames * (t + 1) / nt);
+        draw_frames(0, frames / nt);
+        for (auto& th : pool) th.join();
     }
     // twiddle tables: reference rotation table (sft.cpp:29-44) and radix-2 table (oracle.c)
     std::vector<double2> twr(q), twf(q / 2);
