@@ -547,7 +547,9 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
     if (chunk <= 0) {
         // two chunks in flight; keep both intermediates L2-resident (126 MB L2)
         chunk = int64_t((32ull << 20) / gframe);
-        if (chunk < 1) chunk = 1;
+        // frames whose intermediate alone is >= 8 MiB (cfg2: 16 MiB) are compute-bound, not L2-bound:
+        // fill the GPU instead (8 frames per launch: whole waves, one merge launch per 8 frames)
+        if (chunk < 8) chunk = 8;
         if (chunk > 256) chunk = 256;
     }
     if (c->fused && cfg->chunk_frames <= 0) chunk = 512;  // host-buffer path: fill every cluster

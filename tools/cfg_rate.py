@@ -20,7 +20,7 @@ y = torch.from_numpy(fb.y).cuda().repeat(rep, 1, 1)[:frames].contiguous()
 x = torch.from_numpy(fb.x).cuda().repeat(rep, 1, 1)[:frames].contiguous()
 s2 = torch.from_numpy(np.tile(fb.sigma2, rep)[:frames]).cuda()
 kf = torch.from_numpy(np.tile(fb.n_targets, rep)[:frames].astype(np.int32)).cuda() if cfg.per_frame_k else None
-rx = Receiver.from_config(cfg)
+rx = Receiver.from_config(cfg, chunk_frames=int(os.environ.get("CHUNK", "0")))
 dets = rx._dets(frames)
 rx._stream()
 rx.pipeline_raw(y, x, s2, kf, dets, frames)
