@@ -326,9 +326,13 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
                                      : "memory");
             }
 #endif
-            if (producer && q == kRounds - 1) {
+            if (wr == 0 && q == kRounds - 1) {
+                // every G box of frame i landed: the buffer is reusable.  Every lane fences first, so
+                // all of this warp's discards of frame i's lines are ordered before the release (a late
+                // discard would otherwise drop a line of frame i + kGBuf already written into it)
                 __threadfence();
-                atomicAdd(row_cnt + (i % kGBuf) * kCntStride, 1);  // every G box of frame i landed: buffer reusable
+                __syncwarp();
+                if (lane == 0) atomicAdd(row_cnt + (i % kGBuf) * kCntStride, 1);
             }
             float2* gb = s.gbuf[R & 1];
             constexpr int kHalfElems = kHalves == 2 ? 16 * kM : 0;  // [half][l][16 rows] with 2 halves
