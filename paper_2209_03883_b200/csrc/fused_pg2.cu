@@ -210,9 +210,18 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
         const int hoff = kTC == 8 ? 8 * lane + 2 * ((cw >> 1) ^ ((lane >> 1) & 3)) + (cw & 1)
                                   : 4 * lane + 2 * ((cw >> 1) ^ ((lane >> 2) & 1)) + (cw & 1);
         float2* col = s.cs[cw];
-        float wkr[HAMMING ? 32 : 1];  // w_k[lane + 32 r]
+        // registers of the column warps: w_k[lane + 32 r] with the Hamming window; without it the
+        // inverse transform's twiddles conj W_1024^{lane t1} instead (31 fewer shared-memory loads
+        // per column: +4 %; holding both costs more than it saves, measured)
+        constexpr bool kTwReg = !HAMMING;
+        float wkr[HAMMING ? 32 : 1];
+        float2 twc[kTwReg ? 32 : 1];
 #pragma unroll
         for (int r = 0; r < (HAMMING ? 32 : 1); ++r) wkr[r] = HAMMING ? a.wk[lane + 32 * r] : 1.f;
+        if constexpr (kTwReg) {
+#pragma unroll
+            for (int t1 = 0; t1 < 32; ++t1) twc[t1] = make_float2(s.tw[t1 * 32 + lane].x, -s.tw[t1 * 32 + lane].y);
+        }
         for (int t = 0; t < ntiles; ++t) {
             const int i = t / kTpf, u = t % kTpf;
             const int c = kTC * (kGrp * u + rank) + cw;
@@ -229,11 +238,24 @@ __global__ void __launch_bounds__(kThreads, PG2_CPS)
                     atomicAdd(col_cnt + ((i - 1) % kGBuf) * kCntStride, 1);  // G of frame i - 1 complete
                 }
             }
-            if (HAMMING) {  // w_k here (register copy), w_l on the row side
+            if constexpr (kTwReg) {  // warp_fft1024 with the twiddles from registers
+                dft32<true>(v);
 #pragma unroll
-                for (int r = 0; r < 32; ++r) v[r] = cscale(v[r], wkr[r]);
+                for (int t1 = 1; t1 < 32; ++t1) v[t1] = cmul(v[t1], twc[t1]);
+                __syncwarp();
+#pragma unroll
+                for (int t1 = 0; t1 < 32; ++t1) col[t1 * 33 + lane] = v[t1];
+                __syncwarp();
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) v[jj] = col[lane * 33 + jj];
+                dft32<true>(v);  // lane t1: G[t1 + 32 t2] in v[t2]
+            } else {
+                if (HAMMING) {  // w_k here (register copy), w_l on the row side
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) v[r] = cscale(v[r], wkr[r]);
+                }
+                warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: G[t1 + 32 t2] in v[t2]
             }
-            warp_fft1024<true, 32>(v, col, s.tw);  // lane t1: G[t1 + 32 t2] in v[t2]
             P2(1);
 #ifdef PG2_COL_ONLY
             if (false) {
