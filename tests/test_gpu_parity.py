@@ -580,3 +580,21 @@ def test_rowpass_zp_matches_generic_rowpass(cuda):
         a, b = d8.frame(f), d9.frame(f)[:8]
         assert [(x, y) for x, y, _ in a] == [(x, y) for x, y, _ in b]
         assert all(abs(p - q) <= 1e-4 * q for (_, _, p), (_, _, q) in zip(a, b))
+
+
+@pytest.mark.parametrize("window", [0, 1])
+def test_fused_periodogram_many_frames_on_device(cuda, window, monkeypatch):
+    """1000 frames (~55 per 8-CTA frame group: each double-buffered G buffer reused ~27 times,
+    the discard -> release ordering exercised on every frame) against the previous kernel,
+    compared on the device."""
+    import torch
+    n, m, F = 1024, 256, 1000
+    g = torch.Generator(device="cuda").manual_seed(11 + window)
+    h = torch.randn(F, n, m, dtype=torch.complex64, device="cuda", generator=g)
+    h *= torch.linspace(0.5, 2.0, F, device="cuda")[:, None, None]
+    with Receiver(n, m, window=window) as rx:
+        p = rx.periodogram(h)
+        monkeypatch.setenv("OFDMR_PG_V1", "1")
+        q = rx.periodogram(h)
+    err = ((p - q).abs().amax(dim=(1, 2)) / q.amax(dim=(1, 2))).max().item()
+    assert err <= MAP_TOL, err
