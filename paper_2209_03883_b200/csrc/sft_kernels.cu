@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
     int* alias = clist + q;                                   // [q]
     __shared__ int s_cand[kMaxCand];
     __shared__ double2 s_c1[kMaxCand], s_c2[kMaxCand];
+    __shared__ int s_dkl[kMaxCand];  // decoded (k << 12) | l per candidate, -1 = rejected
     __shared__ int s_ck[kMaxComp], s_cl[kMaxComp];
     __shared__ double2 s_camp[kMaxComp];
     __shared__ double s_red[kSftNT / 32];
@@ -387,10 +388,14 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
             }
         }
         __syncthreads();
-        // (11)-(18) sequential decode / gate / merge in candidate order
-        if (tid == 0) {
-            double total_power = s_total;
-            for (int i = 0; i < ncand; ++i) {
+        // (11)-(15) per candidate, in parallel: a candidate's subtraction, decode, gate and amplitude
+        // only involve components whose tone bin is its own bin (or its residue mod Q/g when it is
+        // not aliased), and no other candidate of this iteration adds, merges or erases one of
+        // those (distinct bins; an aliased residue forces full slices) -- so the order-dependent
+        // part is only (16)-(17), applied below by one thread in candidate order
+        for (int i = tid; i < ncand; i += kSftNT) {
+            s_dkl[i] = -1;
+            {
                 const int f = s_cand[i];
                 const double2 c0 = spec[f];
                 if (dnorm(c0) < threshold) continue;
@@ -420,7 +425,20 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
                 const double2 psi1 = dmul(psi0, polar1(kTwoPiD * (double)k / (double)n));
                 const double2 psi2 = dmul(psi0, polar1(kTwoPiD * (double)l / (double)m));
                 const double2 sum = dadd(dadd(ddiv(c0, psi0), ddiv(c1, psi1)), ddiv(c2, psi2));
-                const double2 amp = make_double2(sum.x / 3.0, sum.y / 3.0);
+                s_c1[i] = make_double2(sum.x / 3.0, sum.y / 3.0);  // amp
+                s_c2[i].x = dnorm(c0);
+                s_dkl[i] = (int)((k << 12) | l);
+            }
+        }
+        __syncthreads();
+        // (16)-(18) merge / erase / consume in candidate order
+        if (tid == 0) {
+            double total_power = s_total;
+            for (int i = 0; i < ncand; ++i) {
+                if (s_dkl[i] < 0) continue;
+                const int f = s_cand[i];
+                const long long k = s_dkl[i] >> 12, l = s_dkl[i] & 4095;
+                const double2 amp = s_c1[i];
                 int found = -1;
                 for (int j = 0; j < s_ncomp; ++j)
                     if (s_ck[j] == k && s_cl[j] == l) { found = j; break; }
@@ -442,7 +460,7 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
                 } else {
                     s_err = 1;
                 }
-                total_power -= dnorm(c0);
+                total_power -= s_c2[i].x;
                 spec[f] = make_double2(0.0, 0.0);
             }
             const double residual = total_power > 0.0 ? total_power : 0.0;
