@@ -155,10 +155,10 @@ __device__ void fft_r2(double2* a, int q, int logq, const double2* __restrict__ 
         }
     }
     __syncthreads();
-    for (int len = 2; len <= q; len <<= 1) {
-        const int half = len >> 1, step = q / len;
+    for (int ls = 1; ls <= logq; ++ls) {  // len = 2^ls (powers of two: shifts instead of divisions)
+        const int len = 1 << ls, half = len >> 1, step = q >> ls;
         for (int b = threadIdx.x; b < q / 2; b += kSftNT) {
-            const int grp = b / half, k = b - grp * half;
+            const int grp = b >> (ls - 1), k = b & (half - 1);
             const int i = grp * len + k;
             const double2 w = tw[k * step];
             const double2 u = a[i], v = a[i + half];
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
 
         // (2) reference slice s0[q] = H[(a1 + v1 q) mod N, (a2 + v2 q) mod M], FFT, 1/Q
         for (int t = tid; t < q; t += kSftNT) {
-            const int r = (int)((a1 + (long long)rs * t) % n), c = (int)((a2 + (long long)cs * t) % m);
+            const int r = (int)((a1 + (long long)rs * t) & (n - 1)), c = (int)((a2 + (long long)cs * t) & (m - 1));
             const float2 v = h[(size_t)r * m + c];
             spec[t] = make_double2((double)v.x, (double)v.y);
         }
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
         // (9) offset slices at (r+1, c) and (r, c+1)
         if (g == 1 || s_full) {
             for (int t = tid; t < q; t += kSftNT) {
-                const int r = (int)((a1 + (long long)rs * t) % n), c = (int)((a2 + (long long)cs * t) % m);
+                const int r = (int)((a1 + (long long)rs * t) & (n - 1)), c = (int)((a2 + (long long)cs * t) & (m - 1));
                 const int r1 = r + 1 == n ? 0 : r + 1, c1 = c + 1 == m ? 0 : c + 1;
                 const float2 u = h[(size_t)r1 * m + c], w = h[(size_t)r * m + c1];
                 sp1[t] = make_double2((double)u.x, (double)u.y);
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
         if (g > 1) {
             const int rsd = (int)((v1 * g) % n), csd = (int)((v2 * g) % m);
             for (int t = tid; t < qd; t += kSftNT) {
-                const int r = (int)((a1 + (long long)rsd * t) % n), c = (int)((a2 + (long long)csd * t) % m);
+                const int r = (int)((a1 + (long long)rsd * t) & (n - 1)), c = (int)((a2 + (long long)csd * t) & (m - 1));
                 const int r1 = r + 1 == n ? 0 : r + 1, c1 = c + 1 == m ? 0 : c + 1;
                 const float2 u = h[(size_t)r1 * m + c], w = h[(size_t)r * m + c1];
                 s1d[t] = make_double2((double)u.x, (double)u.y);
