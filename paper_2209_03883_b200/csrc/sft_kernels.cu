@@ -133,11 +133,38 @@ __device__ bool lattice_decode(double kap, double lam, int f, long long v1, long
         egcd(pmod(a / d, qd), qd, &inv, &tmp);
         inv = pmod(inv, qd);
         const long long l0 = pmod(((rhs / d) * inv) % qd, qd);
-        for (long long l = l0 % m; l < m; l += qd) {
-            if (l < 0) continue;
-            if (tone_bin(k, l, v1, v2, n, m, q) != f) continue;
-            const double dist = hypot(kd, wrap_dist(lam, l, m));
-            if (dist < best) { best = dist; *out_k = k; *out_l = l; found = true; }
+        const long long start = l0 % m, cnt = start < m ? (m - 1 - start) / qd + 1 : 0;
+        if (cnt <= 8) {
+            for (long long l = start; l < m; l += qd) {
+                if (l < 0) continue;
+                if (tone_bin(k, l, v1, v2, n, m, q) != f) continue;
+                const double dist = hypot(kd, wrap_dist(lam, l, m));
+                if (dist < best) { best = dist; *out_k = k; *out_l = l; found = true; }
+            }
+        } else {
+            // the reference scans all cnt solutions l = start + j qd in increasing order with a
+            // strict "<" (sft.cpp:141-155); wrap_dist only grows away from lam (circularly), so the
+            // minimum -- and every l tying with it -- lies among the progression elements that
+            // bracket lam and the two at each end (wrap-around): evaluate just those, in increasing
+            // l, with the same arithmetic (identical result, O(1) instead of O(cnt))
+            const long long jb = (long long)floor((lam - (double)start) / (double)qd);
+            long long js[8] = {jb - 1, jb, jb + 1, jb + 2, 0, 1, cnt - 2, cnt - 1};
+            for (int x = 1; x < 8; ++x)  // insertion sort (8 entries)
+                for (int y = x; y > 0 && js[y - 1] > js[y]; --y) {
+                    const long long t = js[y];
+                    js[y] = js[y - 1];
+                    js[y - 1] = t;
+                }
+            long long prev = -1;
+            for (int x = 0; x < 8; ++x) {
+                const long long jj = js[x];
+                if (jj < 0 || jj >= cnt || jj == prev) continue;
+                prev = jj;
+                const long long l = start + jj * qd;
+                if (tone_bin(k, l, v1, v2, n, m, q) != f) continue;
+                const double dist = hypot(kd, wrap_dist(lam, l, m));
+                if (dist < best) { best = dist; *out_k = k; *out_l = l; found = true; }
+            }
         }
     }
     return found;
