@@ -182,17 +182,43 @@ __device__ void fft_r2(double2* a, int q, int logq, const double2* __restrict__ 
         }
     }
     __syncthreads();
-    for (int ls = 1; ls <= logq; ++ls) {  // len = 2^ls (powers of two: shifts instead of divisions)
+    // stages ls and ls + 1 fused per thread: the 4 points {i, i + h, i + 2h, i + 3h} (h = 2^(ls-1))
+    // are closed under both stages' butterflies, which run in registers in the oracle's order with
+    // its twiddles (bit-identical), one barrier per pair of stages
+    auto bfly = [](double2& u, double2& v, const double2 w) {
+        const double vr = v.x * w.x - v.y * w.y;
+        const double vi = v.x * w.y + v.y * w.x;
+        v = make_double2(u.x - vr, u.y - vi);
+        u = make_double2(u.x + vr, u.y + vi);
+    };
+    int ls = 1;
+    for (; ls + 1 <= logq; ls += 2) {
+        const int half = 1 << (ls - 1), len = 2 * half;
+        for (int b = threadIdx.x; b < q / 4; b += kSftNT) {
+            const int grp = b >> (ls - 1), k = b & (half - 1);
+            const int i = grp * 2 * len + k;
+            double2 x0 = a[i], x1 = a[i + half], x2 = a[i + len], x3 = a[i + len + half];
+            const double2 w1 = tw[k * (q >> ls)];  // stage ls: pairs (i, i + h), (i + 2h, i + 3h)
+            bfly(x0, x1, w1);
+            bfly(x2, x3, w1);
+            bfly(x0, x2, tw[k * (q >> (ls + 1))]);  // stage ls + 1: pairs (i, i + 2h), (i + h, i + 3h)
+            bfly(x1, x3, tw[(k + half) * (q >> (ls + 1))]);
+            a[i] = x0;
+            a[i + half] = x1;
+            a[i + len] = x2;
+            a[i + len + half] = x3;
+        }
+        __syncthreads();
+    }
+    if (ls == logq) {  // odd log2(q): one radix-2 stage left
         const int len = 1 << ls, half = len >> 1, step = q >> ls;
         for (int b = threadIdx.x; b < q / 2; b += kSftNT) {
             const int grp = b >> (ls - 1), k = b & (half - 1);
             const int i = grp * len + k;
-            const double2 w = tw[k * step];
-            const double2 u = a[i], v = a[i + half];
-            const double vr = v.x * w.x - v.y * w.y;
-            const double vi = v.x * w.y + v.y * w.x;
-            a[i + half] = make_double2(u.x - vr, u.y - vi);
-            a[i] = make_double2(u.x + vr, u.y + vi);
+            double2 u = a[i], v = a[i + half];
+            bfly(u, v, tw[k * step]);
+            a[i] = u;
+            a[i + half] = v;
         }
         __syncthreads();
     }
