@@ -296,15 +296,17 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
         __syncthreads();
         fft_r2(spec, q, a.logq, a.tw_fft);
         for (int t = tid; t < q; t += kSftNT) spec[t] = make_double2(spec[t].x * inv_q, spec[t].y * inv_q);
+        // (3) accepted tones' bins and phasors in parallel (s_dkl / s_c1 are free here) ...
+        for (int i = tid; i < s_ncomp; i += kSftNT) {
+            s_dkl[i] = tone_bin(s_ck[i], s_cl[i], v1, v2, n, m, q);
+            const double th = kTwoPiD * ((double)(a1 * s_ck[i]) / (double)n + (double)(a2 * s_cl[i]) / (double)m);
+            s_c1[i] = dmul(s_camp[i], polar1(th));
+        }
         __syncthreads();
         if (tid == 0) {
             s_samples += q;
-            // (3) subtract accepted tones at their bins (sft.cpp:232-236), in list order
-            for (int i = 0; i < s_ncomp; ++i) {
-                const int f = tone_bin(s_ck[i], s_cl[i], v1, v2, n, m, q);
-                const double th = kTwoPiD * ((double)(a1 * s_ck[i]) / (double)n + (double)(a2 * s_cl[i]) / (double)m);
-                spec[f] = dsub(spec[f], dmul(s_camp[i], polar1(th)));
-            }
+            // ... subtracted from their bins in list order (sft.cpp:232-236)
+            for (int i = 0; i < s_ncomp; ++i) spec[s_dkl[i]] = dsub(spec[s_dkl[i]], s_c1[i]);
         }
         __syncthreads();
         // (4) threshold on the first iteration (sft.cpp:238-249)
