@@ -78,29 +78,33 @@ __device__ __forceinline__ long long pmod(long long a, long long m) {
 }
 
 __device__ __forceinline__ int tone_bin(long long k, long long l, long long v1, long long v2, int n, int m, int q) {
-    const unsigned long long qn = q / n, qm = q / m;
-    const unsigned long long f =
-        ((unsigned long long)v1 * (unsigned long long)k * qn + (unsigned long long)v2 * (unsigned long long)l * qm) %
-        (unsigned long long)q;
+    // (v1 k Q/N + v2 l Q/M) mod Q with N, M, Q powers of two (the GPU path's precondition):
+    // v1 k (Q/N) mod Q = (Q/N) ((v1 k) mod N), and k < N, v1 < N <= 2048 keep v1 k in 32 bits
+    const unsigned qn = (unsigned)(q / n), qm = (unsigned)(q / m);
+    const unsigned f = (qn * (((unsigned)v1 * (unsigned)k) & (unsigned)(n - 1)) +
+                        qm * (((unsigned)v2 * (unsigned)l) & (unsigned)(m - 1))) &
+                       (unsigned)(q - 1);
     return (int)f;
 }
 
 __device__ long long egcd(long long a, long long b, long long* x, long long* y) {
-    // iterative form of sft.cpp:85-96 (same Bezout coefficients)
-    long long x0 = 1, y0 = 0, x1 = 0, y1 = 1;
-    while (b != 0) {
-        const long long qt = a / b;
-        long long t = a - qt * b; a = b; b = t;
+    // iterative form of sft.cpp:85-96 (same Bezout coefficients); the operands here are < Q <= 2048,
+    // so the quotients and the coefficients (|x|, |y| <= Q) are exact in 32-bit arithmetic
+    int aa = (int)a, bb = (int)b, x0 = 1, y0 = 0, x1 = 0, y1 = 1;
+    while (bb != 0) {
+        const int qt = aa / bb;
+        int t = aa - qt * bb; aa = bb; bb = t;
         t = x0 - qt * x1; x0 = x1; x1 = t;
         t = y0 - qt * y1; y0 = y1; y1 = t;
     }
     *x = x0;
     *y = y0;
-    return a;
+    return aa;
 }
 
 __device__ double wrap_dist(double a, long long b, int period) {
-    double d = fmod(a - (double)b, (double)period);
+    double d = a - (double)b;
+    if (fabs(d) >= (double)period) d = fmod(d, (double)period);  // fmod is the identity below the period
     if (d > (double)period / 2) d -= (double)period;
     if (d < -(double)period / 2) d += (double)period;
     return fabs(d);
