@@ -14,6 +14,9 @@
 #include <cstring>
 #include <numeric>
 #include <random>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -680,6 +683,7 @@ int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int 
     s.cap_q = int(std::min<int64_t>(cap_q, s.cap_q ? s.cap_q : cap_q));
     e = cudaMemcpyAsync(s.draws, slopes.data(), sizeof(int32_t) * slopes.size(), cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(s.tw_fft, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice, st);
+    s.tw_q = 0;  // tw_fft rewritten here: sft_run rebuilds its tables on its next call
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host vectors go out of scope
     if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
     int logq = 0;
@@ -700,6 +704,74 @@ void sft_free(SftScratch& s) {
     cudaFree(s.err);
     s = SftScratch{};
 }
+
+namespace {
+
+// Persistent host worker pool for the per-frame draws: run(nt, fn) calls fn(t, nt) for t < nt,
+// t = 0 on the caller, and returns when all are done.  One run at a time (contexts on several host
+// threads queue); the pool lives for the process (never destroyed: no joins at exit).
+class HostPool {
+   public:
+    static HostPool& get() {
+        static HostPool* pool = new HostPool;
+        return *pool;
+    }
+    int size() const { return (int)workers_.size() + 1; }
+    void run(int nt, const std::function<void(int, int)>& fn) {
+        std::lock_guard<std::mutex> run_lock(run_mu_);
+        nt = std::max(1, std::min(nt, size()));
+        if (nt == 1) {
+            fn(0, 1);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            active_ = nt - 1;
+            pending_ = nt - 1;
+            nt_ = nt;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0, nt);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+
+   private:
+    HostPool() {
+        const int n = (int)std::max(1u, std::thread::hardware_concurrency()) - 1;
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
+        for (auto& w : workers_) w.detach();
+    }
+    void loop(int id) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(int, int)>* f;
+            int nt;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (id > active_) continue;
+                f = fn_;
+                nt = nt_;
+            }
+            (*f)(id, nt);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> workers_;
+    const std::function<void(int, int)>* fn_ = nullptr;
+    int active_ = 0, pending_ = 0, nt_ = 1;
+    uint64_t gen_ = 0;
+};
+
+}  // namespace
 
 int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const ofdmr_sft_config& cfg,
             const uint64_t* seeds, const double* sigma2, int32_t* k_out, int32_t* l_out, double* amp_out,
@@ -734,18 +806,32 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
             }
         }
     };
-    // one engine per frame (seeding + first twist dominate): frames split over host threads,
-    // every frame's draws are independent of the split
+    // one engine per frame (seeding + first twist dominate): frames split over a persistent pool of
+    // host threads (spawning threads per call cost more than the draws); every frame's draws are
+    // independent of the split
     {
-        const int64_t nt = std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()), frames / 64 + 1);
-        std::vector<std::thread> pool;
-        for (int64_t t = 1; t < nt; ++t) pool.emplace_back(draw_frames, frames * t / nt, frames * (t + 1) / nt);
-        draw_frames(0, frames / nt);
-        for (auto& th : pool) th.join();
+        const int nt = (int)std::min<int64_t>(HostPool::get().size(), frames / 64 + 1);
+        HostPool::get().run(nt, [&](int t, int nt_run) {
+            draw_frames(frames * t / nt_run, frames * (t + 1) / nt_run);
+        });
     }
-    // twiddle tables: reference rotation table (sft.cpp:29-44) and radix-2 table (oracle.c)
-    std::vector<double2> twr(q), twf(q / 2);
-    {
+    const double2* old_ref = s.tw_ref;
+    const double2* old_fft = s.tw_fft;
+    int64_t cap_s2 = s.cap_frames, cap_err = s.cap_frames, cap_q = s.cap_q, cap_q2 = s.cap_q;
+    cudaError_t e = ensure(&s.draws, s.cap_draws, int64_t(draws.size()));
+    if (e == cudaSuccess) e = ensure(&s.sigma2, cap_s2, frames);
+    if (e == cudaSuccess) e = ensure(&s.err, cap_err, frames);
+    if (e == cudaSuccess) e = ensure(&s.tw_ref, cap_q, q);
+    if (e == cudaSuccess) e = ensure(&s.tw_fft, cap_q2, q);
+    if (e != cudaSuccess) { err = std::string("sft: allocation: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    s.cap_frames = std::min(cap_s2, cap_err);
+    s.cap_q = int(std::min(cap_q, cap_q2));
+    e = cudaMemcpyAsync(s.draws, draws.data(), sizeof(int32_t) * draws.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(s.sigma2, sigma2, sizeof(double) * frames, cudaMemcpyHostToDevice, st);
+    // twiddle tables: reference rotation table (sft.cpp:29-44) and radix-2 table (oracle.c),
+    // built and uploaded only when Q changed or the buffers were reallocated
+    if (e == cudaSuccess && (s.tw_q != q || s.tw_ref != old_ref || s.tw_fft != old_fft)) {
+        std::vector<double2> twr(q), twf(q / 2);
         const double sa = -kTwoPiD / double(q);
         double cr = 1.0, ci = 0.0;
         const double sr = std::cos(sa), si = std::sin(sa);
@@ -764,20 +850,10 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
             const double ang = (double)(-1) * kTwoPiD * (double)k / (double)q;
             twf[k] = make_double2(std::cos(ang), std::sin(ang));
         }
+        e = cudaMemcpyAsync(s.tw_ref, twr.data(), sizeof(double2) * q, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(s.tw_fft, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice, st);
+        s.tw_q = e == cudaSuccess ? q : 0;
     }
-    int64_t cap_s2 = s.cap_frames, cap_err = s.cap_frames, cap_q = s.cap_q, cap_q2 = s.cap_q;
-    cudaError_t e = ensure(&s.draws, s.cap_draws, int64_t(draws.size()));
-    if (e == cudaSuccess) e = ensure(&s.sigma2, cap_s2, frames);
-    if (e == cudaSuccess) e = ensure(&s.err, cap_err, frames);
-    if (e == cudaSuccess) e = ensure(&s.tw_ref, cap_q, q);
-    if (e == cudaSuccess) e = ensure(&s.tw_fft, cap_q2, q);
-    if (e != cudaSuccess) { err = std::string("sft: allocation: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    s.cap_frames = std::min(cap_s2, cap_err);
-    s.cap_q = int(std::min(cap_q, cap_q2));
-    e = cudaMemcpyAsync(s.draws, draws.data(), sizeof(int32_t) * draws.size(), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(s.sigma2, sigma2, sizeof(double) * frames, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(s.tw_ref, twr.data(), sizeof(double2) * q, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(s.tw_fft, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) { err = std::string("sft: upload: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
 
     SftArgs a{};

@@ -21,6 +21,7 @@ struct SftScratch {
     int64_t cap_frames = 0;
     int64_t cap_draws = 0;
     int cap_q = 0;
+    int tw_q = 0;                  // Q whose twiddle tables tw_ref / tw_fft currently hold (0 = none)
 };
 
 void sft_free(SftScratch& s);
