@@ -152,6 +152,7 @@ struct GenArgs {
     //   mode 1: scene + pilots + payload -> fp64 x in xd (no channel),
     //   (precode_kernel: x_tx = Z x per column, fp64),
     //   mode 2: scene again (same streams), mean_power of the fp64 x_tx, channel + noise.
+    int fph_rows;           // target rows of the fph table in shared memory (max targets of the launch)
     int mode;               // 0: unprecoded single pass
     double2* xd;            // mode 1: fp64 x out; mode 2: fp64 x_tx in ([count][N][M])
 };
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
     const ofdmr_gen_params& p = a.p;
     const int n = p.n, m = p.m, tid = threadIdx.x, w = tid >> 5;
     double2* fph = reinterpret_cast<double2*>(gsm + ((sizeof(GenShared) + 15) & ~size_t(15)));
-    double* nrm = reinterpret_cast<double*>(fph + (size_t)kMaxT * m);
+    double* nrm = reinterpret_cast<double*>(fph + (size_t)a.fph_rows * m);
     uint64_t* ring = reinterpret_cast<uint64_t*>(nrm + 2 * m);
     unsigned char* pil = reinterpret_cast<unsigned char*>(ring + a.ring_mask + 1);
 
@@ -590,7 +591,11 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
     while (ring < need) ring <<= 1;
     if (ring < 512) ring = 512;
     a.ring_mask = ring - 1;
-    const size_t smem = ((sizeof(GenShared) + 15) & ~size_t(15)) + sizeof(double2) * kMaxT * p->m +
+    // fph holds one row per target of the launch (not kMaxT): 32 KiB less shared memory per CTA at
+    // cfg4's 8 targets, 4 instead of 2 resident CTAs per SM to overlap one CTA's MT19937 production
+    // with another's consumption
+    a.fph_rows = std::max(1, a.explicit_scene ? a.exp_count : p->targets_max);
+    const size_t smem = ((sizeof(GenShared) + 15) & ~size_t(15)) + sizeof(double2) * a.fph_rows * p->m +
                         sizeof(double) * 2 * p->m + sizeof(uint64_t) * ring + (size_t)p->n;
     cudaError_t e = cudaFuncSetAttribute(gen_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return 10;
