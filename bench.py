@@ -287,7 +287,7 @@ def extra_configs(args, dev, local, threads):
     mcfg = configs.CFG1
     rng_t, vel_t = np.array([8.0, 17.5, 31.0]), np.array([-35.0, 12.0, 60.0])
     grid = [-15.0, -5.0, 5.0]
-    mc.rmse_sweep(mcfg, rng_t, vel_t, grid[:1], 64, 1)  # warm-up
+    mc.rmse_sweep(mcfg, rng_t, vel_t, grid[:1], 2048, 1)  # warm-up: one full batch (buffers allocated and cached)
     trials = 4096
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -124,7 +124,7 @@ def rmse_sweep(cfg: RadarConfig, ranges, vels, snr_grid_db, trials: int, seed: i
     import torch
 
     from . import gen
-    from .receiver import Receiver
+    from .receiver import ConfigError, Receiver
 
     if trials < 1:
         raise ValueError("rmse_sweep: trials must be >= 1")
@@ -140,31 +140,74 @@ def rmse_sweep(cfg: RadarConfig, ranges, vels, snr_grid_db, trials: int, seed: i
     lib = _native.lib()
     rows = []
     B = min(batch, trials)
-    y = torch.empty(B, cfg.n, cfg.m, dtype=torch.complex64, device=dev)
-    x = torch.empty(B, cfg.n, cfg.m, dtype=torch.complex64, device=dev)
-    s2 = torch.empty(B, dtype=torch.float64, device=dev)
-    st = torch.empty(B, dtype=torch.int32, device=dev)
+    K = rcfg.max_targets
+    pin = dict(dtype=torch.int32, pin_memory=True)
     with Receiver.from_config(rcfg, device=dev.index) as rx:
+        # two batch slots: the GPU generates and receives batch j while the host matches batch j - 1
+        slots = []
+        for _ in range(2):
+            slots.append(dict(
+                y=torch.empty(B, cfg.n, cfg.m, dtype=torch.complex64, device=dev),
+                x=torch.empty(B, cfg.n, cfg.m, dtype=torch.complex64, device=dev),
+                s2=torch.empty(B, dtype=torch.float64, device=dev),
+                gst=torch.empty(B, dtype=torch.int32, device=dev),
+                pst=torch.empty(B, dtype=torch.int32, device=dev),
+                d=rx._dets(B),
+                h_delay=torch.empty(B, K, **pin), h_dopp=torch.empty(B, K, **pin), h_cnt=torch.empty(B, **pin),
+                h_gst=torch.empty(B, **pin), h_pst=torch.empty(B, **pin), ev=torch.cuda.Event()))
+
+        def enqueue(sl, snr, t0, nb):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = lib.ofdmr_gen_device_explicit(C.byref(p), seed, t0, nb, ranges.ctypes.data_as(_native.P_f64),
+                                               vels.ctypes.data_as(_native.P_f64), T, float(snr), sl["y"].data_ptr(),
+                                               sl["x"].data_ptr(), sl["s2"].data_ptr(), sl["gst"].data_ptr(), None,
+                                               C.c_void_p(stream))
+            if rc:
+                raise RuntimeError(f"ofdmr_gen_device_explicit failed ({rc})")
+            d = sl["d"]
+            rx._stream()
+            rc = rx._lib.ofdmr_pipeline(rx._h, sl["y"].data_ptr(), sl["x"].data_ptr(), sl["s2"].data_ptr(), None,
+                                        d.delay_bin.data_ptr(), d.doppler_bin.data_ptr(), d.peak_power.data_ptr(),
+                                        d.counts.data_ptr(), None, None, sl["pst"].data_ptr(), nb)
+            if rc:
+                raise RuntimeError(f"ofdmr_pipeline failed ({rc})")
+            for src, dst in ((d.delay_bin, "h_delay"), (d.doppler_bin, "h_dopp"), (d.counts, "h_cnt"),
+                             (sl["gst"], "h_gst"), (sl["pst"], "h_pst")):
+                sl[dst][:nb].copy_(src[:nb], non_blocking=True)
+            sl["ev"].record()
+
+        def finish(sl, nb, stats):
+            sl["ev"].synchronize()
+            if int(sl["h_gst"][:nb].sum()):
+                raise RuntimeError("generator rejection draw (regenerate on the CPU)")
+            pst = sl["h_pst"][:nb].numpy()
+            if (pst & 1).any():
+                raise ConfigError("spectral_division: zero cell in X")
+            dd, vv, cc = sl["h_delay"][:nb].numpy(), sl["h_dopp"][:nb].numpy(), sl["h_cnt"][:nb].numpy()
+            over = np.flatnonzero(pst & 2)
+            if over.size:  # fused-path candidate overflow: those frames exactly, as Receiver.pipeline does
+                dets, _ = rx.pipeline(sl["y"][torch.as_tensor(over, device=dev)],
+                                      sl["x"][torch.as_tensor(over, device=dev)],
+                                      sl["s2"][torch.as_tensor(over, device=dev)])
+                dd, vv, cc = dd.copy(), vv.copy(), cc.copy()
+                dd[over] = dets.delay_bin.cpu().numpy()
+                vv[over] = dets.doppler_bin.cpu().numpy()
+                cc[over] = dets.counts.cpu().numpy()
+            for i in range(nb):
+                phys = [bins_to_physics(int(dd[i, j]), int(vv[i, j]), cfg) for j in range(int(cc[i]))]
+                match_detections(phys, truths, res, stats)
+
         for snr in snr_grid_db:
             stats = MatchStats()
-            for t0 in range(0, trials, B):
+            pending = None
+            for bi, t0 in enumerate(range(0, trials, B)):
                 nb = min(B, trials - t0)
-                stream = torch.cuda.current_stream(dev).cuda_stream
-                rc = lib.ofdmr_gen_device_explicit(C.byref(p), seed, t0, nb, ranges.ctypes.data_as(_native.P_f64),
-                                                   vels.ctypes.data_as(_native.P_f64), T, float(snr), y.data_ptr(),
-                                                   x.data_ptr(), s2.data_ptr(), st.data_ptr(), None,
-                                                   C.c_void_p(stream))
-                if rc:
-                    raise RuntimeError(f"ofdmr_gen_device_explicit failed ({rc})")
-                if int(st[:nb].sum().item()):
-                    raise RuntimeError("generator rejection draw (regenerate on the CPU)")
-                dets, _ = rx.pipeline(y[:nb], x[:nb], s2[:nb])
-                d = dets.delay_bin.cpu().numpy()
-                v = dets.doppler_bin.cpu().numpy()
-                c = dets.counts.cpu().numpy()
-                for i in range(nb):
-                    phys = [bins_to_physics(int(d[i, j]), int(v[i, j]), cfg) for j in range(int(c[i]))]
-                    match_detections(phys, truths, res, stats)
+                sl = slots[bi % 2]
+                enqueue(sl, snr, t0, nb)
+                if pending is not None:
+                    finish(*pending, stats)
+                pending = (sl, nb)
+            finish(*pending, stats)
             rows.append(finish_row(float(snr), est_name, stats, trials))
     return rows
 

@@ -14,7 +14,7 @@ from paper_2209_03883_b200 import montecarlo as mc  # noqa: E402
 cfg = configs.CFG1
 rng_t, vel_t = np.array([8.0, 17.5, 31.0]), np.array([-35.0, 12.0, 60.0])
 grid = [-15.0, -5.0, 5.0]
-mc.rmse_sweep(cfg, rng_t, vel_t, grid[:1], 64, 1)
+mc.rmse_sweep(cfg, rng_t, vel_t, grid[:1], 2048, 1)
 acc = {"t": 0.0}
 orig_match, orig_phys = mc.match_detections, mc.bins_to_physics
 
