@@ -413,7 +413,10 @@ int run_persist(ofdmr_context* c, const float2* h, const float2* y, const float2
                 int32_t* status, int64_t frames) {
     const ofdmr_config& g = c->cfg;
     auto& ps = c->ps;
-    const int nchunks = int((frames + ps.cf - 1) / ps.cf);
+    // frames per chunk: a batch smaller than one chunk gets a chunk of its own size (no empty
+    // tickets for the CTAs to draw one by one; the ring slots are a subset of the allocated ones)
+    const int cf = int(std::min<int64_t>(ps.cf, frames));
+    const int nchunks = int((frames + cf - 1) / cf);
     const int64_t need = 1 + frames + nchunks;
     if (need > ps.cap) {
         cudaFree(ps.counters);
@@ -463,7 +466,7 @@ int run_persist(ofdmr_context* c, const float2* h, const float2* y, const float2
     r.s2h_out = s2h_out;
     pa.tw1024_t = c->tw1024_t;
     pa.frames = int(frames);
-    pa.cf = ps.cf;
+    pa.cf = cf;
     pa.ring = ps.ring;
     pa.nchunks = nchunks;
     pa.nblk = c->nblk;
