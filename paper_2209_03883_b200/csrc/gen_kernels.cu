@@ -44,6 +44,10 @@ constexpr uint64_t kMatA = 0xB5026F5AA96619E9ull;
 constexpr uint64_t kUpper = 0xFFFFFFFF80000000ull, kLower = 0x7FFFFFFFull;
 constexpr int kMaxT = 16;
 constexpr int kMaxM = 1024;
+// 8 consumer warps (one cell per thread and row) + warp 8, which draws row k + 1's MT19937-64
+// outputs while the consumers process row k (the draws' order and values are unchanged)
+constexpr int kGenThreads = 288;
+constexpr int kProducerWarp = 8;
 
 __device__ __forceinline__ uint64_t splitmix(uint64_t base, uint64_t stream) {
     // rng.hpp derive_seed (SplitMix64 of base ^ golden * (stream + 1))
@@ -163,14 +167,14 @@ struct GenShared {
     int rej;
     double snr_db;
     double b_re[kMaxT], b_im[kMaxT], delay[kMaxT], dopp[kMaxT];
-    double d_re[kMaxT], d_im[kMaxT];  // this row's delay phasors
+    double d_re2[2][kMaxT], d_im2[2][kMaxT];  // delay phasors of rows k (k & 1) and k + 1
     double mp;                        // running sequential sum of |x|^2
     double sd;
 };
 
 // dynamic smem after GenShared: fph[kMaxT][M] double2, nrm[2][M] double, pilot codes [N] bytes,
 // draw ring [ring] u64
-__global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
+__global__ void __launch_bounds__(kGenThreads) gen_frame_kernel(GenArgs a) {
     extern __shared__ __align__(16) unsigned char gsm[];
     GenShared& s = *reinterpret_cast<GenShared*>(gsm);
     const ofdmr_gen_params& p = a.p;
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
     const int T = s.ntar;
     const double t_useful = 1.0 / p.df_hz;
     const double ts = t_useful + (double)p.n_cp * (t_useful / (double)n);
-    for (int i = tid; i < T * m; i += 256) {
+    for (int i = tid; tid < 256 && i < T * m; i += 256) {
         const int t = i / m, l = i % m;
         double sn, cs;
         sincos(kTwoPiG * (double)l * ts * s.dopp[t], &sn, &cs);
@@ -273,41 +277,47 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
     // ---- pass 1: x_tx row by row; mean_power summed sequentially (warp 1, lane 0)
     const int bps = a.bps, half = bps / 2;
     const uint32_t need = (uint32_t)(m - 1) * bps;  // payload draws per row
-    uint32_t produced = 0, consumed = 0;             // warp 0 bookkeeping (uniform in the CTA)
-    for (int k = 0; k < n; ++k) {
-        if (w == 0) {
-            while (produced < consumed + need) {
-                mt_block(s.mt, ring, produced, mask);
-                produced += kMtN;
-            }
-        } else {
-            while (produced < consumed + need) produced += kMtN;  // keep the counters uniform
+    uint32_t produced = 0, consumed = 0;             // produced: producer warp only
+    if (w == kProducerWarp)
+        while (produced < need) {  // row 0
+            mt_block(s.mt, ring, produced, mask);
+            produced += kMtN;
         }
-        __syncthreads();
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
         double* nr = nrm + (k & 1) * m;
-        for (int l = tid; l < m; l += 256) {
-            double xr, xi;
-            if (l == 0) {
-                const unsigned b = pil[k];
-                xr = (b & 1) ? -a.inv_sqrt2 : a.inv_sqrt2;
-                xi = (b & 2) ? -a.inv_sqrt2 : a.inv_sqrt2;
-            } else {
-                unsigned wd = 0;
-                const uint32_t base = consumed + (uint32_t)(l - 1) * bps;
-                for (int b = 0; b < bps; ++b) {
-                    const uint64_t v = ring[(base + b) & mask];
-                    if (v >= 0xFFFFFFFFFFFFFFFEull) atomicOr(&s.rej, 1);
-                    wd = (wd << 1) | (unsigned)(v & 1ull);
+        if (w == kProducerWarp) {
+            // row k + 1's draws land behind row k's window (ring >= 2 rows + one block)
+            if (k + 1 < n)
+                while (produced < consumed + 2 * need) {
+                    mt_block(s.mt, ring, produced, mask);
+                    produced += kMtN;
                 }
-                const unsigned gi = wd >> half, gq = wd & ((1u << half) - 1u);
-                xr = a.lev_d[a.lev_of_gray[gi]];
-                xi = a.lev_d[a.lev_of_gray[gq]];
-            }
-            if (a.mode == 1) {
-                xdf[(size_t)k * m + l] = make_double2(xr, xi);
-            } else {
-                xo[(size_t)k * m + l] = make_float2((float)xr, (float)xi);
-                nr[l] = xr * xr + xi * xi;
+        } else {
+            for (int l = tid; l < m; l += 256) {
+                double xr, xi;
+                if (l == 0) {
+                    const unsigned b = pil[k];
+                    xr = (b & 1) ? -a.inv_sqrt2 : a.inv_sqrt2;
+                    xi = (b & 2) ? -a.inv_sqrt2 : a.inv_sqrt2;
+                } else {
+                    unsigned wd = 0;
+                    const uint32_t base = consumed + (uint32_t)(l - 1) * bps;
+                    for (int b = 0; b < bps; ++b) {
+                        const uint64_t v = ring[(base + b) & mask];
+                        if (v >= 0xFFFFFFFFFFFFFFFEull) atomicOr(&s.rej, 1);
+                        wd = (wd << 1) | (unsigned)(v & 1ull);
+                    }
+                    const unsigned gi = wd >> half, gq = wd & ((1u << half) - 1u);
+                    xr = a.lev_d[a.lev_of_gray[gi]];
+                    xi = a.lev_d[a.lev_of_gray[gq]];
+                }
+                if (a.mode == 1) {
+                    xdf[(size_t)k * m + l] = make_double2(xr, xi);
+                } else {
+                    xo[(size_t)k * m + l] = make_float2((float)xr, (float)xi);
+                    nr[l] = xr * xr + xi * xi;
+                }
             }
         }
         consumed += need;
@@ -354,26 +364,37 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
     }
     __syncthreads();
 
-    // ---- pass 2: channel + noise, row by row
+    // ---- pass 2: channel + noise, row by row (the producer warp draws row k + 1's noise and
+    // computes its delay phasors while the consumers process row k)
     uint32_t produced = 0, consumed = 0;
     const uint32_t need2 = noisy ? 2u * (uint32_t)m : 0u;
     const double sd = s.sd;
+    auto phasors = [&](int k, int lane_t) {
+        double sn, cs;
+        sincos(-kTwoPiG * (double)k * p.df_hz * s.delay[lane_t], &sn, &cs);
+        s.d_re2[k & 1][lane_t] = 1.0 * cs;
+        s.d_im2[k & 1][lane_t] = 1.0 * sn;
+    };
+    if (w == kProducerWarp) {
+        while (produced < need2) {  // row 0
+            mt_block(s.mt, ring, produced, mask);
+            produced += kMtN;
+        }
+        if ((tid & 31) < T) phasors(0, tid & 31);
+    }
+    __syncthreads();
     for (int k = 0; k < n; ++k) {
-        if (w == 0) {
-            while (produced < consumed + need2) {
-                mt_block(s.mt, ring, produced, mask);
-                produced += kMtN;
+        if (w == kProducerWarp) {
+            if (k + 1 < n) {
+                while (produced < consumed + 2 * need2) {
+                    mt_block(s.mt, ring, produced, mask);
+                    produced += kMtN;
+                }
+                if ((tid & 31) < T) phasors(k + 1, tid & 31);
             }
         } else {
-            while (produced < consumed + need2) produced += kMtN;
-        }
-        if (tid < T) {
-            double sn, cs;
-            sincos(-kTwoPiG * (double)k * p.df_hz * s.delay[tid], &sn, &cs);
-            s.d_re[tid] = 1.0 * cs;
-            s.d_im[tid] = 1.0 * sn;
-        }
-        __syncthreads();
+        const double* d_re = s.d_re2[k & 1];
+        const double* d_im = s.d_im2[k & 1];
         for (int l = tid; l < m; l += 256) {
             // exact fp64 x from the stored c64 value (or the precoded fp64 x_tx in mode 2)
             double xr, xi;
@@ -397,8 +418,8 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
             double yr = 0.0, yi = 0.0, hr = 0.0, hi = 0.0;
             for (int t = 0; t < T; ++t) {
                 // row = b * dph[k]; y += row * fph[l] * x  (std::complex products, left to right)
-                const double rr = s.b_re[t] * s.d_re[t] - s.b_im[t] * s.d_im[t];
-                const double ri = s.b_re[t] * s.d_im[t] + s.b_im[t] * s.d_re[t];
+                const double rr = s.b_re[t] * d_re[t] - s.b_im[t] * d_im[t];
+                const double ri = s.b_re[t] * d_im[t] + s.b_im[t] * d_re[t];
                 const double2 fp = fph[(size_t)t * m + l];
                 const double t1r = rr * fp.x - ri * fp.y;
                 const double t1i = rr * fp.y + ri * fp.x;
@@ -425,6 +446,7 @@ __global__ void __launch_bounds__(256) gen_frame_kernel(GenArgs a) {
                 yi = yi + sd * (r * cs);
             }
             yo[(size_t)k * m + l] = make_float2((float)yr, (float)yi);
+        }
         }
         consumed += need2;
         __syncthreads();
@@ -587,7 +609,7 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
         a.exp_snr = exp_snr;
     }
     uint32_t ring = 1;
-    const uint32_t need = (uint32_t)std::max((p->m - 1) * bps, 2 * p->m) + kMtN;
+    const uint32_t need = 2u * (uint32_t)std::max((p->m - 1) * bps, 2 * p->m) + kMtN;  // rows k, k + 1 + a block
     while (ring < need) ring <<= 1;
     if (ring < 512) ring = 512;
     a.ring_mask = ring - 1;
@@ -601,7 +623,7 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
     if (e != cudaSuccess) return 10;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!p->zc_precode) {
-        gen_frame_kernel<<<(unsigned)count, 256, smem, st>>>(a);
+        gen_frame_kernel<<<(unsigned)count, kGenThreads, smem, st>>>(a);
         return cudaGetLastError() == cudaSuccess ? 0 : 10;
     }
     // ZC precode (D = N): x (fp64) -> Z x per column -> channel, in chunks of frames
@@ -630,11 +652,11 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
         if (a.h_true) b.h_true = a.h_true + c0 * cells;
         b.mode = 1;
         b.xd = xb;
-        gen_frame_kernel<<<(unsigned)nc, 256, smem, st>>>(b);
+        gen_frame_kernel<<<(unsigned)nc, kGenThreads, smem, st>>>(b);
         zc_precode_kernel<<<dim3((unsigned)tiles, (unsigned)nc), 256, 0, st>>>(z, xb, tb, p->n, p->m);
         b.mode = 2;
         b.xd = tb;
-        gen_frame_kernel<<<(unsigned)nc, 256, smem, st>>>(b);
+        gen_frame_kernel<<<(unsigned)nc, kGenThreads, smem, st>>>(b);
     }
     cudaFreeAsync(xb, st);
     cudaFreeAsync(tb, st);
