@@ -600,3 +600,31 @@ def test_fused_periodogram_many_frames_on_device(cuda, window, monkeypatch):
         q = rx.periodogram(h)
     err = ((p - q).abs().amax(dim=(1, 2)) / q.amax(dim=(1, 2))).max().item()
     assert err <= MAP_TOL, err
+
+
+def test_sft_concurrent_host_threads(cuda):
+    """Two host threads, one receiver each, run FPS-SFT at the same time (the per-frame draws
+    share one persistent host worker pool): results equal the sequential ones."""
+    import threading
+    c3 = configs.CFG3
+    F = 32
+    h, s2, _, _ = gen.sparse_frames(c3.n, c3.m, c3.targets, c3.snr_db, c3.base_seed, 0, F)
+    seeds = np.array([gen.derive_seed(c3.base_seed + f, 0x736674) for f in range(F)], np.uint64)
+
+    def run(out, idx):
+        with Receiver(16, 16) as rx:
+            o = rx.sft(h, seeds, s2, i_max=c3.i_max, pfa=c3.pfa, decimation=c3.decimation)
+            torch.cuda.synchronize()
+            out[idx] = (o["k"].cpu().numpy(), o["l"].cpu().numpy(), o["n_entries"].cpu().numpy())
+
+    seq = {}
+    run(seq, 0)
+    par = {}
+    ts = [threading.Thread(target=run, args=(par, i)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(2):
+        for a, b in zip(par[i], seq[0]):
+            assert np.array_equal(a, b)
