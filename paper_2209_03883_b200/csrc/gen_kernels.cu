@@ -157,6 +157,8 @@ struct GenArgs {
     //   (precode_kernel: x_tx = Z x per column, fp64),
     //   mode 2: scene again (same streams), mean_power of the fp64 x_tx, channel + noise.
     int fph_rows;           // target rows of the fph table in shared memory (max targets of the launch)
+    int uniform_power;      // 1: every cell has the same |x|^2 (QPSK): mean_power's sequential sum is
+    double uniform_mp;      //    frame-independent, summed once on the host in the same order
     int mode;               // 0: unprecoded single pass
     double2* xd;            // mode 1: fp64 x out; mode 2: fp64 x_tx in ([count][N][M])
 };
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_frame_kernel(GenArgs a) {
         s.ntar = cnt;
         s.rej = rej;
         s.snr_db = snr;
-        s.mp = 0.0;
+        s.mp = a.uniform_power ? a.uniform_mp : 0.0;
         a.n_targets[f] = cnt;
         if (a.snr_db) a.snr_db[f] = snr;
         for (int t = 0; t < cnt && t < a.max_targets; ++t) {
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_frame_kernel(GenArgs a) {
         }
         consumed += need;
         __syncthreads();
-        if (tid == 32 && a.mode == 0) {  // sequential sum of this row (gen.cpp mean_power order)
+        if (tid == 32 && a.mode == 0 && !a.uniform_power) {  // sequential sum of this row (gen.cpp mean_power order)
             double acc = s.mp;
             for (int l = 0; l < m; ++l) acc += nr[l];
             s.mp = acc;
@@ -598,6 +600,23 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
         a.lev_f[q] = (float)a.lev_d[q];
     }
     a.inv_sqrt2 = 1.0 / std::sqrt(2.0);
+    if (bps == 2 && !p->zc_precode) {
+        // QPSK pilots and payload: |x|^2 = xr xr + xi xi is the same double in every cell, so the
+        // kernel's sequential mean_power sum (cell order, gen.cpp mean_power) is a constant of the
+        // grid size: summed here once, in the same order (the per-row chain leaves the critical path)
+        const double v = a.inv_sqrt2 * a.inv_sqrt2 + a.inv_sqrt2 * a.inv_sqrt2;
+        static thread_local int64_t cached_cells = -1;
+        static thread_local double cached_sum = 0.0;
+        const int64_t cells = (int64_t)p->n * p->m;
+        if (cached_cells != cells) {
+            double acc = 0.0;
+            for (int64_t i = 0; i < cells; ++i) acc += v;
+            cached_cells = cells;
+            cached_sum = acc;
+        }
+        a.uniform_power = 1;
+        a.uniform_mp = cached_sum;
+    }
     if (exp_ranges) {
         if (exp_count < 0 || exp_count > kMaxT || (exp_count > 0 && !exp_vels)) return 2;
         a.explicit_scene = 1;
