@@ -197,18 +197,24 @@ def rmse_sweep(cfg: RadarConfig, ranges, vels, snr_grid_db, trials: int, seed: i
                 phys = [bins_to_physics(int(dd[i, j]), int(vv[i, j]), cfg) for j in range(int(cc[i]))]
                 match_detections(phys, truths, res, stats)
 
-        for snr in snr_grid_db:
-            stats = MatchStats()
-            pending = None
-            for bi, t0 in enumerate(range(0, trials, B)):
+        # batches of every SNR point in one stream of work: the host matches batch j - 1 (which may
+        # belong to the previous SNR point) while the GPU generates and receives batch j
+        all_stats = [MatchStats() for _ in snr_grid_db]
+        pending = None
+        bi = 0
+        for si, snr in enumerate(snr_grid_db):
+            for t0 in range(0, trials, B):
                 nb = min(B, trials - t0)
                 sl = slots[bi % 2]
+                bi += 1
                 enqueue(sl, snr, t0, nb)
                 if pending is not None:
-                    finish(*pending, stats)
-                pending = (sl, nb)
-            finish(*pending, stats)
-            rows.append(finish_row(float(snr), est_name, stats, trials))
+                    finish(*pending)
+                pending = (sl, nb, all_stats[si])
+        if pending is not None:
+            finish(*pending)
+        for si, snr in enumerate(snr_grid_db):
+            rows.append(finish_row(float(snr), est_name, all_stats[si], trials))
     return rows
 
 
