@@ -49,6 +49,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "fused_ce": [],
         "fused_pg": [],
         "fused_pg2": [],
+        "fused_pg3": [],
         "rowpass_zp": [],
         "noise_kernels": [],
         "ofdm_kernels": [],

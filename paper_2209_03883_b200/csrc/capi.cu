@@ -57,6 +57,10 @@ cudaError_t launch_ofdm(bool inverse, const float2* in, float2* out, int n, int 
 cudaError_t launch_noise_select(const float* p, int64_t count, double pf, double* sigma2_out, int64_t frames,
                                 void* scratch, int sms, cudaStream_t st, int64_t* launches);
 cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st);
+cudaError_t launch_fused_pg3(const Pg2Args& a, bool hamming, int groups, cudaStream_t st);
+int fused_pg3_max_groups();
+size_t fused_pg3_counter_ints(int groups);
+size_t fused_pg3_scratch_elems(int groups);
 int fused_pg2_max_groups();
 size_t fused_pg2_counter_ints(int groups);
 size_t fused_pg2_scratch_elems(int groups);
@@ -121,6 +125,9 @@ struct ofdmr_context {
     int pg2_groups = 0;               // warp-specialised periodogram: 16-CTA frame groups
     float2* pg2_scratch = nullptr;    // per group 2 x 1024 x 256 G (L2)
     int* pg2_counters = nullptr;      // per group progress counters
+    int pg3_groups = 0;               // split-exchange periodogram (fused_pg3.cu)
+    float2* pg3_scratch = nullptr;
+    int* pg3_counters = nullptr;
     void* noise_scratch = nullptr;    // estimate_noise_power radix-select histograms
     int64_t noise_cap = 0;            // frames the scratch holds
     float2* dscratch = nullptr;  // fused: per-CTA L x M compressed intermediate
@@ -681,6 +688,8 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->pg_counters);
     cudaFree(c->pg2_scratch);
     cudaFree(c->pg2_counters);
+    cudaFree(c->pg3_scratch);
+    cudaFree(c->pg3_counters);
     cudaFree(c->noise_scratch);
     cudaFree(c->fedges);
     cudaFree(c->fpend);
@@ -834,6 +843,41 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
     (void)chunk;
     const bool pg_shape = c->fast && g.n_subcarriers == 1024 && g.n_symbols == 256 && g.n_prime == 1024 &&
                           g.m_prime == 256 && getenv("OFDMR_PG_PERSIST") == nullptr;
+    if (pg_shape && getenv("OFDMR_PG_V1") == nullptr && getenv("OFDMR_PG2") == nullptr) {
+        // split-radix exchange periodogram (fused_pg3.cu): column warps DFT_32 + twiddle, row
+        // warps DFT_32 + FFT_256, 8-CTA frame groups, double-buffered G in L2
+        if (!c->pg3_scratch) {
+            c->pg3_groups = fused_pg3_max_groups();
+            if (c->pg3_groups <= 0) return fail(OFDMR_ERR_CUDA, "fused periodogram: no co-resident frame group");
+            OFDMR_CUDA(cudaMalloc(&c->pg3_scratch, sizeof(float2) * fused_pg3_scratch_elems(c->pg3_groups)));
+            OFDMR_CUDA(cudaMalloc(&c->pg3_counters, sizeof(int) * fused_pg3_counter_ints(c->pg3_groups)));
+        }
+        const size_t cnt_bytes = sizeof(int) * fused_pg3_counter_ints(c->pg3_groups);
+        Pg2Args pa{};
+        const bool win = g.window == OFDMR_WINDOW_HAMMING;
+        pa.wk = win ? c->wk : nullptr;
+        pa.wl = win ? c->wl : nullptr;
+        pa.tw1024_t = c->tw1024_t;
+        pa.tw256_t = c->tw256_t;
+        pa.gscratch = c->pg3_scratch;
+        pa.counters = c->pg3_counters;
+        pa.scale = c->scale;
+        for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 28) {
+            const int64_t nf = std::min<int64_t>((int64_t)1 << 28, frames - f0);
+            OFDMR_CUDA(cudaMemsetAsync(c->pg3_counters, 0, cnt_bytes, c->stream));
+            pa.h = static_cast<const float2*>(h) + fc * f0;
+            pa.p = p + pframe * f0;
+            pa.frames = int(nf);
+            cudaError_t e;
+            {
+                StageTimer t(c, 0, c->stream);
+                e = launch_fused_pg3(pa, win, int(std::min<int64_t>(c->pg3_groups, nf)), c->stream);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "fused_pg3");
+            ++c->launches;
+        }
+        return OFDMR_OK;
+    }
     if (pg_shape && getenv("OFDMR_PG_V1") == nullptr) {
         // warp-specialised single-launch periodogram (16-CTA frame groups, column and row
         // warps concurrent, double-buffered G in L2)

@@ -24,12 +24,70 @@ namespace ofdmr {
 
 constexpr int kTwLen = 4096;  // twiddle table length (max supported FFT length)
 
+// Complex fp32 arithmetic on sm_100a's packed FP32x2 pipe (FADD2 / FMUL2 / FFMA2): one
+// warp-instruction operates on both halves of a float2, so every complex add is ONE issue slot
+// and a complex multiply TWO (FMUL2 + FFMA2 with the swapped, half-negated operand encoded as
+// an operand modifier), against 2 and 4 scalar instructions.  The FP32 pipe itself is not
+// faster (128 lane-ops / SM / cycle either way, tools/micro/f32x2_micro.cu) but the FFT kernels
+// here are issue-bound, not FMA-pipe-bound.  Each half is the IEEE round-to-nearest operation
+// of the scalar form (no contraction beyond the explicit fma).  -DOFDMR_SCALAR_FP32 restores
+// the scalar code for A/B measurements.
+#ifndef OFDMR_SCALAR_FP32
+typedef unsigned long long f2bits;
+__device__ __forceinline__ f2bits f2_pack(float a, float b) {
+    f2bits r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f2bits f2_pack(float2 a) { return f2_pack(a.x, a.y); }
+__device__ __forceinline__ float2 f2_unpack(f2bits r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 f2_add(float2 a, float2 b) {
+    f2bits r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(r);
+}
+__device__ __forceinline__ float2 f2_sub(float2 a, float2 b) {
+    f2bits r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(r);
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+    f2bits r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+    return f2_unpack(r);
+}
+// a * b + c, per half
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+    f2bits r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
+    return f2_unpack(r);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return f2_add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return f2_sub(a, b); }
+// a w = w.x (a.x, a.y) + w.y (-a.y, a.x): FMUL2 + FFMA2
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+    return f2_fma(make_float2(-a.y, a.x), make_float2(w.y, w.y), f2_mul(a, make_float2(w.x, w.x)));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return f2_mul(a, make_float2(s, s)); }
+// e + (c + j s) o for real constants c, s: two FFMA2
+__device__ __forceinline__ float2 cfma_cs(float c, float s, float2 o, float2 e) {
+    return f2_fma(make_float2(-o.y, o.x), make_float2(s, s), f2_fma(o, make_float2(c, c), e));
+}
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cfma_cs(float c, float s, float2 o, float2 e) {
+    return make_float2(fmaf(c, o.x, fmaf(-s, o.y, e.x)), fmaf(c, o.y, fmaf(s, o.x, e.y)));
+}
+#endif
 __device__ __forceinline__ float cnorm(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
 
 __host__ __device__ constexpr int pad_len(int len) { return len + len / 32 + 1; }
@@ -80,14 +138,18 @@ template <bool INV, int K> __device__ __forceinline__ float2 mul_w32(float2 a) {
     else {
         constexpr float c = W32c<k>::c();
         constexpr float s = INV ? W32c<k>::s() : -W32c<k>::s();
+#ifndef OFDMR_SCALAR_FP32
+        return f2_fma(make_float2(-a.y, a.x), make_float2(s, s), f2_mul(a, make_float2(c, c)));
+#else
         return make_float2(c * a.x - s * a.y, c * a.y + s * a.x);
+#endif
     }
 }
 
 
 // Radix-2 butterfly with a constant twiddle w = W_32^K (forward e^{-2 pi i K/32}, inverse
-// conjugate): lo = e + w o, hi = e - w o.  General K: four FMAs for lo and hi = 2e - lo
-// (six FP instructions instead of a 4-instruction multiply plus four adds).
+// conjugate): lo = e + w o, hi = e - w o.  General K: lo with two FFMA2 and hi = 2e - lo with
+// one (three packed instructions instead of a 2-instruction multiply plus two adds).
 template <bool INV, int K>
 __device__ __forceinline__ void bfly32(float2& lo, float2& hi, float2 e, float2 o) {
     constexpr int k = K % 32;
@@ -98,8 +160,12 @@ __device__ __forceinline__ void bfly32(float2& lo, float2& hi, float2 e, float2 
     } else {
         constexpr float c = W32c<k>::c();
         constexpr float s = INV ? W32c<k>::s() : -W32c<k>::s();
-        const float2 a = make_float2(fmaf(c, o.x, fmaf(-s, o.y, e.x)), fmaf(c, o.y, fmaf(s, o.x, e.y)));
+        const float2 a = cfma_cs(c, s, o, e);
+#ifndef OFDMR_SCALAR_FP32
+        hi = f2_fma(e, make_float2(2.0f, 2.0f), make_float2(-a.x, -a.y));
+#else
         hi = make_float2(fmaf(2.0f, e.x, -a.x), fmaf(2.0f, e.y, -a.y));
+#endif
         lo = a;
     }
 }

@@ -162,7 +162,11 @@ template <bool HAMMING>
 __global__ void __launch_bounds__(kThreads, PG2_CPS)
     fused_pg2_kernel(Pg2Args a, const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap gmap) {
     extern __shared__ unsigned char smem_raw[];
-    Pg2Smem& s = *reinterpret_cast<Pg2Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B alignment (TMA swizzle atoms) as an offset from the __shared__ symbol: the pointer
+    // stays in the shared window, so every access below compiles to LDS/STS (a round trip
+    // through uintptr_t would make them 64-bit generic LD.E/ST.E on the LSU's global queue)
+    const unsigned s_pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+    Pg2Smem& s = *reinterpret_cast<Pg2Smem*>(smem_raw + s_pad);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool is_col = warp < kColWarps;  // (interleaving the roles across schedulers measured slower)
     const int ridx = is_col ? warp : warp - kColWarps;

@@ -58,6 +58,9 @@ int main() {
     cudaMalloc(&tw, 1024 * sizeof(float2));
     cudaMalloc(&out, 1 << 24);
     cudaMemcpy(tw, t.data(), 1024 * sizeof(float2), cudaMemcpyHostToDevice);
+    run<1>(1, sms, tw, out);
+    run<2>(1, sms, tw, out);
+    run<4>(1, sms, tw, out);
     run<8>(1, sms, tw, out);
     run<8>(2, sms, tw, out);
     run<4>(4, sms, tw, out);
