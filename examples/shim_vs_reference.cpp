@@ -113,6 +113,25 @@ int main() {
     std::printf("sft_iterate: reference %zu entries, b200 %zu entries, same support = %d, iterations %zu/%zu\n",
                 s1.entries.size(), s2.entries.size(), int(a1 == a2), s1.iterations, s2.iterations);
     fails += a1 != a2;
+    // detections_from_spectrum / sft_detect (sft.hpp:67-75) on the same spectrum and grid
+    {
+        const auto d1 = detections_from_spectrum(s1, 64, 32, wc, 0.01, 1e-2, 4);
+        const auto d2 = b200::detections_from_spectrum(s1, 64, 32, wc, 0.01, 1e-2, 4);
+        bool same = d1.size() == d2.size();
+        for (std::size_t i = 0; same && i < d1.size(); ++i)
+            same = d1[i].delay_bin == d2[i].delay_bin && d1[i].doppler_bin == d2[i].doppler_bin &&
+                   d1[i].peak_power == d2[i].peak_power && d1[i].range_m == d2[i].range_m &&
+                   d1[i].velocity_mps == d2[i].velocity_mps;
+        SftConfig sd;
+        sd.seed = 11;
+        const auto t1 = sft_detect(s, wc, sd, 0.01, 1e-2, 5), t2 = b200::sft_detect(s, wc, sd, 0.01, 1e-2, 5);
+        bool same2 = t1.size() == t2.size();
+        for (std::size_t i = 0; same2 && i < t1.size(); ++i)
+            same2 = t1[i].delay_bin == t2[i].delay_bin && t1[i].doppler_bin == t2[i].doppler_bin;
+        std::printf("detections_from_spectrum: %zu/%zu identical = %d; sft_detect %zu/%zu identical bins = %d\n",
+                    d1.size(), d2.size(), int(same), t1.size(), t2.size(), int(same2));
+        fails += !same || !same2;
+    }
     // estimate_noise_power on the reference's own periodogram
     {
         const double pfw = w.power_factor();

@@ -13,9 +13,10 @@
  * Errors: every function returns OFDMR_OK (0), OFDMR_ERR_CONFIG (2, mirrors
  * ofdmradar::ConfigError, include/ofdmradar/errors.hpp:9-12) or OFDMR_ERR_CUDA (10).
  * ofdmr_last_error() returns a thread-local message for the last failure.  A zero
- * X cell (spectral_division's ConfigError, src/estimation.cpp:17) is reported per
- * frame through the device `status` array (bit 0) — stream-ordered calls cannot
- * throw; the synchronous host entry point returns OFDMR_ERR_CONFIG for it.
+ * X cell (spectral_division's ConfigError, src/estimation.cpp:17: both components exactly
+ * zero; denormal or huge cells are divided in fp64, not rejected) is reported per frame
+ * through the device `status` array (bit 0) — stream-ordered calls cannot throw; the
+ * synchronous host entry point returns OFDMR_ERR_CONFIG for it.
  *
  * Sizes: N, M, N', M' must be powers of two in [16, 4096] (B200 design limit; the
  * reference also accepts other sizes through FFTW), N' >= N, M' >= M
@@ -135,15 +136,19 @@ int ofdmr_extract_peaks(ofdmr_context* ctx, const float* p, const double* eta, c
 int ofdmr_pipeline(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
                    const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
                    int32_t* counts, double* sigma2_h_out, float* p_out, int32_t* status, int64_t frames);
-/* Status bit 1 (value 2) after ofdmr_pipeline: the fused fast path kept at most 1024
- * strict local maxima above eta per half-frame and this frame had more (only when sigma2
- * is mis-set far below the noise floor); recompute such frames with this entry point,
- * which always takes the chunked two-pass path (exact for any candidate count). */
+/* Status bit 1 (value 2) after ofdmr_pipeline: recompute this frame with this entry point,
+ * which always takes the chunked two-pass path (exact for any candidate count, and the only
+ * path that sets bit 0).  The fused fast path sets it when it kept at most 1024 strict local
+ * maxima above eta per half-frame and the frame had more (only when sigma2 is mis-set far
+ * below the noise floor), or when some |x|^2 fell outside the fp32 normal range (an exactly
+ * zero x cell -> bit 0 on recompute, estimation.cpp:17; a denormal or huge x cell, which the
+ * exact path divides in fp64 like the reference does on the upcast complex<double>). */
 int ofdmr_pipeline_general(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
                            const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
                            int32_t* counts, double* sigma2_h_out, float* p_out, int32_t* status, int64_t frames);
-/* Same on HOST buffers (pinned recommended): copies inside, double-buffered, synchronous.
- * Returns OFDMR_ERR_CONFIG if any frame had a zero X cell. */
+/* Same on HOST buffers (pinned recommended): copies inside, double-buffered (chunk i+1's copies
+ * and kernels are enqueued before chunk i's status is checked), synchronous on return; status-bit-1
+ * frames are recomputed on the exact path.  Returns OFDMR_ERR_CONFIG if any frame had a zero X cell. */
 int ofdmr_pipeline_host(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
                         const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
                         int32_t* counts, int64_t frames);
@@ -160,14 +165,49 @@ typedef struct ofdmr_sft_config {
     int32_t max_entries;     /* entries kept per frame (<= 64) */
 } ofdmr_sft_config;
 
-/* sft_iterate over a batch of N x M c64 grids h (device).  seeds[f] = SftConfig.seed,
- * sigma2[f] = SftConfig.sigma2 (host arrays).  Outputs (device, [frame][max_entries]):
- * k, l, amplitude (complex double re/im interleaved), n_entries, and per-frame stats
- * (iterations, samples_used, converged, residual_energy; device). */
+/* sft_iterate (sft.cpp:185-459) over a batch of N x M c64 grids h (device).  seeds[f] =
+ * SftConfig.seed, sigma2[f] = SftConfig.sigma2 (host arrays; the slope / offset draws are made on
+ * the device from the seeds).  Outputs (device, [frame][max_entries]): k, l, amplitude (complex
+ * double re/im interleaved), n_entries, and per-frame stats (iterations, samples_used, converged,
+ * residual_energy; device, each may be NULL).  status (device, may be NULL): when given the call
+ * is stream-ordered and a frame that exceeds the on-chip limits (> 128 accepted tones, or more
+ * entries than max_entries) gets bit 2 (value 4); when NULL the call synchronises and returns
+ * OFDMR_ERR_CONFIG for such a frame. */
 int ofdmr_sft(ofdmr_context* ctx, const void* h, int32_t n, int32_t m, const ofdmr_sft_config* cfg,
               const uint64_t* seeds, const double* sigma2, int32_t* k_out, int32_t* l_out, double* amp_out,
               int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged,
-              double* residual, int64_t frames);
+              double* residual, int32_t* status, int64_t frames);
+
+/* detections_from_spectrum (sft.cpp:461-490) on device SFT entries ([frame][max_entries] k, l,
+ * complex-double amplitudes, n_entries): power = |A|^2 N M >= eta = -sigma2[f] ln(pfa) (sigma2 on
+ * the device), delay = (N - k) mod N, Doppler = (l + M/2) mod M - M/2, ordered by (power desc,
+ * delay, Doppler), at most k_per_frame[f] (NULL = cfg.max_targets) records of the ofdmr_detect
+ * layout.  Stream-ordered. */
+int ofdmr_sft_detections(ofdmr_context* ctx, const int32_t* k, const int32_t* l, const double* amp,
+                         const int32_t* n_entries, int32_t max_entries, int32_t n, int32_t m, const double* sigma2,
+                         double pfa, const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin,
+                         float* peak_power, int32_t* counts, int64_t frames);
+
+/* sft_detect (sft.cpp:492-500): sft_iterate with SftConfig{cfg, seed = seeds[f] (host),
+ * sigma2 = sigma2[f] (DEVICE)} then detections_from_spectrum with the same sigma2 and cfg->pfa.
+ * Stream-ordered; status (device) as in ofdmr_sft. */
+int ofdmr_sft_detect(ofdmr_context* ctx, const void* h, int32_t n, int32_t m, const ofdmr_sft_config* cfg,
+                     const uint64_t* seeds, const double* sigma2, const int32_t* k_per_frame, int32_t* delay_bin,
+                     int32_t* doppler_bin, float* peak_power, int32_t* counts, int32_t* status, int64_t frames);
+
+/* The FPS-SFT branch of run_pipeline (pipeline.cpp:60-113) on device frames: estimate_channel
+ * (cfg.estimator: LS / ZCP-LS / DFT-CE with L = cfg.n_cp) -> sigma_h^2 = division_noise_power(
+ * sigma2[f], x_tx) -> [noise_seeds != NULL: sigma2 = estimate_noise_from_slice(H, noise_seeds[f])]
+ * -> sft_iterate(H, SftConfig{cfg, seed = sft_seeds[f], sigma2}) -> detections_from_spectrum(
+ * sigma2, cfg->pfa, K).  sigma2 (per-frame AWGN power) on the device, seeds on the host
+ * (run_pipeline: sft seed = derive_seed(seed, 0x736674), noise seed = derive_seed(seed, 0x6e6573)).
+ * sigma2_used_out (device, may be NULL) = PipelineResult::sigma2_used.  status (device): bit 0
+ * zero X cell, bit 2 SFT overflow.  Stream-ordered; N x M channel estimates of up to 1 GiB of
+ * frames at a time live in context scratch. */
+int ofdmr_pipeline_sft(ofdmr_context* ctx, const void* y, const void* x_tx, const double* sigma2,
+                       const uint64_t* sft_seeds, const uint64_t* noise_seeds, const ofdmr_sft_config* cfg,
+                       const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
+                       int32_t* counts, double* sigma2_used_out, int32_t* status, int64_t frames);
 
 /* estimate_noise_from_slice, pipeline.cpp:26-43 (run_pipeline's FPS-SFT estimate-noise mode,
  * pipeline.cpp:97-98): per frame, Rng(seeds[f]) draws the admissible slope, the slice of

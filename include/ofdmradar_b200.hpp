@@ -263,7 +263,7 @@ inline SparseSpectrum sft_iterate(const ComplexGrid& h, const SftConfig& cfg) {
     cuda(cudaMemcpy(hd.p, hh.data(), sizeof(float) * hh.size(), cudaMemcpyHostToDevice));
     const uint64_t seed = cfg.seed;
     const double s2 = cfg.sigma2;
-    check(ofdmr_sft(c, hd.p, n, m, &sc, &seed, &s2, kd.p, ld.p, ad.p, ne.p, it.p, su.p, cv.p, rs.p, 1));
+    check(ofdmr_sft(c, hd.p, n, m, &sc, &seed, &s2, kd.p, ld.p, ad.p, ne.p, it.p, su.p, cv.p, rs.p, nullptr, 1));
     cuda(cudaDeviceSynchronize());
     int32_t nent = 0, iters = 0, conv = 0;
     int64_t used = 0;
@@ -285,6 +285,78 @@ inline SparseSpectrum sft_iterate(const ComplexGrid& h, const SftConfig& cfg) {
     s.iterations = std::size_t(iters);
     s.samples_used = std::size_t(used);
     return s;
+}
+
+namespace detail {
+// Detection records of an FPS-SFT entry set: peak_power recomputed in fp64 from the matching
+// entry (the device record carries it in fp32), physics as sft.cpp:476-479.
+inline std::vector<Detection> sft_records(const std::vector<int32_t>& dh, const std::vector<int32_t>& vh,
+                                          int32_t cnt, const SparseSpectrum& spec, std::size_t n, std::size_t m,
+                                          const WaveformConfig& cfg) {
+    std::vector<Detection> out(static_cast<std::size_t>(cnt));
+    const double nm = double(n) * double(m);
+    for (int32_t i = 0; i < cnt; ++i) {
+        Detection& d = out[i];
+        d.delay_bin = dh[i];
+        d.doppler_bin = vh[i];
+        const long k = (long(n) - d.delay_bin) % long(n), l = ((d.doppler_bin % long(m)) + long(m)) % long(m);
+        for (const auto& e : spec.entries)
+            if (long(e.k) == k && long(e.l) == l) d.peak_power = std::norm(e.amplitude) * nm;
+        d.range_m = kSpeedOfLight * double(d.delay_bin) / (2.0 * double(n) * cfg.subcarrier_spacing_hz);
+        d.velocity_mps =
+            kSpeedOfLight * double(d.doppler_bin) / (2.0 * cfg.carrier_hz * double(m) * cfg.symbol_time());
+    }
+    return out;
+}
+}  // namespace detail
+
+// sft.hpp:67-70 — detections_from_spectrum through the device entry point (ofdmr_sft_detections):
+// threshold, bin mapping and the (power, delay, Doppler) ranking run on the GPU in fp64.
+inline std::vector<Detection> detections_from_spectrum(const SparseSpectrum& spec, std::size_t n, std::size_t m,
+                                                       const WaveformConfig& cfg, double sigma2, double pfa,
+                                                       std::size_t max_targets) {
+    using namespace detail;
+    if (sigma2 < 0.0) throw ConfigError("threshold: sigma2 must be >= 0");
+    if (!(pfa > 0.0 && pfa <= 1.0)) throw ConfigError("threshold: pfa must lie in (0,1]");
+    if (spec.entries.empty() || max_targets == 0) return {};
+    if (spec.entries.size() > 64) throw ConfigError("detections_from_spectrum: at most 64 entries on the GPU path");
+    const int32_t k = int32_t(max_targets > 64 ? 64 : max_targets);
+    const int32_t ne = int32_t(spec.entries.size());
+    ofdmr_context* c = context(16, 16, 16, 16, OFDMR_WINDOW_RECT, OFDMR_EST_LS, 0, k, 1e-2);
+    std::vector<int32_t> kh(ne), lh(ne);
+    std::vector<double> ah(2 * ne);
+    for (int32_t i = 0; i < ne; ++i) {
+        kh[i] = int32_t(spec.entries[i].k);
+        lh[i] = int32_t(spec.entries[i].l);
+        ah[2 * i] = spec.entries[i].amplitude.real();
+        ah[2 * i + 1] = spec.entries[i].amplitude.imag();
+    }
+    DevBuf<int32_t> kd(ne), ld(ne), nd(1), dd(k), vd(k), cn(1);
+    DevBuf<double> ad(2 * ne), sd(1);
+    DevBuf<float> pw(k);
+    cuda(cudaMemcpy(kd.p, kh.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
+    cuda(cudaMemcpy(ld.p, lh.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice));
+    cuda(cudaMemcpy(ad.p, ah.data(), sizeof(double) * 2 * ne, cudaMemcpyHostToDevice));
+    cuda(cudaMemcpy(nd.p, &ne, sizeof(int32_t), cudaMemcpyHostToDevice));
+    cuda(cudaMemcpy(sd.p, &sigma2, sizeof(double), cudaMemcpyHostToDevice));
+    check(ofdmr_sft_detections(c, kd.p, ld.p, ad.p, nd.p, ne, int32_t(n), int32_t(m), sd.p, pfa, nullptr, dd.p, vd.p,
+                               pw.p, cn.p, 1));
+    int32_t cnt = 0;
+    std::vector<int32_t> dh(k), vh(k);
+    cuda(cudaMemcpy(&cnt, cn.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    cuda(cudaMemcpy(dh.data(), dd.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost));
+    cuda(cudaMemcpy(vh.data(), vd.p, sizeof(int32_t) * k, cudaMemcpyDeviceToHost));
+    return sft_records(dh, vh, cnt, spec, n, m, cfg);
+}
+
+// sft.hpp:73-75 — sft_detect (sft.cpp:492-500): sigma2 / pfa fill the SftConfig when unset.
+inline std::vector<Detection> sft_detect(const ComplexGrid& h, const WaveformConfig& cfg, const SftConfig& sft_cfg,
+                                         double sigma2, double pfa, std::size_t max_targets) {
+    SftConfig scfg = sft_cfg;
+    if (scfg.sigma2 == 0.0) scfg.sigma2 = sigma2;
+    if (scfg.pfa <= 0.0) scfg.pfa = pfa;
+    const SparseSpectrum spec = b200::sft_iterate(h, scfg);
+    return b200::detections_from_spectrum(spec, h.rows(), h.cols(), cfg, sigma2, pfa, max_targets);
 }
 
 }  // namespace ofdmradar::b200

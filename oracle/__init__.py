@@ -141,6 +141,8 @@ def ref() -> C.CDLL:
         _ref.ref_sft_batch_c64.argtypes = [vp, i64, i64, i64, i64, vp, vp, d, i64, i64, vp, vp, vp, vp, vp, C.c_int]
         _ref.ref_make_frame_pair.argtypes = [i64, i64, d, d, i64, C.c_int, vp, vp, i64, d, C.c_uint64, vp, vp, vp]
         _ref.ref_rng_u64.argtypes = [C.c_uint64, i64, vp]
+        _ref.ref_run_pipeline_sft.argtypes = [i64, i64, d, d, i64, C.c_int, C.c_int, vp, vp, C.c_int32, d, C.c_uint64,
+                                              C.c_int, i64, i64, vp, vp, vp, vp, vp]
         _ref.ref_sft_noise_case.argtypes = [i64, i64, d, d, i64, vp, vp, C.c_int32, d, C.c_uint64, vp, vp]
         _ref.ref_estimate_noise_power.restype = d
         _ref.ref_estimate_noise_power.argtypes = [vp, i64, i64, d]
@@ -385,3 +387,51 @@ def ref_mse_sweep(scn, snr_grid, trials: int, seed: int) -> np.ndarray:
     rc = ref().ref_mse_sweep(*args, _p(g), len(g), trials, seed, _p(rows))
     assert rc == 0
     return rows
+
+
+def ref_make_frame_pair(n, m, df, fc, n_cp, qam, ranges, vels, snr_db: float, seed: int):
+    """run_pipeline's frame for `seed` (make_random_frame + apply_channel, pipeline.cpp:65-70) from
+    the reference sources: (y, x) complex128 N x M and the realization's sigma2."""
+    r = np.ascontiguousarray(ranges, np.float64)
+    v = np.ascontiguousarray(vels, np.float64)
+    y = np.empty((n, m), np.complex128)
+    x = np.empty((n, m), np.complex128)
+    s2 = C.c_double()
+    rc = ref().ref_make_frame_pair(n, m, df, fc, n_cp, qam, _p(r), _p(v), len(r), snr_db, seed, _p(y), _p(x),
+                                   C.byref(s2))
+    if rc:
+        raise ValueError(f"ref_make_frame_pair failed ({rc})")
+    return y, x, s2.value
+
+
+def ref_run_pipeline_sft(n, m, df, fc, n_cp, qam, estimator, ranges, vels, snr_db: float, seed: int,
+                         estimate_noise: bool, i_max: int, max_targets: int):
+    """The reference's run_pipeline with the FPS-SFT detector: ([(delay, doppler, power)], sigma2_used)."""
+    r = np.ascontiguousarray(ranges, np.float64)
+    v = np.ascontiguousarray(vels, np.float64)
+    k = max(max_targets, 1)
+    d = np.zeros(k, np.int64)
+    dp = np.zeros(k, np.int64)
+    w = np.zeros(k)
+    cnt = C.c_long()
+    s2u = C.c_double()
+    rc = ref().ref_run_pipeline_sft(n, m, df, fc, n_cp, qam, estimator, _p(r), _p(v), len(r), snr_db, seed,
+                                    1 if estimate_noise else 0, i_max, max_targets, _p(d), _p(dp), _p(w),
+                                    C.byref(cnt), C.byref(s2u))
+    if rc:
+        raise ValueError(f"ref_run_pipeline_sft failed ({rc})")
+    return [(int(d[i]), int(dp[i]), float(w[i])) for i in range(cnt.value)], s2u.value
+
+
+def sft_pipeline_frame(y: np.ndarray, x: np.ndarray, sigma2: float, estimator: int, n_cp: int, sft_seed: int,
+                       noise_seed: int | None, i_max: int, pfa: float, max_targets: int):
+    """The FPS-SFT branch of run_pipeline (pipeline.cpp:47-58, 79, 97-113) restated on one frame with
+    the oracle's functions (fp64 on the upcast inputs): ([(delay, doppler, power)], sigma2_used, spectrum)."""
+    h = spectral_division(y, x)
+    if estimator == 1:
+        h = dft_ce(h, n_cp)
+    s2 = division_noise_power(sigma2, x)
+    if noise_seed is not None:
+        s2 = estimate_noise_from_slice(h, noise_seed)
+    spec = sft_iterate(h, sft_seed, s2, i_max=i_max, pfa=pfa)
+    return detections_from_spectrum(spec["entries"], h.shape[0], h.shape[1], s2, pfa, max_targets), s2, spec

@@ -30,6 +30,35 @@ static const double kTwoPi = 6.283185307179586476925286766559;
 
 static int is_pow2(size_t n) { return n && !(n & (n - 1)); }
 
+/* Per-(n, sign) twiddle tables, computed once with the same expression as before and cached
+ * for the life of the process (the reference caches its FFTW plans the same way, fft.cpp:17-43),
+ * so a transform no longer pays malloc + n/2 cos/sin per call.  Values and butterfly order are
+ * unchanged: every output is bit-identical to the uncached version. */
+#define ORC_TW_MAX_LOG2 40
+static double* g_tw_cache[2][ORC_TW_MAX_LOG2];
+static pthread_mutex_t g_tw_mu = PTHREAD_MUTEX_INITIALIZER;
+
+static const double* pow2_twiddles(size_t n, int sign) {
+    int lg = 0;
+    while (((size_t)1 << lg) < n) lg++;
+    const int si = sign > 0;
+    double* tw = __atomic_load_n(&g_tw_cache[si][lg], __ATOMIC_ACQUIRE);
+    if (tw) return tw;
+    pthread_mutex_lock(&g_tw_mu);
+    tw = g_tw_cache[si][lg];
+    if (!tw) {
+        tw = (double*)malloc(sizeof(double) * (n > 1 ? n : 2)); /* n/2 complex twiddles of the top level */
+        for (size_t k = 0; k < n / 2; k++) {
+            const double ang = (double)sign * kTwoPi * (double)k / (double)n;
+            tw[2 * k] = cos(ang);
+            tw[2 * k + 1] = sin(ang);
+        }
+        __atomic_store_n(&g_tw_cache[si][lg], tw, __ATOMIC_RELEASE);
+    }
+    pthread_mutex_unlock(&g_tw_mu);
+    return tw;
+}
+
 /* In-place iterative radix-2 on interleaved doubles. sign = -1 forward, +1 inverse. */
 static void fft_pow2(double* a, size_t n, int sign) {
     if (n <= 1) return;
@@ -45,12 +74,7 @@ static void fft_pow2(double* a, size_t n, int sign) {
             a[2 * j + 1] = t1;
         }
     }
-    double* tw = (double*)malloc(sizeof(double) * n); /* n/2 complex twiddles of the top level */
-    for (size_t k = 0; k < n / 2; k++) {
-        const double ang = (double)sign * kTwoPi * (double)k / (double)n;
-        tw[2 * k] = cos(ang);
-        tw[2 * k + 1] = sin(ang);
-    }
+    const double* tw = pow2_twiddles(n, sign);
     for (size_t len = 2; len <= n; len <<= 1) {
         const size_t half = len / 2, step = n / len;
         for (size_t i = 0; i < n; i += len) {
@@ -67,34 +91,69 @@ static void fft_pow2(double* a, size_t n, int sign) {
             }
         }
     }
-    free(tw);
 }
 
-/* Bluestein chirp-z for arbitrary n (reference tests use 48, 70, 560, lcm sizes). */
-static void fft_bluestein(double* a, size_t n, int sign) {
+/* Bluestein chirp-z for arbitrary n (reference tests use 48, 70, 560, lcm sizes).  The chirp w
+ * and the transformed kernel FFT(B) depend only on (n, sign): cached like the radix-2 twiddles
+ * (same expressions, same transform: bit-identical results). */
+typedef struct blu_plan {
+    size_t n, m;
+    int sign;
+    double* w;   /* 2n: chirp e^{sign j pi k^2 / n} */
+    double* fb;  /* 2m: FFT_m of the conjugate chirp kernel */
+    struct blu_plan* next;
+} blu_plan;
+static blu_plan* g_blu_plans;
+static pthread_mutex_t g_blu_mu = PTHREAD_MUTEX_INITIALIZER;
+
+static const blu_plan* bluestein_plan(size_t n, int sign) {
+    pthread_mutex_lock(&g_blu_mu);
+    for (blu_plan* p = g_blu_plans; p; p = p->next)
+        if (p->n == n && p->sign == sign) {
+            pthread_mutex_unlock(&g_blu_mu);
+            return p;
+        }
     size_t m = 1;
     while (m < 2 * n - 1) m <<= 1;
-    double* w = (double*)malloc(sizeof(double) * 2 * n);
-    double* A = (double*)calloc(2 * m, sizeof(double));
-    double* B = (double*)calloc(2 * m, sizeof(double));
+    blu_plan* p = (blu_plan*)malloc(sizeof(blu_plan));
+    p->n = n;
+    p->m = m;
+    p->sign = sign;
+    p->w = (double*)malloc(sizeof(double) * 2 * n);
+    p->fb = (double*)calloc(2 * m, sizeof(double));
     for (size_t k = 0; k < n; k++) {
         const unsigned long long k2 = ((unsigned long long)k * k) % (2ULL * n);
         const double ang = (double)sign * kTwoPi * 0.5 * (double)k2 / (double)n;
-        w[2 * k] = cos(ang);
-        w[2 * k + 1] = sin(ang);
+        p->w[2 * k] = cos(ang);
+        p->w[2 * k + 1] = sin(ang);
     }
+    double* B = p->fb;
+    B[0] = p->w[0];
+    B[1] = -p->w[1];
+    for (size_t k = 1; k < n; k++) {
+        B[2 * k] = B[2 * (m - k)] = p->w[2 * k];
+        B[2 * k + 1] = B[2 * (m - k) + 1] = -p->w[2 * k + 1];
+    }
+    pthread_mutex_unlock(&g_blu_mu);
+    fft_pow2(B, m, -1);
+    pthread_mutex_lock(&g_blu_mu);
+    p->next = g_blu_plans;
+    g_blu_plans = p;
+    pthread_mutex_unlock(&g_blu_mu);
+    return p;
+}
+
+static void fft_bluestein(double* a, size_t n, int sign) {
+    const blu_plan* pl = bluestein_plan(n, sign);
+    const size_t m = pl->m;
+    const double* w = pl->w;
+    const double* B = pl->fb;
+    double* A = (double*)calloc(2 * m, sizeof(double));
     for (size_t k = 0; k < n; k++) {
         A[2 * k] = a[2 * k] * w[2 * k] - a[2 * k + 1] * w[2 * k + 1];
         A[2 * k + 1] = a[2 * k] * w[2 * k + 1] + a[2 * k + 1] * w[2 * k];
     }
-    B[0] = w[0];
-    B[1] = -w[1];
-    for (size_t k = 1; k < n; k++) {
-        B[2 * k] = B[2 * (m - k)] = w[2 * k];
-        B[2 * k + 1] = B[2 * (m - k) + 1] = -w[2 * k + 1];
-    }
     fft_pow2(A, m, -1);
-    fft_pow2(B, m, -1);
     for (size_t k = 0; k < m; k++) {
         const double r = A[2 * k] * B[2 * k] - A[2 * k + 1] * B[2 * k + 1];
         const double i = A[2 * k] * B[2 * k + 1] + A[2 * k + 1] * B[2 * k];
@@ -108,9 +167,7 @@ static void fft_bluestein(double* a, size_t n, int sign) {
         a[2 * k] = cr * w[2 * k] - ci * w[2 * k + 1];
         a[2 * k + 1] = cr * w[2 * k + 1] + ci * w[2 * k];
     }
-    free(w);
     free(A);
-    free(B);
 }
 
 /* fft.hpp:12-15 contract: unscaled; sign -1 = forward e^{-j}, +1 = inverse e^{+j}. */

@@ -352,6 +352,37 @@ int ref_run_pipeline(int64_t n, int64_t m, int64_t np, int64_t mp, double df, do
     }
 }
 
+/// run_pipeline (pipeline.cpp:60-115) with the FPS-SFT detector (DetectorKind::FpsSft, sft_i_max,
+/// optionally estimate_noise) on a scenario whose frames ref_make_frame_pair rebuilds with the same
+/// seed: detections (delay, Doppler, peak power) and PipelineResult::sigma2_used.
+int ref_run_pipeline_sft(int64_t n, int64_t m, double df, double fc, int64_t n_cp, int qam, int estimator,
+                         const double* ranges, const double* vels, int32_t count, double snr_db, uint64_t seed,
+                         int estimate_noise, int64_t i_max, int64_t max_targets, long* delay, long* doppler,
+                         double* power, long* n_det, double* sigma2_used) {
+    try {
+        SimulationConfig cfg = scenario(n, m, n, m, df, fc, n_cp, 0, 0.01, estimator, ranges, vels, count);
+        cfg.waveform.qam_order = std::size_t(qam);
+        cfg.channel.snr_db = snr_db;
+        cfg.detector.kind = DetectorKind::FpsSft;
+        cfg.detector.estimate_noise = estimate_noise != 0;
+        cfg.detector.sft_i_max = std::size_t(i_max);
+        cfg.detector.max_targets = std::size_t(max_targets);
+        const auto res = run_pipeline(cfg, seed);
+        for (std::size_t i = 0; i < res.detections.size(); ++i) {
+            delay[i] = res.detections[i].delay_bin;
+            doppler[i] = res.detections[i].doppler_bin;
+            power[i] = res.detections[i].peak_power;
+        }
+        *n_det = long(res.detections.size());
+        *sigma2_used = res.sigma2_used;
+        return 0;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (...) {
+        return 3;
+    }
+}
+
 /// run_pipeline (pipeline.cpp:60-115) with the FPS-SFT detector in estimate-noise mode: the
 /// reference's own sigma2_used (= estimate_noise_from_slice(h, derive_seed(seed, 0x6e6573)),
 /// an anonymous-namespace function) and the channel estimate h it was computed from, rebuilt

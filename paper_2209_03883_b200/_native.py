@@ -104,7 +104,12 @@ RECEIVER_SYMBOLS = [
     ("ofdmr_pipeline", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_general", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
     ("ofdmr_pipeline_host", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
-    ("ofdmr_sft", i32, [vp, vp, i32, i32, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
+    ("ofdmr_sft", i32, [vp, vp, i32, i32, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                        i64]),
+    ("ofdmr_sft_detections", i32, [vp, vp, vp, vp, vp, i32, i32, i32, vp, C.c_double, vp, vp, vp, vp, vp, i64]),
+    ("ofdmr_sft_detect", i32, [vp, vp, i32, i32, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp, vp, i64]),
+    ("ofdmr_pipeline_sft", i32, [vp, vp, vp, vp, vp, vp, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp,
+                                 i64]),
     ("ofdmr_sft_estimate_noise", i32, [vp, vp, i32, i32, vp, vp, i64]),
 ]
 

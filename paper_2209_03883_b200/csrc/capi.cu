@@ -177,6 +177,20 @@ struct ofdmr_context {
     cudaEvent_t ev_done[2] = {nullptr, nullptr};
     // FPS-SFT scratch
     SftScratch sft{};
+    // FPS-SFT pipeline / sft_detect scratch (grown on demand): channel estimates of one chunk,
+    // per-frame entries and noise powers
+    struct SftPipe {
+        float2* h = nullptr;
+        int64_t cap_h = 0;  // frames
+        int32_t* k = nullptr;
+        int32_t* l = nullptr;
+        double* amp = nullptr;
+        int32_t* ne = nullptr;
+        double* s2h = nullptr;
+        double* s2u = nullptr;
+        int32_t* st = nullptr;
+        int64_t cap = 0;  // frames
+    } sp;
     // optional per-stage event timing (bench roofline): stage 0 colpass, 1 rowpass, 2 merge
     bool profiling = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof;
@@ -719,6 +733,14 @@ void ofdmr_destroy(ofdmr_context* c) {
     if (c->host_st) cudaFreeHost(c->host_st);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     sft_free(c->sft);
+    cudaFree(c->sp.h);
+    cudaFree(c->sp.k);
+    cudaFree(c->sp.l);
+    cudaFree(c->sp.amp);
+    cudaFree(c->sp.ne);
+    cudaFree(c->sp.s2h);
+    cudaFree(c->sp.s2u);
+    cudaFree(c->sp.st);
     for (auto& p : c->prof) {
         cudaEventDestroy(p.second.first);
         cudaEventDestroy(p.second.second);
@@ -1281,10 +1303,38 @@ int ofdmr_pipeline_host(ofdmr_context* c, const void* y, const void* x, const do
             OFDMR_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
         }
         OFDMR_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-        OFDMR_CUDA(cudaMallocHost(&c->host_st, sizeof(int32_t) * size_t(ch)));
+        OFDMR_CUDA(cudaMallocHost(&c->host_st, 2 * sizeof(int32_t) * size_t(ch)));
     }
+    // Chunk i+1's H2D (copy stream) and compute are enqueued before chunk i's status is read back,
+    // so the host check of one chunk overlaps the next chunk's transfers and kernels; a chunk
+    // with status bit 1 (fused-path overflow or abnormal |x|^2) is recomputed on the exact
+    // general path before its buffers are reused (chunk i+2 is enqueued only after the check).
     bool zero_cell = false;
-    int64_t idx = 0;
+    auto finish = [&](int64_t f0, int64_t nf, int b) -> int {
+        int32_t* hs = c->host_st + size_t(b) * size_t(ch);
+        OFDMR_CUDA(cudaEventSynchronize(c->ev_done[b]));
+        bool redo = false;
+        for (int64_t i = 0; i < nf; ++i) redo |= (hs[i] & 2) != 0;
+        if (redo) {
+            int rc2 = ofdmr_pipeline_general(c, c->dev_y[b], c->dev_x[b], c->dev_s2[b], kpf ? c->dev_k[b] : nullptr,
+                                             c->dev_d[b], c->dev_dp[b], c->dev_pw[b], c->dev_cnt[b], nullptr, nullptr,
+                                             c->dev_st[b], nf);
+            if (rc2) return rc2;
+            OFDMR_CUDA(cudaMemcpyAsync(d + size_t(K) * f0, c->dev_d[b], sizeof(int32_t) * K * nf,
+                                       cudaMemcpyDeviceToHost, c->stream));
+            OFDMR_CUDA(cudaMemcpyAsync(dp + size_t(K) * f0, c->dev_dp[b], sizeof(int32_t) * K * nf,
+                                       cudaMemcpyDeviceToHost, c->stream));
+            OFDMR_CUDA(cudaMemcpyAsync(pw + size_t(K) * f0, c->dev_pw[b], sizeof(float) * K * nf,
+                                       cudaMemcpyDeviceToHost, c->stream));
+            OFDMR_CUDA(cudaMemcpyAsync(cnt + f0, c->dev_cnt[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
+                                       c->stream));
+            OFDMR_CUDA(cudaMemcpyAsync(hs, c->dev_st[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, c->stream));
+            OFDMR_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        for (int64_t i = 0; i < nf; ++i) zero_cell |= (hs[i] & 1) != 0;
+        return OFDMR_OK;
+    };
+    int64_t idx = 0, prev_f0 = -1, prev_nf = 0;
     for (int64_t f0 = 0; f0 < frames; f0 += ch, ++idx) {
         const int b = int(idx & 1);
         const int64_t nf = std::min<int64_t>(ch, frames - f0);
@@ -1311,29 +1361,19 @@ int ofdmr_pipeline_host(ofdmr_context* c, const void* y, const void* x, const do
         OFDMR_CUDA(cudaMemcpyAsync(pw + size_t(K) * f0, c->dev_pw[b], sizeof(float) * K * nf, cudaMemcpyDeviceToHost,
                                    c->stream));
         OFDMR_CUDA(cudaMemcpyAsync(cnt + f0, c->dev_cnt[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, c->stream));
-        OFDMR_CUDA(cudaMemcpyAsync(c->host_st, c->dev_st[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost, c->stream));
+        OFDMR_CUDA(cudaMemcpyAsync(c->host_st + size_t(b) * size_t(ch), c->dev_st[b], sizeof(int32_t) * nf,
+                                   cudaMemcpyDeviceToHost, c->stream));
         OFDMR_CUDA(cudaEventRecord(c->ev_done[b], c->stream));
-        OFDMR_CUDA(cudaStreamSynchronize(c->stream));  // host_st is single-buffered
-        bool overflow = false;
-        for (int64_t i = 0; i < nf; ++i) {
-            zero_cell |= (c->host_st[i] & 1) != 0;
-            overflow |= (c->host_st[i] & 2) != 0;
+        if (prev_f0 >= 0) {
+            rc = finish(prev_f0, prev_nf, b ^ 1);
+            if (rc) return rc;
         }
-        if (overflow) {  // > 1024 strict maxima above eta in a half-frame: exact general path
-            int rc2 = ofdmr_pipeline_general(c, c->dev_y[b], c->dev_x[b], c->dev_s2[b], kpf ? c->dev_k[b] : nullptr,
-                                             c->dev_d[b], c->dev_dp[b], c->dev_pw[b], c->dev_cnt[b], nullptr, nullptr,
-                                             c->dev_st[b], nf);
-            if (rc2) return rc2;
-            OFDMR_CUDA(cudaMemcpyAsync(d + size_t(K) * f0, c->dev_d[b], sizeof(int32_t) * K * nf,
-                                       cudaMemcpyDeviceToHost, c->stream));
-            OFDMR_CUDA(cudaMemcpyAsync(dp + size_t(K) * f0, c->dev_dp[b], sizeof(int32_t) * K * nf,
-                                       cudaMemcpyDeviceToHost, c->stream));
-            OFDMR_CUDA(cudaMemcpyAsync(pw + size_t(K) * f0, c->dev_pw[b], sizeof(float) * K * nf,
-                                       cudaMemcpyDeviceToHost, c->stream));
-            OFDMR_CUDA(cudaMemcpyAsync(cnt + f0, c->dev_cnt[b], sizeof(int32_t) * nf, cudaMemcpyDeviceToHost,
-                                       c->stream));
-            OFDMR_CUDA(cudaStreamSynchronize(c->stream));
-        }
+        prev_f0 = f0;
+        prev_nf = nf;
+    }
+    if (prev_f0 >= 0) {
+        const int rc = finish(prev_f0, prev_nf, int((idx - 1) & 1));
+        if (rc) return rc;
     }
     OFDMR_CUDA(cudaStreamSynchronize(c->stream));
     if (zero_cell) return fail(OFDMR_ERR_CONFIG, "spectral_division: zero cell in X");
@@ -1355,16 +1395,142 @@ int ofdmr_sft_estimate_noise(ofdmr_context* c, const void* h, int32_t n, int32_t
 int ofdmr_sft(ofdmr_context* c, const void* h, int32_t n, int32_t m, const ofdmr_sft_config* cfg,
               const uint64_t* seeds, const double* sigma2, int32_t* k_out, int32_t* l_out, double* amp_out,
               int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged, double* residual,
-              int64_t frames) {
+              int32_t* status, int64_t frames) {
     if (!c || !h || !cfg || !seeds || !sigma2 || !k_out || !l_out || !amp_out || !n_entries)
         return fail(OFDMR_ERR_CONFIG, "sft: null argument");
     if (n <= 0 || m <= 0) return fail(OFDMR_ERR_CONFIG, "sft_iterate: empty grid");
     if (frames <= 0) return OFDMR_OK;
     OFDMR_CUDA(cudaSetDevice(c->device));
     std::string err;
-    const int rc = sft_run(c->sft, c->stream, static_cast<const float2*>(h), n, m, *cfg, seeds, sigma2, k_out, l_out,
-                           amp_out, n_entries, iterations, samples_used, converged, residual, frames, &c->launches, err);
+    if (status) OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
+    const int rc = sft_run(c->sft, c->stream, static_cast<const float2*>(h), n, m, *cfg, seeds, sigma2, false, k_out,
+                           l_out, amp_out, n_entries, iterations, samples_used, converged, residual, status, frames,
+                           &c->launches, err);
     if (rc) return fail(rc, err);
+    return OFDMR_OK;
+}
+
+namespace {
+
+int sft_pipe_reserve(ofdmr_context* c, int64_t frames, int64_t h_frames, int max_entries) {
+    auto& p = c->sp;
+    if (h_frames > p.cap_h) {
+        cudaFree(p.h);
+        p.h = nullptr;
+        p.cap_h = 0;
+        const size_t fc = size_t(c->cfg.n_subcarriers) * size_t(c->cfg.n_symbols);
+        OFDMR_CUDA(cudaMalloc(&p.h, sizeof(float2) * fc * size_t(h_frames)));
+        p.cap_h = h_frames;
+    }
+    if (frames > p.cap) {
+        cudaFree(p.k);
+        cudaFree(p.l);
+        cudaFree(p.amp);
+        cudaFree(p.ne);
+        cudaFree(p.s2h);
+        cudaFree(p.s2u);
+        cudaFree(p.st);
+        p = ofdmr_context::SftPipe{p.h, p.cap_h};
+        OFDMR_CUDA(cudaMalloc(&p.k, sizeof(int32_t) * 64 * size_t(frames)));
+        OFDMR_CUDA(cudaMalloc(&p.l, sizeof(int32_t) * 64 * size_t(frames)));
+        OFDMR_CUDA(cudaMalloc(&p.amp, sizeof(double) * 2 * 64 * size_t(frames)));
+        OFDMR_CUDA(cudaMalloc(&p.ne, sizeof(int32_t) * size_t(frames)));
+        OFDMR_CUDA(cudaMalloc(&p.s2h, sizeof(double) * size_t(frames)));
+        OFDMR_CUDA(cudaMalloc(&p.s2u, sizeof(double) * size_t(frames)));
+        OFDMR_CUDA(cudaMalloc(&p.st, sizeof(int32_t) * size_t(frames)));
+        p.cap = frames;
+    }
+    (void)max_entries;
+    return OFDMR_OK;
+}
+
+}  // namespace
+
+int ofdmr_sft_detections(ofdmr_context* c, const int32_t* k, const int32_t* l, const double* amp,
+                         const int32_t* n_entries, int32_t max_entries, int32_t n, int32_t m, const double* sigma2,
+                         double pfa, const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin,
+                         float* peak_power, int32_t* counts, int64_t frames) {
+    if (!c || !k || !l || !amp || !n_entries || !sigma2 || !delay_bin || !doppler_bin || !peak_power || !counts)
+        return fail(OFDMR_ERR_CONFIG, "detections_from_spectrum: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    std::string err;
+    const int rc = sft_detections(c->stream, k, l, amp, n_entries, max_entries, n, m, sigma2, pfa, k_per_frame,
+                                  c->cfg.max_targets, delay_bin, doppler_bin, peak_power, counts, frames, &c->launches,
+                                  err);
+    return rc ? fail(rc, err) : OFDMR_OK;
+}
+
+int ofdmr_sft_detect(ofdmr_context* c, const void* h, int32_t n, int32_t m, const ofdmr_sft_config* cfg,
+                     const uint64_t* seeds, const double* sigma2, const int32_t* k_per_frame, int32_t* delay_bin,
+                     int32_t* doppler_bin, float* peak_power, int32_t* counts, int32_t* status, int64_t frames) {
+    if (!c || !h || !cfg || !seeds || !sigma2 || !delay_bin || !doppler_bin || !peak_power || !counts || !status)
+        return fail(OFDMR_ERR_CONFIG, "sft_detect: null argument");
+    if (n <= 0 || m <= 0) return fail(OFDMR_ERR_CONFIG, "sft_iterate: empty grid");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    int rc = sft_pipe_reserve(c, frames, 0, cfg->max_entries);
+    if (rc) return rc;
+    OFDMR_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * size_t(frames), c->stream));
+    ofdmr_sft_config sc = *cfg;
+    sc.max_entries = 64;  // every entry reaches detections_from_spectrum (sft.cpp:467-485)
+    std::string err;
+    rc = sft_run(c->sft, c->stream, static_cast<const float2*>(h), n, m, sc, seeds, sigma2, true, c->sp.k, c->sp.l,
+                 c->sp.amp, c->sp.ne, nullptr, nullptr, nullptr, nullptr, status, frames, &c->launches, err);
+    if (rc) return fail(rc, err);
+    rc = sft_detections(c->stream, c->sp.k, c->sp.l, c->sp.amp, c->sp.ne, 64, n, m, sigma2, cfg->pfa, k_per_frame,
+                        c->cfg.max_targets, delay_bin, doppler_bin, peak_power, counts, frames, &c->launches, err);
+    return rc ? fail(rc, err) : OFDMR_OK;
+}
+
+int ofdmr_pipeline_sft(ofdmr_context* c, const void* y, const void* x_tx, const double* sigma2,
+                       const uint64_t* sft_seeds, const uint64_t* noise_seeds, const ofdmr_sft_config* cfg,
+                       const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
+                       int32_t* counts, double* sigma2_used_out, int32_t* status, int64_t frames) {
+    if (!c || !y || !x_tx || !sigma2 || !sft_seeds || !cfg || !delay_bin || !doppler_bin || !peak_power || !counts ||
+        !status)
+        return fail(OFDMR_ERR_CONFIG, "pipeline_sft: null argument");
+    if (frames <= 0) return OFDMR_OK;
+    OFDMR_CUDA(cudaSetDevice(c->device));
+    const int n = c->cfg.n_subcarriers, m = c->cfg.n_symbols, K = c->cfg.max_targets;
+    const size_t fc = size_t(n) * size_t(m);
+    // channel estimates of one chunk in scratch (<= 1 GiB)
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(frames, (int64_t(1) << 30) / int64_t(fc * 8)));
+    int rc = sft_pipe_reserve(c, chunk, chunk, cfg->max_entries);
+    if (rc) return rc;
+    ofdmr_sft_config sc = *cfg;
+    sc.max_entries = 64;
+    std::string err;
+    for (int64_t f0 = 0; f0 < frames; f0 += chunk) {
+        const int64_t nf = std::min<int64_t>(chunk, frames - f0);
+        const float2* yc = static_cast<const float2*>(y) + fc * f0;
+        const float2* xc = static_cast<const float2*>(x_tx) + fc * f0;
+        int32_t* stc = status + f0;
+        // estimate_channel (pipeline.cpp:47-58): LS / ZCP-LS / DFT-CE per the context estimator
+        rc = ofdmr_estimate_channel(c, yc, xc, c->sp.h, stc, nf);
+        if (rc) return rc;
+        // sigma_h^2 = division_noise_power(sigma2, x_tx) (pipeline.cpp:79)
+        rc = division_noise(c->stream, xc, int64_t(fc), sigma2 + f0, c->sp.s2h, nf, &c->launches, err);
+        if (rc) return fail(rc, err);
+        const double* s2u = c->sp.s2h;
+        if (noise_seeds) {  // estimate_noise mode: estimate_noise_from_slice (pipeline.cpp:97-98)
+            rc = sft_slice_noise(c->sft, c->stream, c->sp.h, n, m, noise_seeds + f0, c->sp.s2u, nf, &c->launches, err);
+            if (rc) return fail(rc, err);
+            s2u = c->sp.s2u;
+        }
+        if (sigma2_used_out)
+            OFDMR_CUDA(cudaMemcpyAsync(sigma2_used_out + f0, s2u, sizeof(double) * nf, cudaMemcpyDeviceToDevice,
+                                       c->stream));
+        // sft_iterate with SftConfig{i_max, seed, sigma2 = s2u, pfa} (pipeline.cpp:99-109)
+        rc = sft_run(c->sft, c->stream, c->sp.h, n, m, sc, sft_seeds + f0, s2u, true, c->sp.k, c->sp.l, c->sp.amp,
+                     c->sp.ne, nullptr, nullptr, nullptr, nullptr, stc, nf, &c->launches, err);
+        if (rc) return fail(rc, err);
+        // detections_from_spectrum(spec, N, M, w, sigma2, pfa, max_targets) (pipeline.cpp:110-111)
+        rc = sft_detections(c->stream, c->sp.k, c->sp.l, c->sp.amp, c->sp.ne, 64, n, m, s2u, cfg->pfa,
+                            k_per_frame ? k_per_frame + f0 : nullptr, K, delay_bin + f0 * K, doppler_bin + f0 * K,
+                            peak_power + f0 * K, counts + f0, nf, &c->launches, err);
+        if (rc) return fail(rc, err);
+    }
     return OFDMR_OK;
 }
 

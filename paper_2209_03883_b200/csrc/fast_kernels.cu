@@ -62,15 +62,9 @@ __device__ __forceinline__ void col_item(const ColArgs& a, const float2* tw, flo
             const int c = (idx & 3) * 2;
             float2 h0, h1;
             if constexpr (MODE & kLS) {
-                const float n0 = fmaf(xv[q].x, xv[q].x, xv[q].y * xv[q].y);
-                const float n1 = fmaf(xv[q].z, xv[q].z, xv[q].w * xv[q].w);
-                float i0 = 0.f, i1 = 0.f;
-                if (n0 == 0.f) zero_cell = 1; else i0 = 1.0f / n0;
-                if (n1 == 0.f) zero_cell = 1; else i1 = 1.0f / n1;
-                inv_acc += (double)i0 + (double)i1;
                 const float4 y4 = yv[q], x4 = xv[q];
-                h0 = make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
-                h1 = make_float2(fmaf(y4.z, x4.z, y4.w * x4.w) * i1, fmaf(y4.w, x4.z, -y4.z * x4.w) * i1);
+                h0 = ls_cell(y4.x, y4.y, x4.x, x4.y, inv_acc, zero_cell);
+                h1 = ls_cell(y4.z, y4.w, x4.z, x4.w, inv_acc, zero_cell);
             } else {
                 h0 = make_float2(yv[q].x, yv[q].y);
                 h1 = make_float2(yv[q].z, yv[q].w);

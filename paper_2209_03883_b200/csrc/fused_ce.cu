@@ -209,7 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell, const float2* dC, float4 (&dpre)[2]) {
         (void)f;
         const int c0 = 16 * u + 8 * rank;
-        float inv_tile = 0.f;
+        float inv_tile = 0.f, nmax = 0.f;
 #pragma unroll 4
         for (int st = 0; st < 16; ++st) {
             // stage st of this tile landed in ring slot (this thread's own 16-B slots)
@@ -221,10 +221,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             const int k = idx >> 2, c = (idx & 3) * 2;
             const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
             const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
-            // a zero (or flushed-denormal) |x|^2 gives rcp = +inf, caught once per tile below
+            // a zero / denormal (flushed) |x|^2 gives rcp = +inf and an overflowing one +inf in
+            // nmax: caught once per tile below
             const float i0 = rcp_approx(n0);
             const float i1 = rcp_approx(n1);
             inv_tile += i0 + i1;
+            nmax = fmaxf(nmax, fmaxf(n0, n1));
             const int pk = k + (k >> 5);
             const float2 r0 = make_float2(fmaf(y4.x, x4.x, y4.y * x4.y) * i0, fmaf(y4.y, x4.x, -y4.x * x4.y) * i0);
             const float2 r1 = make_float2(fmaf(y4.z, x4.z, y4.w * x4.w) * i1, fmaf(y4.w, x4.z, -y4.z * x4.w) * i1);
@@ -233,7 +235,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             // refill the slot (its values were consumed above) with the stage kRing ahead
             a_issue();
         }
-        zero_cell |= isinf(inv_tile);  // estimation.cpp:17 zero-cell check (frame flagged, status bit 0)
+        // |x|^2 outside the fp32 normal range somewhere in the tile (an exactly zero x cell,
+        // estimation.cpp:17, or a denormal / huge one the reference divides in fp64): the frame is
+        // flagged for the exact general path (status bit 1), which decides the zero-cell error
+        zero_cell |= !(inv_tile <= 3.40282347e38f) || !(nmax <= 3.40282347e38f);
         inv_acc += (double)inv_tile;  // fp32 within a tile (32 terms), fp64 across tiles
         __syncthreads();
         PH(0);
@@ -516,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 for (int i = 0; i < kf; ++i) n += s.run[i] != 0;
                 a.counts[f] = n;
                 if (a.s2h_out) a.s2h_out[f] = s.s2hs[slot];
-                if (a.status && s.zcs[slot]) atomicOr(a.status + f, 1);
+                if (a.status && s.zcs[slot]) atomicOr(a.status + f, 2);  // abnormal |x|^2: exact recompute
                 if (a.status && (s.overflow || p.overflow)) atomicOr(a.status + f, 2);
             }
         }

@@ -71,15 +71,9 @@ __global__ void __launch_bounds__(kNT) colpass_kernel(ColArgs a) {
         if (a.y != nullptr) {
             const float4 yv = __ldcs(reinterpret_cast<const float4*>(a.y + off));
             const float4 xv = __ldcs(reinterpret_cast<const float4*>(a.x + off));
-            const float n0 = fmaf(xv.x, xv.x, xv.y * xv.y);
-            const float n1 = fmaf(xv.z, xv.z, xv.w * xv.w);
-            float i0 = 0.f, i1 = 0.f;
-            if (n0 == 0.f) zero_cell = 1; else i0 = 1.0f / n0;
-            if (n1 == 0.f) zero_cell = 1; else i1 = 1.0f / n1;
-            inv_acc += (double)i0 + (double)i1;
-            // y / x = y * conj(x) / |x|^2
-            h0 = make_float2(fmaf(yv.x, xv.x, yv.y * xv.y) * i0, fmaf(yv.y, xv.x, -yv.x * xv.y) * i0);
-            h1 = make_float2(fmaf(yv.z, xv.z, yv.w * xv.w) * i1, fmaf(yv.w, xv.z, -yv.z * xv.w) * i1);
+            // y / x = y * conj(x) / |x|^2 (exact zero-cell semantics, radar_kernels.cuh ls_cell)
+            h0 = ls_cell(yv.x, yv.y, xv.x, xv.y, inv_acc, zero_cell);
+            h1 = ls_cell(yv.z, yv.w, xv.z, xv.w, inv_acc, zero_cell);
         } else {
             const float4 hv = __ldcs(reinterpret_cast<const float4*>(a.h + off));
             h0 = make_float2(hv.x, hv.y);

@@ -11,6 +11,33 @@ constexpr int kNT = 256;      // threads per CTA for the FFT passes
 constexpr int kTwLenHost = 4096;  // twiddle table length (fft_smem.cuh kTwLen)
 constexpr int kMaxK = 64;     // max detections per frame (reference default max_targets, config.hpp:33)
 
+// One LS cell h = y / x (estimation.cpp:10-21) with the reference's zero-cell semantics: only an
+// exactly zero x (both components 0, `xv == cplx(0,0)`, estimation.cpp:17) flags the frame.  |x|^2
+// is formed in fp32 on the fast path; when it falls outside the fp32 normal range (a denormal x,
+// or |x| > 1.8e19) the cell is divided in fp64 instead, as the reference does on the upcast
+// complex<double>, and its 1/|x|^2 term goes to the fp64 accumulator exactly.
+__device__ __noinline__ inline float2 ls_cell_fp64(float yr, float yi, float xr, float xi, double& inv_acc,
+                                                  int& zero_cell) {
+    if (xr == 0.f && xi == 0.f) {
+        zero_cell = 1;
+        return make_float2(0.f, 0.f);
+    }
+    const double dr = xr, di = xi;
+    const double nn = __dadd_rn(__dmul_rn(dr, dr), __dmul_rn(di, di));
+    const double iv = 1.0 / nn;
+    inv_acc += iv;
+    return make_float2(float((double(yr) * dr + double(yi) * di) * iv), float((double(yi) * dr - double(yr) * di) * iv));
+}
+__device__ __forceinline__ float2 ls_cell(float yr, float yi, float xr, float xi, double& inv_acc, int& zero_cell) {
+    const float n = fmaf(xr, xr, xi * xi);
+    if (__builtin_expect(n >= 1.17549435e-38f && n <= 3.40282347e38f, 1)) {
+        const float i = 1.0f / n;
+        inv_acc += (double)i;
+        return make_float2(fmaf(yr, xr, yi * xi) * i, fmaf(yi, xr, -yr * xi) * i);
+    }
+    return ls_cell_fp64(yr, yi, xr, xi, inv_acc, zero_cell);
+}
+
 // Column (subcarrier / delay axis) pass over tiles of C adjacent columns of one frame.
 struct ColArgs {
     const float2* y;        // LS inputs: received frame Y (N x M per frame) ...

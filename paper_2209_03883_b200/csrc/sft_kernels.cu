@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "sft_kernels.cuh"
+#include "mt64.cuh"
 
 namespace ofdmr {
 namespace {
@@ -48,7 +49,8 @@ struct SftArgs {
     int64_t* samples_used;
     int32_t* converged;
     double* residual;
-    int32_t* err;
+    int32_t* err;     // per-frame overflow flag (synchronous API), or null
+    int32_t* status;  // per-frame status, bit 2 = overflow (stream-ordered API), or null
 };
 
 __device__ __forceinline__ double2 dmul(double2 a, double2 b) {
@@ -569,7 +571,8 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
         if (a.samples_used) a.samples_used[fr] = s_samples;
         if (a.converged) a.converged[fr] = s_conv;
         if (a.residual) a.residual[fr] = s_residual;
-        a.err[fr] = s_err;
+        if (a.err) a.err[fr] = s_err;
+        if (a.status && s_err) atomicOr(a.status + fr, 4);
     }
 }
 
@@ -578,26 +581,158 @@ long long gcd_ll(long long a, long long b) {
     return a < 0 ? -a : a;
 }
 long long lcm_ll(long long a, long long b) { return a / gcd_ll(a, b) * b; }
-long long pmod_h(long long a, long long m) {
-    const long long r = a % m;
-    return r < 0 ? r + m : r;
+
+__device__ long long gcd_d(long long a, long long b) {
+    while (b) {
+        const long long t = a % b;
+        a = b;
+        b = t;
+    }
+    return a < 0 ? -a : a;
 }
-bool slope_admissible(long long v1, long long v2, long long n, long long m) {
-    const long long q = lcm_ll(n, m);
-    const long long g1 = gcd_ll(pmod_h(v1, n), n), g2 = gcd_ll(pmod_h(v2, m), m);
-    return lcm_ll(n / g1, m / g2) == q;
+// sft.cpp:46-51 slope_admissible: lcm(N / gcd(v1 mod N, N), M / gcd(v2 mod M, M)) == lcm(N, M)
+__device__ bool slope_admissible_d(long long v1, long long v2, long long n, long long m) {
+    const long long q = n / gcd_d(n, m) * m;
+    const long long r1 = ((v1 % n) + n) % n, r2 = ((v2 % m) + m) % m;
+    const long long a = n / gcd_d(r1, n), b = m / gcd_d(r2, m);
+    return a / gcd_d(a, b) * b == q;
 }
-uint64_t derive_seed(uint64_t base, uint64_t stream) {
-    uint64_t z = base + 0x9e3779b97f4a7c15ULL * (stream + 1);
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
+
+// The data-independent random draws, on the device (one thread per frame walks the frame's
+// MT19937-64 stream, bit-identical to std::mt19937_64 + Rng::uniform_int):
+//   mode 0, FPS-SFT (sft.cpp:191, 212-218): Rng(derive_seed(seed, 0x73667421)); per iteration an
+//           admissible slope (v1, v2), then offsets a1 < N, a2 < M -> draws[f][it] = {v1, v2, a1, a2}
+//   mode 1, estimate_noise_from_slice (pipeline.cpp:31-35): Rng(seed); one admissible slope
+//           -> draws[f] = {v1, v2}
+__global__ void __launch_bounds__(64) sft_draws_kernel(const uint64_t* __restrict__ seeds, int frames, int n, int m,
+                                                       int iters, int mode, int32_t* __restrict__ draws) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= frames) return;
+    uint64_t mt[mt64::kMtN];
+    mt64::mt_seed(mt, mode == 0 ? mt64::splitmix(seeds[f], 0x73667421ull) : seeds[f]);
+    mt64::MtScalar r{mt, mt64::kMtN};
+    for (int it = 0; it < iters; ++it) {
+        long long v1, v2;
+        do {
+            v1 = (long long)(1 + r.uniform_int(n > 1 ? (uint64_t)(n - 1) : 1ull));
+            v2 = (long long)(1 + r.uniform_int(m > 1 ? (uint64_t)(m - 1) : 1ull));
+        } while (!slope_admissible_d(v1, v2, n, m));
+        if (mode == 0) {
+            const long long a1 = (long long)r.uniform_int((uint64_t)n), a2 = (long long)r.uniform_int((uint64_t)m);
+            int32_t* d = draws + ((size_t)f * iters + it) * 4;
+            d[0] = (int32_t)v1;
+            d[1] = (int32_t)v2;
+            d[2] = (int32_t)a1;
+            d[3] = (int32_t)a2;
+        } else {
+            draws[2 * (size_t)f] = (int32_t)v1;
+            draws[2 * (size_t)f + 1] = (int32_t)v2;
+        }
+    }
 }
-uint64_t uniform_int(std::mt19937_64& e, uint64_t n) {
-    const uint64_t limit = UINT64_MAX - UINT64_MAX % n;
-    uint64_t v;
-    do { v = e(); } while (v >= limit);
-    return v % n;
+
+// detections_from_spectrum (sft.cpp:461-490), one warp per frame: power = |A|^2 N M (fp64, no
+// FMA: this unit is compiled -fmad=false), kept when !(power < eta) with eta = -sigma2 ln(pfa)
+// (detection_threshold with power factor 1, ln(pfa) from the host's libm), delay (N - k) mod N,
+// Doppler (l + M/2) mod M - M/2, ordered by (power desc, delay asc, Doppler asc), cut at K.
+struct SftDetArgs {
+    const int32_t* k;
+    const int32_t* l;
+    const double* amp;
+    const int32_t* n_entries;
+    int max_entries;
+    int n, m;
+    const double* sigma2;
+    double log_pfa;
+    const int32_t* k_per_frame;
+    int kmax;
+    int32_t* det_delay;
+    int32_t* det_doppler;
+    float* det_power;
+    int32_t* counts;
+    int frames;
+};
+__global__ void __launch_bounds__(128) sft_detect_kernel(SftDetArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int f = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (f >= a.frames) return;
+    const int ne = min(a.n_entries[f], a.max_entries);
+    const double eta = -a.sigma2[f] * a.log_pfa * 1.0;
+    const double nm = (double)a.n * (double)a.m;
+    const long long half = a.m / 2;
+    double pw[2];
+    long long dl[2], dp[2];
+    bool keep[2];
+    for (int t = 0; t < 2; ++t) {
+        const int i = lane + 32 * t;
+        keep[t] = false;
+        pw[t] = 0.0;
+        dl[t] = dp[t] = 0;
+        if (i < ne) {
+            const size_t o = (size_t)f * a.max_entries + i;
+            const double re = a.amp[2 * o], im = a.amp[2 * o + 1];
+            pw[t] = (re * re + im * im) * nm;
+            keep[t] = !(pw[t] < eta);
+            dl[t] = ((long long)a.n - a.k[o]) % (long long)a.n;
+            dp[t] = ((long long)a.l[o] + half) % (long long)a.m - half;
+        }
+    }
+    const int kf = a.k_per_frame ? min(a.k_per_frame[f], a.kmax) : a.kmax;
+    int kept = __popc(__ballot_sync(0xffffffffu, keep[0])) + __popc(__ballot_sync(0xffffffffu, keep[1]));
+    for (int t = 0; t < 2; ++t) {
+        int rank = 0;
+        for (int src = 0; src < 64; ++src) {  // entry src = lane' + 32 t'
+            const int sl = src & 31, st = src >> 5;
+            const double pj = __shfl_sync(0xffffffffu, st ? pw[1] : pw[0], sl);
+            const long long dj = __shfl_sync(0xffffffffu, st ? dl[1] : dl[0], sl);
+            const long long vj = __shfl_sync(0xffffffffu, st ? dp[1] : dp[0], sl);
+            const bool kj = __shfl_sync(0xffffffffu, st ? keep[1] : keep[0], sl);
+            if (kj && keep[t] && src != lane + 32 * t &&
+                (pj != pw[t] ? pj > pw[t] : (dj != dl[t] ? dj < dl[t] : vj < dp[t])))
+                ++rank;
+        }
+        if (keep[t] && rank < kf) {
+            const size_t o = (size_t)f * a.kmax + rank;
+            a.det_delay[o] = (int32_t)dl[t];
+            a.det_doppler[o] = (int32_t)dp[t];
+            a.det_power[o] = (float)pw[t];
+        }
+    }
+    const int cnt = min(kept, kf);
+    for (int i = cnt + lane; i < a.kmax; i += 32) {
+        const size_t o = (size_t)f * a.kmax + i;
+        a.det_delay[o] = 0;
+        a.det_doppler[o] = 0;
+        a.det_power[o] = 0.f;
+    }
+    if (lane == 0) a.counts[f] = cnt;
+}
+
+// division_noise_power (pipeline.cpp:18-23): sigma2 * mean(1 / |x|^2) per frame, one CTA per frame,
+// each term 1 / (re^2 + im^2) in fp64 on the upcast c64 cell (as std::norm of complex<double>),
+// summed in a fixed tree order (deterministic; the reference's sequential order is not
+// reproduced, so sigma_h^2 agrees to ~1e-15 relative, not bit for bit).
+__global__ void __launch_bounds__(256) division_noise_kernel(const float2* __restrict__ x, long long cells,
+                                                             const double* __restrict__ sigma2, double* __restrict__ out) {
+    __shared__ double red[256];
+    const int f = blockIdx.x;
+    const float2* xf = x + (size_t)f * cells;
+    double acc = 0.0;
+    for (long long i = threadIdx.x; i < cells; i += 256) {
+        const float2 v = __ldcs(xf + i);
+        const double re = v.x, im = v.y;
+        acc += 1.0 / (re * re + im * im);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double sg = sigma2[f];
+        out[f] = sg <= 0.0 ? 0.0 : sg * red[0] / (double)cells;
+    }
 }
 
 // pipeline.cpp:26-43 estimate_noise_from_slice: one CTA per frame; the slice through (0, 0)
@@ -653,184 +788,27 @@ cudaError_t ensure(T** p, int64_t& cap, int64_t need) {
 
 }  // namespace
 
-int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const uint64_t* seeds,
-                    double* sigma2_out, int64_t frames, int64_t* launches, std::string& err) {
-    auto pow2 = [](int v) { return v >= 2 && (v & (v - 1)) == 0; };
-    if (!pow2(n) || !pow2(m)) { err = "estimate_noise_from_slice: N and M must be powers of two on the GPU path"; return OFDMR_ERR_CONFIG; }
-    const int q = int(lcm_ll(n, m));
-    if (q > 2048 || q < 16) { err = "estimate_noise_from_slice: Q = lcm(N, M) must lie in [16, 2048]"; return OFDMR_ERR_CONFIG; }
-    if (frames > 0x7fffffff) { err = "estimate_noise_from_slice: too many frames"; return OFDMR_ERR_CONFIG; }
-    std::vector<int32_t> slopes(size_t(frames) * 2);
-    for (int64_t f = 0; f < frames; ++f) {  // Rng(seed), pipeline.cpp:31-35
-        std::mt19937_64 e(seeds[f]);
-        long long v1, v2;
-        do {
-            v1 = (long long)(1 + uniform_int(e, n > 1 ? n - 1 : 1));
-            v2 = (long long)(1 + uniform_int(e, m > 1 ? m - 1 : 1));
-        } while (!slope_admissible(v1, v2, n, m));
-        slopes[2 * f] = int32_t(v1);
-        slopes[2 * f + 1] = int32_t(v2);
-    }
-    std::vector<double2> twf(q / 2);
-    for (int k = 0; k < q / 2; ++k) {
-        const double ang = (double)(-1) * kTwoPiD * (double)k / (double)q;
-        twf[k] = make_double2(std::cos(ang), std::sin(ang));
-    }
-    int64_t cap_q = s.cap_q;
-    cudaError_t e = ensure(&s.draws, s.cap_draws, int64_t(slopes.size()));
-    if (e == cudaSuccess) e = ensure(&s.tw_fft, cap_q, q);
-    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    s.cap_q = int(std::min<int64_t>(cap_q, s.cap_q ? s.cap_q : cap_q));
-    e = cudaMemcpyAsync(s.draws, slopes.data(), sizeof(int32_t) * slopes.size(), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(s.tw_fft, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice, st);
-    s.tw_q = 0;  // tw_fft rewritten here: sft_run rebuilds its tables on its next call
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host vectors go out of scope
-    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    int logq = 0;
-    while ((1 << logq) < q) ++logq;
-    const size_t smem = sizeof(double2) * q + sizeof(double) * q;
-    slice_noise_kernel<<<unsigned(frames), kSftNT, smem, st>>>(h, n, m, q, logq, s.draws, s.tw_fft, sigma2_out);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    if (launches) ++*launches;
-    return OFDMR_OK;
-}
-
 void sft_free(SftScratch& s) {
     cudaFree(s.draws);
+    cudaFree(s.seeds);
     cudaFree(s.sigma2);
-    cudaFree(s.tw_ref);
-    cudaFree(s.tw_fft);
     cudaFree(s.err);
+    for (auto& t : s.tables) {
+        cudaFree(t.second.first);
+        cudaFree(t.second.second);
+    }
     s = SftScratch{};
 }
 
 namespace {
 
-// Persistent host worker pool for the per-frame draws: run(nt, fn) calls fn(t, nt) for t < nt,
-// t = 0 on the caller, and returns when all are done.  One run at a time (contexts on several host
-// threads queue); the pool lives for the process (never destroyed: no joins at exit).
-class HostPool {
-   public:
-    static HostPool& get() {
-        static HostPool* pool = new HostPool;
-        return *pool;
-    }
-    int size() const { return (int)workers_.size() + 1; }
-    void run(int nt, const std::function<void(int, int)>& fn) {
-        std::lock_guard<std::mutex> run_lock(run_mu_);
-        nt = std::max(1, std::min(nt, size()));
-        if (nt == 1) {
-            fn(0, 1);
-            return;
-        }
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            fn_ = &fn;
-            active_ = nt - 1;
-            pending_ = nt - 1;
-            nt_ = nt;
-            ++gen_;
-        }
-        cv_.notify_all();
-        fn(0, nt);
-        std::unique_lock<std::mutex> lk(mu_);
-        done_cv_.wait(lk, [&] { return pending_ == 0; });
-        fn_ = nullptr;
-    }
-
-   private:
-    HostPool() {
-        const int n = (int)std::max(1u, std::thread::hardware_concurrency()) - 1;
-        for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
-        for (auto& w : workers_) w.detach();
-    }
-    void loop(int id) {
-        uint64_t seen = 0;
-        for (;;) {
-            const std::function<void(int, int)>* f;
-            int nt;
-            {
-                std::unique_lock<std::mutex> lk(mu_);
-                cv_.wait(lk, [&] { return gen_ != seen; });
-                seen = gen_;
-                if (id > active_) continue;
-                f = fn_;
-                nt = nt_;
-            }
-            (*f)(id, nt);
-            std::lock_guard<std::mutex> lk(mu_);
-            if (--pending_ == 0) done_cv_.notify_one();
-        }
-    }
-    std::mutex run_mu_, mu_;
-    std::condition_variable cv_, done_cv_;
-    std::vector<std::thread> workers_;
-    const std::function<void(int, int)>* fn_ = nullptr;
-    int active_ = 0, pending_ = 0, nt_ = 1;
-    uint64_t gen_ = 0;
-};
-
-}  // namespace
-
-int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const ofdmr_sft_config& cfg,
-            const uint64_t* seeds, const double* sigma2, int32_t* k_out, int32_t* l_out, double* amp_out,
-            int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged, double* residual,
-            int64_t frames, int64_t* launches, std::string& err) {
-    auto pow2 = [](int v) { return v >= 2 && (v & (v - 1)) == 0; };
-    if (!pow2(n) || !pow2(m)) { err = "sft: N and M must be powers of two on the GPU path"; return OFDMR_ERR_CONFIG; }
-    const int q = int(lcm_ll(n, m));
-    if (q > 2048 || q < 16) { err = "sft: Q = lcm(N, M) must lie in [16, 2048] on the GPU path"; return OFDMR_ERR_CONFIG; }
-    if (cfg.i_max < 0 || cfg.max_entries < 1 || cfg.max_entries > 64 || frames > 65535 * 32) {
-        err = "sft: bad i_max / max_entries";
-        return OFDMR_ERR_CONFIG;
-    }
-    const int i_max = cfg.i_max;
-    // host-side data-independent draws (sft.cpp:191, 212-218)
-    std::vector<int32_t> draws(size_t(frames) * size_t(i_max > 0 ? i_max : 1) * 4);
-    auto draw_frames = [&](int64_t f0, int64_t f1) {
-        for (int64_t f = f0; f < f1; ++f) {
-            std::mt19937_64 e(derive_seed(seeds[f], 0x73667421));
-            for (int it = 0; it < i_max; ++it) {
-                long long v1, v2;
-                do {
-                    v1 = (long long)(1 + uniform_int(e, n > 1 ? n - 1 : 1));
-                    v2 = (long long)(1 + uniform_int(e, m > 1 ? m - 1 : 1));
-                } while (!slope_admissible(v1, v2, n, m));
-                const long long a1 = (long long)uniform_int(e, n), a2 = (long long)uniform_int(e, m);
-                int32_t* d = &draws[(size_t(f) * i_max + it) * 4];
-                d[0] = int32_t(v1);
-                d[1] = int32_t(v2);
-                d[2] = int32_t(a1);
-                d[3] = int32_t(a2);
-            }
-        }
-    };
-    // one engine per frame (seeding + first twist dominate): frames split over a persistent pool of
-    // host threads (spawning threads per call cost more than the draws); every frame's draws are
-    // independent of the split
-    {
-        const int nt = (int)std::min<int64_t>(HostPool::get().size(), frames / 64 + 1);
-        HostPool::get().run(nt, [&](int t, int nt_run) {
-            draw_frames(frames * t / nt_run, frames * (t + 1) / nt_run);
-        });
-    }
-    const double2* old_ref = s.tw_ref;
-    const double2* old_fft = s.tw_fft;
-    int64_t cap_s2 = s.cap_frames, cap_err = s.cap_frames, cap_q = s.cap_q, cap_q2 = s.cap_q;
-    cudaError_t e = ensure(&s.draws, s.cap_draws, int64_t(draws.size()));
-    if (e == cudaSuccess) e = ensure(&s.sigma2, cap_s2, frames);
-    if (e == cudaSuccess) e = ensure(&s.err, cap_err, frames);
-    if (e == cudaSuccess) e = ensure(&s.tw_ref, cap_q, q);
-    if (e == cudaSuccess) e = ensure(&s.tw_fft, cap_q2, q);
-    if (e != cudaSuccess) { err = std::string("sft: allocation: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    s.cap_frames = std::min(cap_s2, cap_err);
-    s.cap_q = int(std::min(cap_q, cap_q2));
-    e = cudaMemcpyAsync(s.draws, draws.data(), sizeof(int32_t) * draws.size(), cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(s.sigma2, sigma2, sizeof(double) * frames, cudaMemcpyHostToDevice, st);
-    // twiddle tables: reference rotation table (sft.cpp:29-44) and radix-2 table (oracle.c),
-    // built and uploaded only when Q changed or the buffers were reallocated
-    if (e == cudaSuccess && (s.tw_q != q || s.tw_ref != old_ref || s.tw_fft != old_fft)) {
+// Twiddle tables of one Q, built once on the host with the reference's / oracle's libm calls and
+// kept for the life of the context (never rewritten, so stream-ordered launches may use them):
+// first = the rotation table of sft.cpp:29-44 (exact std::polar resync every 256), second = the
+// radix-2 butterfly twiddles of oracle.c fft_pow2.
+int sft_tables(SftScratch& s, int q, const double2** tw_ref, const double2** tw_fft, std::string& err) {
+    auto it = s.tables.find(q);
+    if (it == s.tables.end()) {
         std::vector<double2> twr(q), twf(q / 2);
         const double sa = -kTwoPiD / double(q);
         double cr = 1.0, ci = 0.0;
@@ -850,11 +828,74 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
             const double ang = (double)(-1) * kTwoPiD * (double)k / (double)q;
             twf[k] = make_double2(std::cos(ang), std::sin(ang));
         }
-        e = cudaMemcpyAsync(s.tw_ref, twr.data(), sizeof(double2) * q, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(s.tw_fft, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice, st);
-        s.tw_q = e == cudaSuccess ? q : 0;
+        double2 *dr = nullptr, *df = nullptr;
+        cudaError_t e = cudaMalloc(&dr, sizeof(double2) * q);
+        if (e == cudaSuccess) e = cudaMalloc(&df, sizeof(double2) * (q / 2 > 0 ? q / 2 : 1));
+        if (e == cudaSuccess) e = cudaMemcpy(dr, twr.data(), sizeof(double2) * q, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(df, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(dr);
+            cudaFree(df);
+            err = std::string("sft: twiddle tables: ") + cudaGetErrorString(e);
+            return OFDMR_ERR_CUDA;
+        }
+        it = s.tables.emplace(q, std::make_pair(dr, df)).first;
     }
-    if (e != cudaSuccess) { err = std::string("sft: upload: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    *tw_ref = it->second.first;
+    *tw_fft = it->second.second;
+    return OFDMR_OK;
+}
+
+int upload_seeds(SftScratch& s, cudaStream_t st, const uint64_t* seeds, int64_t frames, std::string& err) {
+    cudaError_t e = ensure(&s.seeds, s.cap_seeds, frames);
+    // pageable source: the copy is staged before cudaMemcpyAsync returns (the host array may go)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(s.seeds, seeds, sizeof(uint64_t) * frames, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        err = std::string("sft: seeds: ") + cudaGetErrorString(e);
+        return OFDMR_ERR_CUDA;
+    }
+    return OFDMR_OK;
+}
+
+}  // namespace
+
+int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const ofdmr_sft_config& cfg,
+            const uint64_t* seeds, const double* sigma2, bool sigma2_on_device, int32_t* k_out, int32_t* l_out,
+            double* amp_out, int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged,
+            double* residual, int32_t* status, int64_t frames, int64_t* launches, std::string& err) {
+    auto pow2 = [](int v) { return v >= 2 && (v & (v - 1)) == 0; };
+    if (!pow2(n) || !pow2(m)) { err = "sft: N and M must be powers of two on the GPU path"; return OFDMR_ERR_CONFIG; }
+    const int q = int(lcm_ll(n, m));
+    if (q > 2048 || q < 16) { err = "sft: Q = lcm(N, M) must lie in [16, 2048] on the GPU path"; return OFDMR_ERR_CONFIG; }
+    if (cfg.i_max < 0 || cfg.max_entries < 1 || cfg.max_entries > 64 || frames > 65535 * 32) {
+        err = "sft: bad i_max / max_entries";
+        return OFDMR_ERR_CONFIG;
+    }
+    const int i_max = cfg.i_max;
+    const int iters = i_max > 0 ? i_max : 1;
+    int rc = upload_seeds(s, st, seeds, frames, err);
+    if (rc) return rc;
+    cudaError_t e = ensure(&s.draws, s.cap_draws, frames * iters * 4);
+    int64_t cap_s2 = s.cap_frames, cap_err = s.cap_frames;
+    if (e == cudaSuccess && !sigma2_on_device) e = ensure(&s.sigma2, cap_s2, frames);
+    if (e == cudaSuccess && !status) e = ensure(&s.err, cap_err, frames);
+    if (e != cudaSuccess) { err = std::string("sft: allocation: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    s.cap_frames = std::min(sigma2_on_device ? cap_err : cap_s2, status ? cap_s2 : cap_err);
+    if (i_max > 0) {
+        sft_draws_kernel<<<unsigned((frames + 63) / 64), 64, 0, st>>>(s.seeds, int(frames), n, m, i_max, 0, s.draws);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) { err = std::string("sft: draws: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+        if (launches) ++*launches;
+    }
+    const double* s2 = sigma2;
+    if (!sigma2_on_device) {
+        e = cudaMemcpyAsync(s.sigma2, sigma2, sizeof(double) * frames, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) { err = std::string("sft: upload: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+        s2 = s.sigma2;
+    }
+    const double2 *tw_ref = nullptr, *tw_fft = nullptr;
+    rc = sft_tables(s, q, &tw_ref, &tw_fft, err);
+    if (rc) return rc;
 
     SftArgs a{};
     a.h = h;
@@ -871,9 +912,9 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
     a.decimation = cfg.decimation;
     a.max_entries = cfg.max_entries;
     a.draws = s.draws;
-    a.sigma2 = s.sigma2;
-    a.tw_ref = s.tw_ref;
-    a.tw_fft = s.tw_fft;
+    a.sigma2 = s2;
+    a.tw_ref = tw_ref;
+    a.tw_fft = tw_fft;
     a.k_out = k_out;
     a.l_out = l_out;
     a.amp_out = amp_out;
@@ -882,7 +923,8 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
     a.samples_used = samples_used;
     a.converged = converged;
     a.residual = residual;
-    a.err = s.err;
+    a.err = status ? nullptr : s.err;
+    a.status = status;
     const size_t smem = sizeof(double2) * (3 * size_t(q) + size_t(q)) + sizeof(double) * q + sizeof(int) * 2 * q;
     e = cudaFuncSetAttribute(sft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) { err = std::string("sft: smem attr: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
@@ -890,13 +932,87 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
     e = cudaGetLastError();
     if (e != cudaSuccess) { err = std::string("sft: launch: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
     if (launches) ++*launches;
-    // overflow flags (comps > kMaxComp) — stream-ordered check requires a sync
+    if (status) return OFDMR_OK;  // stream-ordered: overflow reported in status bit 2
+    // no status array: the reference's exception needs the flags now (synchronous)
     std::vector<int32_t> ef(frames);
     e = cudaMemcpyAsync(ef.data(), s.err, sizeof(int32_t) * frames, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { err = std::string("sft: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
     for (int64_t f = 0; f < frames; ++f)
-        if (ef[f]) { err = "sft: more than 128 accepted tones in a frame"; return OFDMR_ERR_CONFIG; }
+        if (ef[f]) { err = "sft: more than 128 accepted tones or 64 entries in a frame"; return OFDMR_ERR_CONFIG; }
+    return OFDMR_OK;
+}
+
+int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const uint64_t* seeds,
+                    double* sigma2_out, int64_t frames, int64_t* launches, std::string& err) {
+    auto pow2 = [](int v) { return v >= 2 && (v & (v - 1)) == 0; };
+    if (!pow2(n) || !pow2(m)) { err = "estimate_noise_from_slice: N and M must be powers of two on the GPU path"; return OFDMR_ERR_CONFIG; }
+    const int q = int(lcm_ll(n, m));
+    if (q > 2048 || q < 16) { err = "estimate_noise_from_slice: Q = lcm(N, M) must lie in [16, 2048]"; return OFDMR_ERR_CONFIG; }
+    if (frames > 0x7fffffff) { err = "estimate_noise_from_slice: too many frames"; return OFDMR_ERR_CONFIG; }
+    int rc = upload_seeds(s, st, seeds, frames, err);
+    if (rc) return rc;
+    cudaError_t e = ensure(&s.draws, s.cap_draws, frames * 4);
+    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    const double2 *tw_ref = nullptr, *tw_fft = nullptr;
+    rc = sft_tables(s, q, &tw_ref, &tw_fft, err);
+    if (rc) return rc;
+    sft_draws_kernel<<<unsigned((frames + 63) / 64), 64, 0, st>>>(s.seeds, int(frames), n, m, 1, 1, s.draws);
+    int logq = 0;
+    while ((1 << logq) < q) ++logq;
+    const size_t smem = sizeof(double2) * q + sizeof(double) * q;
+    slice_noise_kernel<<<unsigned(frames), kSftNT, smem, st>>>(h, n, m, q, logq, s.draws, tw_fft, sigma2_out);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+    if (launches) *launches += 2;
+    return OFDMR_OK;
+}
+
+int sft_detections(cudaStream_t st, const int32_t* k, const int32_t* l, const double* amp, const int32_t* n_entries,
+                   int max_entries, int n, int m, const double* sigma2, double pfa, const int32_t* k_per_frame, int kmax,
+                   int32_t* det_delay, int32_t* det_doppler, float* det_power, int32_t* counts, int64_t frames,
+                   int64_t* launches, std::string& err) {
+    if (!(pfa > 0.0 && pfa <= 1.0)) { err = "threshold: pfa must lie in (0,1]"; return OFDMR_ERR_CONFIG; }
+    if (max_entries < 1 || max_entries > 64 || kmax < 1 || kmax > 64) {
+        err = "detections_from_spectrum: max_entries and max_targets must lie in [1, 64] on the GPU path";
+        return OFDMR_ERR_CONFIG;
+    }
+    for (int64_t f0 = 0; f0 < frames; f0 += 4 * 65535) {
+        const int64_t nf = std::min<int64_t>(4 * 65535, frames - f0);
+        SftDetArgs a{};
+        a.k = k + f0 * max_entries;
+        a.l = l + f0 * max_entries;
+        a.amp = amp + 2 * f0 * max_entries;
+        a.n_entries = n_entries + f0;
+        a.max_entries = max_entries;
+        a.n = n;
+        a.m = m;
+        a.sigma2 = sigma2 + f0;
+        a.log_pfa = std::log(pfa);
+        a.k_per_frame = k_per_frame ? k_per_frame + f0 : nullptr;
+        a.kmax = kmax;
+        a.det_delay = det_delay + f0 * kmax;
+        a.det_doppler = det_doppler + f0 * kmax;
+        a.det_power = det_power + f0 * kmax;
+        a.counts = counts + f0;
+        a.frames = int(nf);
+        sft_detect_kernel<<<unsigned((nf + 3) / 4), 128, 0, st>>>(a);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { err = std::string("detections_from_spectrum: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+        if (launches) ++*launches;
+    }
+    return OFDMR_OK;
+}
+
+int division_noise(cudaStream_t st, const float2* x, int64_t cells, const double* sigma2, double* out, int64_t frames,
+                   int64_t* launches, std::string& err) {
+    for (int64_t f0 = 0; f0 < frames; f0 += 65535) {
+        const int64_t nf = std::min<int64_t>(65535, frames - f0);
+        division_noise_kernel<<<unsigned(nf), 256, 0, st>>>(x + f0 * cells, cells, sigma2 + f0, out + f0);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { err = std::string("division_noise_power: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+        if (launches) ++*launches;
+    }
     return OFDMR_OK;
 }
 

@@ -374,6 +374,7 @@ class Receiver:
         pmap = (torch.empty(F, self.cfg.n_prime, self.cfg.m_prime, dtype=torch.float32, device=self.device)
                 if want_map else None)
         st = torch.empty(F, dtype=torch.int32, device=self.device)
+        self.last_status = st  # per-frame status of the last pipeline call (bit 0 zero cell, bit 1 overflow)
         self._stream()
         _check(self._lib.ofdmr_pipeline(self._h, y.data_ptr(), x.data_ptr(), s2.data_ptr(),
                                         k.data_ptr() if k is not None else None, d.delay_bin.data_ptr(),
@@ -381,10 +382,12 @@ class Receiver:
                                         d.sigma2_h.data_ptr(), pmap.data_ptr() if pmap is not None else None,
                                         st.data_ptr(), F))
         if check:
-            self._raise_status(st)
             over = torch.nonzero(st & 2).flatten()
+            self.last_recomputed = int(over.numel())  # frames re-run on the exact general path
             if over.numel():
-                # candidate-list overflow on the fused path: recompute those frames exactly
+                # status bit 1: candidate-list overflow on the fused path, or an |x|^2 outside the fp32
+                # normal range (zero / denormal / huge x cell): recompute those frames exactly on the
+                # general path, whose status then decides the zero-cell error (bit 0)
                 idx = over
                 sub = self._dets(idx.numel())
                 sub.sigma2_h = torch.empty(idx.numel(), dtype=torch.float64, device=self.device)
@@ -400,6 +403,8 @@ class Receiver:
                 d.peak_power[idx] = sub.peak_power
                 d.counts[idx] = sub.counts
                 d.sigma2_h[idx] = sub.sigma2_h
+                st[idx] = st2
+            self._raise_status(st)
         return d, pmap
 
     def pipeline_raw(self, y: torch.Tensor, x: torch.Tensor, s2: torch.Tensor, k: torch.Tensor | None,
@@ -436,16 +441,36 @@ class Receiver:
         _check(self._lib.ofdmr_pipeline_host(self._h, y_ptr, x_ptr, s2_ptr, k_ptr, d_ptr, dp_ptr, pw_ptr, cnt_ptr,
                                              frames))
 
+    @staticmethod
+    def _sft_config(i_max, detect_threshold, pfa, decimation, frac_tol, amp_tol, max_entries):
+        c = _native.OfdmrSftConfig()
+        c.i_max, c.detect_threshold, c.pfa, c.decimation = i_max, detect_threshold, pfa, decimation
+        c.frac_tol, c.amp_tol, c.max_entries = frac_tol, amp_tol, max_entries
+        return c
+
+    def _f64_dev(self, v, F: int) -> torch.Tensor:
+        if isinstance(v, torch.Tensor):
+            return v.to(self.device, torch.float64).reshape(-1).expand(F).contiguous()
+        return torch.as_tensor(np.broadcast_to(np.asarray(v, np.float64), (F,)).copy()).to(self.device)
+
+    @staticmethod
+    def _raise_sft_status(status: torch.Tensor) -> None:
+        if bool((status & 1).any()):
+            raise ConfigError("spectral_division: zero cell in X")
+        if bool((status & 4).any()):
+            raise ConfigError("sft: more than 128 accepted tones or 64 entries in a frame")
+
     def sft(self, h, seeds, sigma2, i_max: int = 10, detect_threshold: float = 0.0, pfa: float = 1e-2,
-            decimation: int = 8, frac_tol: float = 0.25, amp_tol: float = 0.35, max_entries: int = 64):
-        """sft_iterate (sft.cpp:185-459) over a batch; returns dict of device tensors."""
+            decimation: int = 8, frac_tol: float = 0.25, amp_tol: float = 0.35, max_entries: int = 64,
+            stream_ordered: bool = False):
+        """sft_iterate (sft.cpp:185-459) over a batch; returns dict of device tensors.  The slope /
+        offset draws run on the device from the per-frame seeds.  stream_ordered=True: no host sync,
+        out["status"] bit 2 flags a frame beyond the on-chip limits (else ConfigError here)."""
         h, single = _batched(_as_grid(h, self.device))
         F, n, m = h.shape
         seeds = np.ascontiguousarray(np.broadcast_to(np.asarray(seeds, np.uint64), (F,)))
         s2 = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma2, np.float64), (F,)))
-        c = _native.OfdmrSftConfig()
-        c.i_max, c.detect_threshold, c.pfa, c.decimation = i_max, detect_threshold, pfa, decimation
-        c.frac_tol, c.amp_tol, c.max_entries = frac_tol, amp_tol, max_entries
+        c = self._sft_config(i_max, detect_threshold, pfa, decimation, frac_tol, amp_tol, max_entries)
         z = dict(device=self.device)
         out = dict(k=torch.zeros(F, max_entries, dtype=torch.int32, **z),
                    l=torch.zeros(F, max_entries, dtype=torch.int32, **z),
@@ -455,13 +480,88 @@ class Receiver:
                    samples_used=torch.zeros(F, dtype=torch.int64, **z),
                    converged=torch.zeros(F, dtype=torch.int32, **z),
                    residual=torch.zeros(F, dtype=torch.float64, **z))
+        if stream_ordered:
+            out["status"] = torch.zeros(F, dtype=torch.int32, **z)
         self._stream()
         _check(self._lib.ofdmr_sft(self._h, h.data_ptr(), n, m, C.byref(c), seeds.ctypes.data, s2.ctypes.data,
                                    out["k"].data_ptr(), out["l"].data_ptr(), out["amp"].data_ptr(),
                                    out["n_entries"].data_ptr(), out["iterations"].data_ptr(),
                                    out["samples_used"].data_ptr(), out["converged"].data_ptr(),
-                                   out["residual"].data_ptr(), F))
+                                   out["residual"].data_ptr(),
+                                   out["status"].data_ptr() if stream_ordered else None, F))
         return out
+
+    def sft_detections(self, out: dict, n: int, m: int, sigma2, pfa: float = 1e-2, k_per_frame=None) -> Detections:
+        """detections_from_spectrum (sft.cpp:461-490) on the device for a batch of sft() outputs."""
+        F = out["n_entries"].shape[0]
+        me = out["k"].shape[1]
+        s2 = self._f64_dev(sigma2, F)
+        k = self._k(k_per_frame, F)
+        d = self._dets(F)
+        self._stream()
+        _check(self._lib.ofdmr_sft_detections(self._h, out["k"].data_ptr(), out["l"].data_ptr(), out["amp"].data_ptr(),
+                                              out["n_entries"].data_ptr(), me, n, m, s2.data_ptr(), pfa,
+                                              k.data_ptr() if k is not None else None, d.delay_bin.data_ptr(),
+                                              d.doppler_bin.data_ptr(), d.peak_power.data_ptr(), d.counts.data_ptr(), F))
+        d.sigma2_h = s2
+        return d
+
+    def sft_detect(self, h, seeds, sigma2, pfa: float = 1e-2, i_max: int = 10, decimation: int = 8,
+                   frac_tol: float = 0.25, amp_tol: float = 0.35, detect_threshold: float = 0.0, k_per_frame=None,
+                   check: bool = True) -> Detections:
+        """sft_detect (sft.cpp:492-500) over a batch: sft_iterate with sigma2 / pfa, then
+        detections_from_spectrum, all on the device (ofdmr_sft_detect)."""
+        h, _ = _batched(_as_grid(h, self.device))
+        F, n, m = h.shape
+        seeds = np.ascontiguousarray(np.broadcast_to(np.asarray(seeds, np.uint64), (F,)))
+        s2 = self._f64_dev(sigma2, F)
+        c = self._sft_config(i_max, detect_threshold, pfa, decimation, frac_tol, amp_tol, 64)
+        k = self._k(k_per_frame, F)
+        d = self._dets(F)
+        st = torch.empty(F, dtype=torch.int32, device=self.device)
+        self._stream()
+        _check(self._lib.ofdmr_sft_detect(self._h, h.data_ptr(), n, m, C.byref(c), seeds.ctypes.data, s2.data_ptr(),
+                                          k.data_ptr() if k is not None else None, d.delay_bin.data_ptr(),
+                                          d.doppler_bin.data_ptr(), d.peak_power.data_ptr(), d.counts.data_ptr(),
+                                          st.data_ptr(), F))
+        self.last_status = st
+        if check:
+            self._raise_sft_status(st)
+        d.sigma2_h = s2
+        return d
+
+    def pipeline_sft(self, y, x_tx, sigma2, sft_seeds, noise_seeds=None, i_max: int = 10, decimation: int = 8,
+                     pfa: float | None = None, k_per_frame=None, check: bool = True) -> Detections:
+        """The FPS-SFT branch of run_pipeline (pipeline.cpp:97-113) on a batch of frames, one
+        C-ABI call (ofdmr_pipeline_sft): estimate_channel -> division_noise_power -> [estimate_noise_
+        from_slice when noise_seeds is given] -> sft_iterate -> detections_from_spectrum.
+        sft_seeds[f] / noise_seeds[f] are run_pipeline's derive_seed(seed, 0x736674) /
+        derive_seed(seed, 0x6e6573).  Detections.sigma2_h = PipelineResult::sigma2_used."""
+        y, _ = _batched(_as_grid(y, self.device))
+        x, _ = _batched(_as_grid(x_tx, self.device))
+        if y.shape != x.shape:
+            raise ConfigError("spectral_division: shape mismatch")
+        self._shape_check(y)
+        F = y.shape[0]
+        s2 = self._f64_dev(sigma2, F)
+        ss = np.ascontiguousarray(np.broadcast_to(np.asarray(sft_seeds, np.uint64), (F,)))
+        ns = None if noise_seeds is None else np.ascontiguousarray(
+            np.broadcast_to(np.asarray(noise_seeds, np.uint64), (F,)))
+        c = self._sft_config(i_max, 0.0, self.cfg.pfa if pfa is None else pfa, decimation, 0.25, 0.35, 64)
+        k = self._k(k_per_frame, F)
+        d = self._dets(F)
+        d.sigma2_h = torch.empty(F, dtype=torch.float64, device=self.device)
+        st = torch.empty(F, dtype=torch.int32, device=self.device)
+        self._stream()
+        _check(self._lib.ofdmr_pipeline_sft(self._h, y.data_ptr(), x.data_ptr(), s2.data_ptr(), ss.ctypes.data,
+                                            ns.ctypes.data if ns is not None else None, C.byref(c),
+                                            k.data_ptr() if k is not None else None, d.delay_bin.data_ptr(),
+                                            d.doppler_bin.data_ptr(), d.peak_power.data_ptr(), d.counts.data_ptr(),
+                                            d.sigma2_h.data_ptr(), st.data_ptr(), F))
+        self.last_status = st
+        if check:
+            self._raise_sft_status(st)
+        return d
 
     def estimate_noise_from_slice(self, h, seeds) -> torch.Tensor:
         """estimate_noise_from_slice (pipeline.cpp:26-43), the FPS-SFT detector's estimate-noise
@@ -604,28 +704,42 @@ def sft_iterate(h, seed: int, sigma2: float = 0.0, i_max: int = 10, detect_thres
 
 def detections_from_spectrum(spec: SparseSpectrum, n: int, m: int, sigma2: float, pfa: float, max_targets: int,
                              rc: RadarConfig | None = None) -> list[Detection]:
-    """sft.cpp:461-490 (host, fp64)."""
+    """sft.cpp:461-490 through the device entry point (ofdmr_sft_detections): threshold, bin
+    mapping and the (power desc, delay, Doppler) ranking in fp64 on the GPU; peak_power is the
+    fp64 |A|^2 N M of the matching entry, physics as sft.cpp:476-479 when a RadarConfig is given."""
+    if sigma2 < 0:
+        raise ConfigError("threshold: sigma2 must be >= 0")
+    if not (0 < pfa <= 1):
+        raise ConfigError("threshold: pfa must lie in (0,1]")
+    if not spec.entries or max_targets <= 0:
+        return []
+    if len(spec.entries) > 64 or max_targets > 64:
+        raise ConfigError("detections_from_spectrum: at most 64 entries / targets on the GPU path")
+    dev = _device()
+    r = _ctx(16, 16, 16, 16, WINDOW_RECT, EST_LS, 0, max_targets)
+    ne = len(spec.entries)
+    out = {"k": torch.tensor([[e[0] for e in spec.entries]], dtype=torch.int32, device=dev),
+           "l": torch.tensor([[e[1] for e in spec.entries]], dtype=torch.int32, device=dev),
+           "amp": torch.tensor([[[e[2].real, e[2].imag] for e in spec.entries]], dtype=torch.float64, device=dev),
+           "n_entries": torch.tensor([ne], dtype=torch.int32, device=dev)}
+    d = r.sft_detections(out, n, m, [sigma2], pfa)
     nm = float(n) * float(m)
-    eta = detection_threshold(sigma2, pfa, 1.0)
+    amp = {(int(k) % n, int(l) % m): a for k, l, a in spec.entries}
     dets = []
-    for k, l, a in spec.entries:
-        power = (a.real * a.real + a.imag * a.imag) * nm
-        if power < eta:
-            continue
-        half = m // 2
-        dets.append(Detection((n - k) % n, (l + half) % m - half, power))
-    dets.sort(key=lambda d: (-d.peak_power, d.delay_bin, d.doppler_bin))
-    dets = dets[:max_targets]
-    if rc is not None:
-        c = KSPEED_OF_LIGHT
-        for d in dets:
-            d.range_m = c * d.delay_bin / (2.0 * n * rc.df_hz)
-            d.velocity_mps = c * d.doppler_bin / (2.0 * 77e9 * m * rc.symbol_time)
+    for db, vb, _ in d.frame(0):
+        a = amp[((n - db) % n, vb % m)]
+        det = Detection(db, vb, (a.real * a.real + a.imag * a.imag) * nm)
+        if rc is not None:
+            det.range_m = KSPEED_OF_LIGHT * db / (2.0 * n * rc.df_hz)
+            det.velocity_mps = KSPEED_OF_LIGHT * vb / (2.0 * 77e9 * m * rc.symbol_time)
+        dets.append(det)
     return dets
 
 
 def sft_detect(h, seed: int, sigma2: float, pfa: float, max_targets: int, **kw) -> list[Detection]:
-    """sft.cpp:492-500."""
+    """sft.cpp:492-500 (one grid): sft_iterate + detections_from_spectrum on the device."""
     h = _as_grid(h, _device())
-    spec = sft_iterate(h, seed, sigma2, pfa=pfa, **kw)
-    return detections_from_spectrum(spec, h.shape[0], h.shape[1], sigma2, pfa, max_targets)
+    n, m = h.shape
+    r = _ctx(16, 16, 16, 16, WINDOW_RECT, EST_LS, 0, max_targets)
+    d = r.sft_detect(h, [seed], [sigma2], pfa=pfa, **kw)
+    return [Detection(a, b, c) for a, b, c in d.frame(0)]

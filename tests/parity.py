@@ -19,13 +19,19 @@ def strict_local_maxima(p: np.ndarray, eta: float):
     return idx[order], vals[order], nb.max(0)
 
 
-def classify(gpu_dets, ref_dets, pmap: np.ndarray, eta: float, k: int) -> str:
-    """'ok' (identical bins and order), 'tie' (difference explained by a near-tie of the
-    oracle's own fp64 values), or 'fail'."""
+def _rel(a: float, b: float) -> float:
+    den = max(abs(a), abs(b))
+    return abs(a - b) / den if den > 0 else 0.0
+
+
+def classify_detail(gpu_dets, ref_dets, pmap: np.ndarray, eta: float, k: int):
+    """(verdict, margin, reason): verdict 'ok' (identical bins and order), 'tie' (every
+    difference is explained by a near-tie of the oracle's own fp64 values: margin = the
+    largest relative fp64 gap among the deciding comparisons, < TIE_REL) or 'fail'."""
     g = [(int(a), int(b)) for a, b, _ in gpu_dets]
     r = [(int(a), int(b)) for a, b, _ in ref_dets]
     if g == r:
-        return "ok"
+        return "ok", None, ""
     rows, cols = pmap.shape
     idx, vals, nbmax = strict_local_maxima(pmap, -np.inf)
     half = cols // 2
@@ -36,27 +42,35 @@ def classify(gpu_dets, ref_dets, pmap: np.ndarray, eta: float, k: int) -> str:
     flat = pmap.ravel()
     nbf = nbmax.ravel()
     suspicious = set(g) ^ set(r)
+    worst, reasons = 0.0, []
+    above = vals[vals >= eta * (1 - TIE_REL)]
     for d in suspicious:
         c = cell(d)
         v = flat[c]
-        near_nb = abs(v - nbf[c]) <= TIE_REL * max(v, nbf[c])
-        near_eta = abs(v - eta) <= TIE_REL * max(abs(eta), v)
-        # near the K-th / (K+1)-th rank boundary among maxima >= eta
-        above = vals[vals >= eta * (1 - TIE_REL)]
-        near_rank = False
+        cands = {"neighbour": _rel(v, nbf[c]), "threshold": _rel(v, eta)}
         if len(above) > k - 1:
             kth = above[min(k - 1, len(above) - 1)]
             nxt = above[k] if len(above) > k else eta
-            near_rank = abs(kth - nxt) <= TIE_REL * kth and (abs(v - kth) <= TIE_REL * kth or abs(v - nxt) <= TIE_REL * kth)
-        if not (near_nb or near_eta or near_rank):
-            return "fail"
+            cands["rank_k"] = max(_rel(kth, nxt), min(_rel(v, kth), _rel(v, nxt)))
+        why, m = min(cands.items(), key=lambda kv: kv[1])
+        if m > TIE_REL:
+            return "fail", m, f"{d}: smallest fp64 margin {m:.3g} ({why})"
+        worst = max(worst, m)
+        reasons.append(f"{d}:{why}")
     if not suspicious:  # same set, different order: adjacent ranks must be near-equal
-        for i, (a, b) in enumerate(zip(g, r)):
+        for a, b in zip(g, r):
             if a != b:
-                va, vb = flat[cell(a)], flat[cell(b)]
-                if abs(va - vb) > TIE_REL * max(va, vb):
-                    return "fail"
-    return "tie"
+                m = _rel(flat[cell(a)], flat[cell(b)])
+                if m > TIE_REL:
+                    return "fail", m, f"order {a} vs {b}: margin {m:.3g}"
+                worst = max(worst, m)
+                reasons.append(f"order {a}/{b}")
+    return "tie", worst, ";".join(reasons)
+
+
+def classify(gpu_dets, ref_dets, pmap: np.ndarray, eta: float, k: int) -> str:
+    """'ok', 'tie' or 'fail' (see classify_detail)."""
+    return classify_detail(gpu_dets, ref_dets, pmap, eta, k)[0]
 
 
 def powers_close(gpu_dets, ref_dets) -> bool:

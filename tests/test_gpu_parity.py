@@ -185,6 +185,47 @@ def test_pipeline_zero_cell_raises(cuda):
             rx.pipeline_host(fb.y, x, fb.sigma2)
 
 
+def test_pipeline_zero_cell_raises_on_fused_path(cuda):
+    # the fused DFT-CE kernel flags abnormal |x|^2 for exact recompute (status bit 1); the exact
+    # path then raises the zero-cell ConfigError (estimation.cpp:17)
+    cfg = configs.CFG4
+    fb = gen.frames(cfg, 0, 3)
+    x = fb.x.copy()
+    x[1, 700, 200] = 0
+    with Receiver.from_config(cfg) as rx:
+        with pytest.raises(ConfigError):
+            rx.pipeline(fb.y, x, fb.sigma2, k_per_frame=fb.n_targets)
+        with pytest.raises(ConfigError):
+            rx.pipeline_host(fb.y, x, fb.sigma2, fb.n_targets)
+
+
+@pytest.mark.parametrize("cfg", [configs.CFG4, configs.CFG0], ids=["fused", "ls"])
+def test_denormal_and_huge_x_cells_are_divided_not_rejected(cuda, cfg):
+    # estimation.cpp:17 rejects only an exactly zero x cell; a denormal x (|x|^2 underflows fp32)
+    # or a huge one (|x|^2 overflows fp32) is divided like the reference's complex<double>
+    fb = gen.frames(cfg, 0, 2)
+    y, x = fb.y.copy(), fb.x.copy()
+    x[0, 100, 3] = np.complex64(1e-39 + 0.5e-39j)   # fp32 denormals
+    y[0, 100, 3] = x[0, 100, 3] * np.complex64(0.5 - 0.25j)
+    x[1, 5, 7] = np.complex64(3e19 - 1e19j)           # |x|^2 ~ 1e39 > FLT_MAX
+    y[1, 5, 7] = x[1, 5, 7] * np.complex64(0.3 + 0.1j)
+    kf = fb.n_targets if cfg.per_frame_k else None
+    rc = _rc(cfg)
+    with Receiver.from_config(cfg) as rx:
+        dets, _ = rx.pipeline(y, x, fb.sigma2, k_per_frame=kf)  # no ConfigError
+        s2h = dets.sigma2_h.cpu().numpy()
+        hd, hv, hp, hc = rx.pipeline_host(y, x, fb.sigma2, kf)
+        h = rx.spectral_division(y, x).cpu().numpy()
+    assert h[0, 100, 3] == pytest.approx(0.5 - 0.25j, rel=1e-6)
+    assert h[1, 5, 7] == pytest.approx(0.3 + 0.1j, rel=1e-6)
+    for f in range(2):
+        k = int(kf[f]) if kf is not None else cfg.max_targets
+        ref, ref_s2h, _, _ = O.receive_frame(rc, y[f], x[f], float(fb.sigma2[f]), k)
+        assert abs(s2h[f] - ref_s2h) <= 1e-6 * ref_s2h, (f, s2h[f], ref_s2h)
+        assert [(a, b) for a, b, _ in dets.frame(f)] == [(a, b) for a, b, _ in ref]
+        assert [(int(hd[f, i]), int(hv[f, i])) for i in range(int(hc[f]))] == [(a, b) for a, b, _ in ref]
+
+
 @pytest.mark.parametrize("f0,F", [(0, 8), (100, 64)])
 def test_sft_cfg3_subset_matches_oracle(cuda, f0, F):
     # 64 more frames (512 slope draws): the lattice decode's shortcut over long solution
