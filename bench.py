@@ -146,6 +146,85 @@ def cpu_reference_rate(cfg, y, x, s2, kf, frames: int, threads: int):
     return frames / dt, kind, dt
 
 
+def timed_parity_sample(cfg, y, x, s2, kf, dets, nf: int, count: int):
+    """`count` evenly spaced frames of the timed batch: their detections (from the timed step)
+    against the reference's receiver on the same c64 frames (oracle/_ref, all host threads)."""
+    import torch
+
+    import oracle as O
+
+    idx = np.linspace(0, nf - 1, count).round().astype(np.int64)
+    it = torch.from_numpy(idx).to(y.device)
+    yh = np.ascontiguousarray(y[it].cpu().numpy())
+    xh = np.ascontiguousarray(x[it].cpu().numpy())
+    sh = np.ascontiguousarray(s2[it].cpu().numpy(), np.float64)
+    kh = np.ascontiguousarray(kf[it].cpu().numpy(), np.int32)
+    K = cfg.max_targets
+    d = np.zeros((count, K), np.int64)
+    v = np.zeros((count, K), np.int64)
+    w = np.zeros((count, K))
+    cnt = np.zeros(count, np.int64)
+    if O.ref_available():
+        rc = O.ref().ref_receive_batch(cfg.n, cfg.m, cfg.n_prime, cfg.m_prime, cfg.estimator, cfg.n_cp, cfg.window,
+                                       cfg.pfa, yh.ctypes.data, xh.ctypes.data, sh.ctypes.data, count,
+                                       kh.ctypes.data, K, d.ctypes.data, v.ctypes.data, w.ctypes.data,
+                                       cnt.ctypes.data, os.cpu_count() or 1)
+        kind = "reference"
+        if rc:
+            return {"error": f"ref_receive_batch rc={rc}"}
+    else:
+        rcfg = O.rx_config(cfg.n, cfg.m, cfg.n_prime, cfg.m_prime, cfg.estimator, cfg.n_cp, cfg.window, cfg.pfa)
+        d, v, w, cnt, _, _ = O.receive_batch(rcfg, yh, xh, sh, K, kh)
+        kind = "port"
+    gd = dets.delay_bin[it].cpu().numpy()
+    gv = dets.doppler_bin[it].cpu().numpy()
+    gp = dets.peak_power[it].cpu().numpy()
+    gc = dets.counts[it].cpu().numpy()
+    fail, worst = 0, 0.0
+    for i in range(count):
+        same = int(gc[i]) == int(cnt[i]) and all(
+            int(gd[i, j]) == int(d[i, j]) and int(gv[i, j]) == int(v[i, j]) for j in range(int(cnt[i])))
+        fail += not same
+        for j in range(min(int(gc[i]), int(cnt[i]))):
+            worst = max(worst, abs(float(gp[i, j]) - w[i, j]) / w[i, j])
+    return {"checked": count, "fail": fail, "max_power_rel_err": worst, "against": kind,
+            "frames": "evenly spaced over the timed batch, detections of the last timed step"}
+
+
+def reference_inputs(cfg, count: int, seed: int = 20220908):
+    """Frames for the CPU legs built by the reference's own generator (oracle/_ref:
+    make_random_frame + apply_channel, ref_make_frame_pair), not by this repo's libraries.
+    Scenes follow cfg4 (QPSK, 3-8 targets, velocity U[-80, 80] m/s, SNR U[-10, 20] dB) with the
+    range drawn inside the reference's model-validity bound (c Tcp / 2 = 39 m at N_cp = 128,
+    channel.cpp:51-63; DFT-CE with L = 128 keeps only those ranges anyway).  The
+    receiver's CPU cost per frame does not depend on the scene.  Returns None when oracle/_ref is
+    not built."""
+    import oracle as O
+
+    if not O.ref_available():
+        return None
+    rng = np.random.default_rng(seed)
+    rmax = 3.0e8 * (cfg.n_cp / (cfg.n * cfg.df_hz)) / 2.0
+    ys, xs, s2, kt = [], [], [], []
+    for f in range(count):
+        k = int(rng.integers(cfg.targets_min, cfg.targets_max + 1))
+        r = rng.uniform(cfg.range_lo, 0.95 * rmax, k)
+        v = rng.uniform(cfg.vel_lo, cfg.vel_hi, k)
+        snr = float(rng.uniform(cfg.snr_lo_db, cfg.snr_hi_db))
+        y, x, sg = O.ref_make_frame_pair(cfg.n, cfg.m, cfg.df_hz, 77e9, cfg.n_cp, cfg.qam, r, v, snr, seed + f)
+        ys.append(y.astype(np.complex64))
+        xs.append(x.astype(np.complex64))
+        s2.append(sg)
+        kt.append(k)
+    return np.stack(ys), np.stack(xs), np.array(s2), np.array(kt, np.int32)
+
+
+def cpu_sample_size(threads: int) -> int:
+    """Frames per CPU measurement (cpu_baseline leg and --impl reference alike): two frames per
+    host thread, so every thread stays busy through one frame's tail."""
+    return max(8, 2 * threads)
+
+
 def make_pool(cfg, first: int, count: int):
     from paper_2209_03883_b200 import gen
 
@@ -156,14 +235,16 @@ def run_reference(args, cfg, rank: int):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    pool = make_pool(cfg, 0, max(64, min(args.pool, 256)))
-    sample = min(len(pool.y), max(8, 2 * threads))
-    # tile the pool so one step is a bounded sample of the same workload
-    reps = -(-sample // len(pool.y))
-    y = np.ascontiguousarray(np.concatenate([pool.y] * reps)[:sample])
-    x = np.ascontiguousarray(np.concatenate([pool.x] * reps)[:sample])
-    s2 = np.concatenate([pool.sigma2] * reps)[:sample]
-    kf = np.concatenate([pool.n_targets] * reps)[:sample]
+    sample = cpu_sample_size(threads)
+    ref_in = reference_inputs(cfg, sample)
+    if ref_in is not None:
+        y, x, s2, kf = ref_in
+        src = "generated by the reference's own make_random_frame + apply_channel (oracle/_ref)"
+    else:
+        pool = make_pool(cfg, 0, sample)
+        y, x, s2, kf = pool.y, pool.x, pool.sigma2, pool.n_targets
+        src = "generated by the seeded C++ port of the reference generator"
+    y, x = np.ascontiguousarray(y), np.ascontiguousarray(x)
     for _ in range(args.warmup):
         cpu_reference_rate(cfg, y, x, s2, kf, sample, threads)
     rates, kind = [], "reference"
@@ -178,8 +259,9 @@ def run_reference(args, cfg, rank: int):
         "config": {"workload": "cfg4: LS -> DFT-CE(L=128) -> Hamming 2-D periodogram 1024x256 -> top-K_f",
                    "frames_per_step": sample, "threads": threads},
         "cpu_baseline": {"value": val, "unit": "frames/s", "cores": threads, "kind": kind,
-                         "sample": f"{sample} cfg4 frames per step (tiled from {len(pool.y)} distinct), median of "
-                                   f"{args.steps} steps; reference sources + substitute FFT (FFTW3 absent)"},
+                         "sample": f"{sample} distinct cfg4-shaped frames per step ({src}), one frame per host "
+                                   f"thread at a time, median of {args.steps} steps; reference sources + substitute "
+                                   f"FFT (plan-cached radix-4, FFTW3 absent)"},
         "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -378,12 +460,13 @@ def main():
 
     rx = Receiver.from_config(cfg, chunk_frames=args.chunk, device=local)
     dets = rx._dets(nf)
+    status = torch.zeros(nf, dtype=torch.int32, device=dev)
     K = cfg.max_targets
     gather = DetectionGather(F, K, rank, world, dev)
 
     def step():
         rx._stream()
-        rx.pipeline_raw(y, x, s2, kf, dets, nf)
+        rx.pipeline_raw(y, x, s2, kf, dets, nf, status)
         if world > 1:  # detections of every shard to rank 0 (NCCL all_gather of padded records)
             gather(dets.delay_bin, dets.doppler_bin, dets.peak_power, dets.counts)
 
@@ -418,6 +501,17 @@ def main():
         dist.all_reduce(lt, op=dist.ReduceOp.SUM)
         launches = int(lt.item())
     value = F / (ms / 1e3)
+
+    # ---- what was timed: status flags of the last timed step, and a sample of its detections
+    # against the reference receiver (oracle/_ref) on the same c64 frames
+    st_h = status.cpu().numpy()
+    timed_status = {"frames": int(nf), "zero_cell": int(((st_h & 1) != 0).sum()),
+                    "recompute_flagged": int(((st_h & 2) != 0).sum()),
+                    "note": "status of the last timed step; recompute-flagged frames would be re-run on the "
+                            "exact path by the public API (ofdmr_pipeline_general)"}
+    parity_sample = None
+    if rank == 0 and not args.no_cpu:
+        parity_sample = timed_parity_sample(cfg, y, x, s2, kf, dets, nf, min(64, nf))
 
     # ---- per-stage kernel time (separate profiling pass; not part of `value`)
     rx.set_profiling(True)
@@ -472,10 +566,11 @@ def main():
         per._stream()
         per._lib.ofdmr_periodogram(per._h, h.data_ptr(), pm.data_ptr(), pf)
         pst, _ = per.get_profile()
-        ptraffic = load_traffic("fused_pg2", pf)
+        ptraffic = load_traffic("fused_pg3", pf)
         periodogram = {"frames": pf, "frames_per_s": pf / (pms / 1e3), "ms_per_step": pms,
-                       "kernel": "fused_pg2 (persistent, warp-specialised: column and row warps concurrent, "
-                                 "H tiles and G row blocks by TMA (3-D 32-row rounds), 8-CTA frame groups, double-buffered G in L2)",
+                       "kernel": "fused_pg3 (persistent, warp-specialised, delay IFFT split 32 x 32 across the L2 "
+                                 "exchange: column warps DFT_32 + twiddle on TMA H tiles, row warps DFT_32 + FFT_256 on "
+                                 "bulk-copied 64 KiB m-blocks; 8-CTA frame groups, double-buffered G in L2; packed FP32x2)",
                        "algorithmic_bytes_per_frame": pbytes, "achieved_gbs": pach, "frac": pach / hbm,
                        "traffic": ptraffic["bytes_per_launch"] if ptraffic else None,
                        "traffic_source": ptraffic["source"] if ptraffic else None,
@@ -544,12 +639,14 @@ def main():
         for i in range(2):
             db[i].copy_(hb[i], non_blocking=True)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for r in range(8):
-            with torch.cuda.stream(cs[r & 1]):
-                db[r & 1].copy_(hb[r & 1], non_blocking=True)
-        torch.cuda.synchronize()
-        link = 8 * (256 << 20) / (time.perf_counter() - t0) / 1e9
+        link = 0.0
+        for _ in range(3):  # best of three 8 GiB probes (a short probe under-measured: frac_of_link > 1)
+            t0 = time.perf_counter()
+            for r in range(32):
+                with torch.cuda.stream(cs[r & 1]):
+                    db[r & 1].copy_(hb[r & 1], non_blocking=True)
+            torch.cuda.synchronize()
+            link = max(link, 32 * (256 << 20) / (time.perf_counter() - t0) / 1e9)
         e2e["h2d_link_gbs"] = link
         e2e["h2d_achieved_gbs"] = e2e["h2d_bytes_per_step"] / et / 1e9
         e2e["frac_of_link"] = e2e["h2d_achieved_gbs"] / link
@@ -559,19 +656,26 @@ def main():
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         threads = os.cpu_count() or 1
-        sample = min(P, max(8, threads)) if P >= 8 else P
-        ysm = np.ascontiguousarray(pool.y[:sample])
-        xsm = np.ascontiguousarray(pool.x[:sample])
-        cpu_reference_rate(cfg, ysm, xsm, pool.sigma2, pool.n_targets, min(sample, threads), threads)  # warm
+        sample = cpu_sample_size(threads)
+        ref_in = reference_inputs(cfg, sample)
+        if ref_in is not None:
+            ysm, xsm, s2sm, ksm = ref_in
+            src = "generated by the reference's own make_random_frame + apply_channel (oracle/_ref)"
+        else:
+            ysm, xsm, s2sm, ksm = (np.ascontiguousarray(np.concatenate([a] * (-(-sample // P)))[:sample])
+                                   for a in (pool.y, pool.x, pool.sigma2, pool.n_targets))
+            src = "the seeded C++ port of the reference generator"
+        cpu_reference_rate(cfg, ysm, xsm, s2sm, ksm, min(sample, threads), threads)  # warm
         reps_c, rates, kind = 0, [], "reference"
         t_start = time.perf_counter()
         while reps_c < 5 and time.perf_counter() - t_start < 20:
-            r, kind, _ = cpu_reference_rate(cfg, ysm, xsm, pool.sigma2, pool.n_targets, sample, threads)
+            r, kind, _ = cpu_reference_rate(cfg, ysm, xsm, s2sm, ksm, sample, threads)
             rates.append(r)
             reps_c += 1
         cpu = {"value": float(np.median(rates)), "unit": "frames/s", "cores": threads, "kind": kind,
-               "sample": f"{sample} distinct cfg4 frames x {reps_c} repeats (median), one frame per host thread; "
-                         "reference sources + substitute FFT (FFTW3 absent)"}
+               "sample": f"{sample} distinct cfg4-shaped frames ({src}) x {reps_c} repeats (median), one frame per "
+                         "host thread at a time, the same sample size as --impl reference; reference sources + "
+                         "substitute FFT (plan-cached radix-4, FFTW3 absent)"}
 
     configs_out = None
     if not args.no_extra and rank == 0 and world == 1:
@@ -592,6 +696,7 @@ def main():
                        "frames": F, "frames_per_rank": nf, "parallelism": f"frame-shard x{world}",
                        "l2": "inputs larger than L2 (32 GiB resident, no reuse between steps)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "timed_status": timed_status, "parity_sample": parity_sample,
             "periodogram_2d": periodogram, "configs": configs_out,
         }
         print(json.dumps(out), flush=True)

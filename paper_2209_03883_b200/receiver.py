@@ -408,12 +408,13 @@ class Receiver:
         return d, pmap
 
     def pipeline_raw(self, y: torch.Tensor, x: torch.Tensor, s2: torch.Tensor, k: torch.Tensor | None,
-                     d: Detections, frames: int) -> None:
-        """Pre-allocated, check-free pipeline call for timing loops (no host sync)."""
+                     d: Detections, frames: int, status: torch.Tensor | None = None) -> None:
+        """Pre-allocated pipeline call for timing loops (no host sync); per-frame status flags go to
+        `status` when given (checked by the caller after the timed region)."""
         _check(self._lib.ofdmr_pipeline(self._h, y.data_ptr(), x.data_ptr(), s2.data_ptr(),
                                         k.data_ptr() if k is not None else None, d.delay_bin.data_ptr(),
                                         d.doppler_bin.data_ptr(), d.peak_power.data_ptr(), d.counts.data_ptr(),
-                                        None, None, None, frames))
+                                        None, None, status.data_ptr() if status is not None else None, frames))
 
     def pipeline_host(self, y: np.ndarray, x_tx: np.ndarray, sigma2: np.ndarray, k_per_frame=None):
         """Host-buffer pipeline (H2D / D2H inside the call).  Returns numpy records."""
