@@ -57,7 +57,7 @@ cudaError_t launch_ofdm(bool inverse, const float2* in, float2* out, int n, int 
 cudaError_t launch_noise_select(const float* p, int64_t count, double pf, double* sigma2_out, int64_t frames,
                                 void* scratch, int sms, cudaStream_t st, int64_t* launches);
 cudaError_t launch_fused_pg2(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st);
-cudaError_t launch_fused_pg3(const Pg2Args& a, bool hamming, int groups, cudaStream_t st);
+cudaError_t launch_fused_pg3(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st);
 int fused_pg3_max_groups();
 size_t fused_pg3_counter_ints(int groups);
 size_t fused_pg3_scratch_elems(int groups);
@@ -893,7 +893,7 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
             cudaError_t e;
             {
                 StageTimer t(c, 0, c->stream);
-                e = launch_fused_pg3(pa, win, int(std::min<int64_t>(c->pg3_groups, nf)), c->stream);
+                e = launch_fused_pg3(pa, win, int(std::min<int64_t>(c->pg3_groups, nf)), c->pg3_groups, c->stream);
             }
             if (e != cudaSuccess) return cuda_fail(e, "fused_pg3");
             ++c->launches;

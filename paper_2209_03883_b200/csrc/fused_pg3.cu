@@ -42,8 +42,25 @@ namespace ofdmr {
 namespace {
 
 constexpr int kN = 1024, kM = 256;
+#ifdef PG3_NOMATH
+constexpr bool PG3_MATH_ON = false;  // diagnostic: data movement and synchronisation only (wrong maps)
+#else
+constexpr bool PG3_MATH_ON = true;
+#endif
+// PG3_TMA_STORE: the column side stages each tile's C values in the H tile buffer it just
+// consumed and writes them to G with ONE TMA tensor store per tile (instead of 32 STG.64 per
+// column warp); the freed LSU queue and the smem of the dropped twiddle table (column twiddles
+// then come through the read-only cache) pay for a third H tile buffer.
+#ifndef PG3_TMA_STORE
+#define PG3_TMA_STORE 0
+#endif
+// P stores: 0 = 16 scalar streaming stores per row-lane, 1 = same with .cg, 2 = staged through the
+// row's smem slot and written as 16-B vectors (4 per row-lane)
+#ifndef PG3_PSTORE
+#define PG3_PSTORE 0
+#endif
 #ifndef PG3_HBUF
-#define PG3_HBUF 2
+#define PG3_HBUF (PG3_TMA_STORE ? 3 : 2)
 #endif
 constexpr int kGrp = 8;                      // CTAs per frame group
 constexpr int kTC = 4;                       // symbols per column tile = column warps
@@ -61,7 +78,9 @@ constexpr unsigned kBlockBytes = kBlockElems * 8u;   // 64 KiB
 struct __align__(1024) Pg3Smem {
     float2 htile[kHBuf][kN * kTC];   // [k][4 symbols], 32-B swizzle (1024-B aligned)
     float2 gbuf[2][kBlockElems];     // m-block slab [l][j ^ (l & 31)], then rows [q][l]
+#if !PG3_TMA_STORE
     float2 tw[1024];                 // tw[m * 32 + j] = W_1024^{j m}
+#endif
     unsigned long long mbar_h[kHBuf];
     unsigned long long mbar_g[2];
 };
@@ -103,6 +122,16 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
+// shared -> global TMA tensor store of a staged tile (bulk-group completion)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<unsigned long long>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void bar_col() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kColWarps) : "memory"); }
 __device__ __forceinline__ void bar_row() { asm volatile("bar.sync 2, %0;" ::"n"(32 * kRowWarps) : "memory"); }
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -131,7 +160,7 @@ __device__ unsigned long long g_pg3_phase[8];
 
 template <bool HAMMING>
 __global__ void __launch_bounds__(kThreads, 1)
-    fused_pg3_kernel(Pg2Args a, const __grid_constant__ CUtensorMap hmap) {
+    fused_pg3_kernel(Pg2Args a, const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap gmap) {
     extern __shared__ unsigned char smem_raw[];
     // 1024-B alignment as an offset from the __shared__ symbol (keeps LDS/STS addressing)
     const unsigned s_pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -140,7 +169,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool is_col = warp < kColWarps;
     const int ridx = is_col ? warp : warp - kColWarps;
     const int g = blockIdx.x / kGrp, rank = blockIdx.x % kGrp, ng = gridDim.x / kGrp;
+#if !PG3_TMA_STORE
     for (int i = tid; i < 1024; i += kThreads) s.tw[i] = a.tw1024_t[i];
+#else
+    (void)gmap;
+#endif
     if (tid == 0) {
         for (int b = 0; b < kHBuf; ++b) mbar_init(&s.mbar_h[b], 1);
         mbar_init(&s.mbar_g[0], 1);
@@ -161,8 +194,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto issue_tile = [&](int tn) {
             const int b = tn % kHBuf;
             mbar_expect_tx(&s.mbar_h[b], kTileBytes);
+#ifdef PG3_H_SAME  // diagnostic: every tile from frame g (H stays in L2)
+            tma_load_3d(s.htile[b], &hmap, kTC * (kGrp * (tn % kTpf) + rank), 0, 4 * g, &s.mbar_h[b],
+                        policy_evict_first());
+#else
             tma_load_3d(s.htile[b], &hmap, kTC * (kGrp * (tn % kTpf) + rank), 0, 4 * (g + (tn / kTpf) * ng), &s.mbar_h[b],
                         policy_evict_first());
+#endif
         };
         if (cw0)
             for (int tn = 0; tn < kHBuf && tn < ntiles; ++tn) issue_tile(tn);
@@ -177,7 +215,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 twc[kTwReg ? 32 : 1];
         if constexpr (kTwReg) {
 #pragma unroll
-            for (int m = 0; m < 32; ++m) twc[m] = make_float2(s.tw[m * 32 + lane].x, -s.tw[m * 32 + lane].y);
+            for (int m = 0; m < 32; ++m) {
+#if PG3_TMA_STORE
+                const float2 w = __ldg(a.tw1024_t + m * 32 + lane);
+#else
+                const float2 w = s.tw[m * 32 + lane];
+#endif
+                twc[m] = make_float2(w.x, -w.y);
+            }
         }
         for (int t = 0; t < ntiles; ++t) {
             const int i = t / kTpf, u = t % kTpf;
@@ -189,8 +234,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int r = 0; r < 32; ++r) v[r] = s.htile[t % kHBuf][hoff + 32 * kTC * r];
             bar_col();  // every column is in registers: the tile buffer is free
             if (cw0) {
+#if !PG3_TMA_STORE
                 if (t + kHBuf < ntiles) issue_tile(t + kHBuf);
+#endif
                 if (t >= kTpf && u == 0) {
+#if PG3_TMA_STORE
+                    bulk_wait_all();  // frame i - 1's tensor stores performed
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
                     __threadfence();
                     atomicAdd(col_cnt + ((i - 1) % kGBuf) * kCntStride, 1);  // G of frame i - 1 complete
                 }
@@ -199,14 +250,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int r = 0; r < 32; ++r) v[r] = cscale(v[r], wkr[r]);
             }
+#ifndef PG3_NOMATH
             dft32<true>(v);  // v[m] = sum_i x[lane + 32 i] W_32^{-m i}
+#endif
 #pragma unroll
-            for (int m = 1; m < 32; ++m) {
+            for (int m = 1; m < (PG3_MATH_ON ? 32 : 1); ++m) {
                 float2 w;
                 if constexpr (kTwReg) {
                     w = twc[m];
                 } else {
+#if PG3_TMA_STORE
+                    w = __ldg(a.tw1024_t + m * 32 + lane);
+#else
                     w = s.tw[m * 32 + lane];
+#endif
                     w.y = -w.y;
                 }
                 v[m] = cmul(v[m], w);
@@ -219,15 +276,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
             }
             P3(2);
+#if PG3_TMA_STORE
+            {
+                // stage C[lane][m] at [m][cw][lane ^ (c & 31)] in the consumed H buffer, then one TMA
+                // store of the [32 m][4 c][32 j] box to G[m][c][j] (rows verbatim: the XOR stays)
+                float2* stg = s.htile[t % kHBuf];
+#pragma unroll
+                for (int m = 0; m < 32; ++m) stg[(m * kTC + cw) * 32 + (lane ^ (c & 31))] = v[m];
+                bar_col();
+                if (cw0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    tma_store_3d(&gmap, stg, 0, kTC * (kGrp * u + rank), (kGBuf * g + i % kGBuf) * 32);
+                    bulk_wait_read_all();  // the staged tile has been read: the buffer takes the next H tile
+                    if (t + kHBuf < ntiles) issue_tile(t + kHBuf);
+                }
+            }
+#else
             // C[lane][m] -> G[m][c][lane ^ (c & 31)]: one 256-B line pair per m (a 16-B pair variant
             // with lane shuffles measured slower: 973 k vs 1.0 M frames/s)
             float2* gcol = a.gscratch + (size_t)(kGBuf * g + i % kGBuf) * kN * kM + (size_t)c * 32 + (lane ^ (c & 31));
 #pragma unroll
             for (int m = 0; m < 32; ++m) __stcg(gcol + (size_t)m * kBlockElems, v[m]);
+#endif
             P3(3);
         }
         bar_col();
         if (ntiles > 0 && cw0) {
+#if PG3_TMA_STORE
+            bulk_wait_all();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
             __threadfence();
             atomicAdd(col_cnt + ((nfr - 1) % kGBuf) * kCntStride, 1);  // last frame
         }
@@ -292,7 +370,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             float2 v[32];
 #pragma unroll
             for (int jj = 0; jj < 32; ++jj) v[jj] = gb[l * 32 + (jj ^ lane)];
+#ifndef PG3_NOMATH
             dft32<true>(v);  // v[q] = X[m + 32 q][l]
+#endif
             bar_row();       // every slab element is in registers
 #pragma unroll
             // rows q: [q][l ^ 8 (q & 1)] (odd rows shifted by half a bank row: the two rows a
@@ -311,21 +391,75 @@ __global__ void __launch_bounds__(kThreads, 1)
                     x[r] = sl[(j ^ hx) + 16 * r];
                     if (HAMMING) x[r] = cscale(x[r], wlr[r]);
                 }
+#ifndef PG3_NOMATH
                 dft16<false>(x);
 #pragma unroll
                 for (int t1 = 1; t1 < 16; ++t1) x[t1] = cmul(x[t1], twr[t1]);
+#endif
                 __syncwarp();
 #pragma unroll
                 for (int t1 = 0; t1 < 16; ++t1) sl[t1 * 16 + (j ^ t1 ^ hx)] = x[t1];
                 __syncwarp();
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) x[jj] = sl[j * 16 + (jj ^ j ^ hx)];
+#ifndef PG3_NOMATH
                 dft16<false>(x);
+#endif
                 const int n = m + 32 * q;
+#ifdef PG3_P_SAME  // diagnostic: every frame's map written over frame g's (P stays in L2)
+                float* prow = a.p + ((size_t)g * kN + n) * kM;
+#else
                 float* prow = a.p + ((size_t)(g + i * ng) * kN + n) * kM;
+#endif
+#if defined(PG3_NO_P)
+                if (cnorm(x[0]) == 12345.f) prow[j] = 0.f;  // diagnostic: no P traffic
+#elif PG3_PSTORE == 3
+                {
+                    // |X|^2 / (N M), fftshifted, into this row's free slot (h = 1 rows 64 B in: the two
+                    // rows of a warp on disjoint banks), then ONE bulk copy of the 1 KiB row to P by the
+                    // half-warp's first lane; the copies' smem reads are waited for before the slot is
+                    // refilled (end of the round)
+                    float* pf = reinterpret_cast<float*>(sl) + 16 * h;
+                    __syncwarp();
+#pragma unroll
+                    for (int t2 = 0; t2 < 16; ++t2) pf[(j + 16 * t2 + 128) & 255] = cnorm(x[t2]) * a.scale;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (j == 0) {
+                        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 1024;" ::"l"(prow),
+                                     "r"(smem_u32(pf))
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                }
+#elif PG3_PSTORE == 2
+                {
+                    // |X|^2 / (N M) with the Doppler fftshift into this row's (now free) slot as fp32
+                    // (h = 1 rows XOR 16 words: the two rows of a warp on disjoint banks), then the
+                    // half-warp streams the 1 KiB row as 16-B vectors: 4 STG.128 per lane
+                    float* pf = reinterpret_cast<float*>(sl);
+                    __syncwarp();
+#pragma unroll
+                    for (int t2 = 0; t2 < 16; ++t2) pf[((j + 16 * t2 + 128) & 255) ^ (16 * h)] = cnorm(x[t2]) * a.scale;
+                    __syncwarp();
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int f4 = j + 16 * r;  // float4 index within the row
+                        const float4 val = reinterpret_cast<const float4*>(pf)[f4 ^ (4 * h)];
+                        __stcs(reinterpret_cast<float4*>(prow) + f4, val);
+                    }
+                }
+#elif PG3_PSTORE == 1
+#pragma unroll
+                for (int t2 = 0; t2 < 16; ++t2) __stcg(prow + ((j + 16 * t2 + 128) & 255), cnorm(x[t2]) * a.scale);
+#else
 #pragma unroll
                 for (int t2 = 0; t2 < 16; ++t2) __stcs(prow + ((j + 16 * t2 + 128) & 255), cnorm(x[t2]) * a.scale);
+#endif
             }
+#if PG3_PSTORE == 3
+            if (j == 0) bulk_wait_read_all();  // this lane's P row copies have read their slots
+#endif
             bar_row();  // transposes done: the buffer may be refilled
             P3(7);
             if (producer && issued == R + 1 && R + 1 < nrounds) try_issue(true);
@@ -388,10 +522,21 @@ int fused_pg3_max_groups() {
     return per_sm * sms / kGrp;
 }
 
-cudaError_t launch_fused_pg3(const Pg2Args& a, bool hamming, int groups, cudaStream_t st) {
+cudaError_t launch_fused_pg3(const Pg2Args& a, bool hamming, int groups, int scratch_groups, cudaStream_t st) {
     auto enc = encode_fn3();
     if (!enc) return cudaErrorNotSupported;
-    CUtensorMap hmap;
+    CUtensorMap hmap, gmap;
+    // G store view: [group x buffer x 32 m][256 c][32 j] f64; box = 32 j x 4 c x 32 m (32 KiB)
+    {
+        const cuuint64_t dims[3] = {32, 256, 32ull * kGBuf * (cuuint64_t)scratch_groups};
+        const cuuint64_t strides[2] = {32 * 8, 256 * 32 * 8};
+        const cuuint32_t box[3] = {32, (cuuint32_t)kTC, 32};
+        const cuuint32_t es[3] = {1, 1, 1};
+        if (enc(&gmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.gscratch, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
     // H: [frames][1024 k][256 l] c64 as a 3-D f64 tensor (l, k mod 256, 4 frame + k / 256);
     // box = 4 symbols x all 1024 subcarriers, 32-B swizzle
     {
@@ -409,7 +554,7 @@ cudaError_t launch_fused_pg3(const Pg2Args& a, bool hamming, int groups, cudaStr
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         Pg2Args aa = a;
-        void* args[] = {&aa, &hmap};
+        void* args[] = {&aa, &hmap, &gmap};
         return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(groups * kGrp), dim3(kThreads),
                                            args, smem, st);
     };
