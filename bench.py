@@ -363,6 +363,27 @@ def extra_configs(args, dev, local, threads):
     del hd
     rx.close()
 
+    # bench_estimators (metrics.cpp:145-253): periodogram vs FPS-SFT on the same frames after the
+    # support check, GPU (paper_2209_03883_b200/estimators.py) next to the reference's own harness
+    try:
+        from paper_2209_03883_b200.estimators import bench_estimators
+        base = configs.CFG0.replace(n=2048, n_prime=2048, m=256, m_prime=256, qam=16, window=1)
+        sizes = [256, 512, 1024, 2048]
+        rows = bench_estimators(base, sizes, 5, 5, 13, snr_db=40.0, batch=256, bandwidth_hz=60e6, device=local)
+        be = {"scenario": "fig6 numerology (B = 60 MHz, 16-QAM, Hamming, SNR 40 dB, K = 5, seed 13) with M = 256",
+              "gpu": [{"n": r.n, "periodogram_ms": r.periodogram_ms, "sft_ms": r.sft_ms, "speedup": r.speedup,
+                       "samples_used": r.samples_used, "periodogram_batch_frames_per_s": r.periodogram_batch_frames_per_s,
+                       "sft_batch_frames_per_s": r.sft_batch_frames_per_s,
+                       "batch_speedup": r.sft_batch_frames_per_s / r.periodogram_batch_frames_per_s} for r in rows],
+              "note": "single-frame latency (what the reference times) and batched rates (256 copies per call)"}
+        if O.ref_available():
+            ref = O.ref_bench_estimators(2048, 256, 60e6 / 2048, 77e9, 16, 1, base.pfa, 40.0, sizes, 5, 3, 13)
+            be["reference_cpu_1_thread"] = [{"n": n, "periodogram_ms": a, "sft_ms": b, "speedup": c, "samples_used": d}
+                                            for n, a, b, c, d in ref]
+        out["bench_estimators"] = be
+    except Exception as exc:  # the extras never break the headline
+        out["bench_estimators"] = {"error": repr(exc)}
+
     # §8(f) item 2: Monte-Carlo RMSE sweep (metrics.cpp:92-120) on the GPU generator + fused
     # receiver, against the reference's own rmse_sweep (single-threaded, as the reference runs it)
     from paper_2209_03883_b200 import montecarlo as mc

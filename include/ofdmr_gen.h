@@ -33,13 +33,17 @@ typedef struct ofdmr_gen_params {
 
 /* GPU generator: frames [first, first + count) straight into device memory.
  *   y, x_tx   device c64 [count][N][M]
- *   sigma2    device double [count]        n_targets device int32 [count]
+ *   sigma2    device double [count]        n_targets device int32 [count] (may be NULL)
  *   ranges, vels device double [count][max_targets] (may be NULL), snr_db device double [count] (may be NULL)
  *   status    device int32 [count]: bit 0 set when a frame hit an MT19937 rejection
  *             (probability ~2^-50 per frame); regenerate such frames with the CPU generator.
  *   stream    cudaStream_t (NULL = default stream)
- * Supports qam_order 4/16/64/256 without ZC precoding, targets_max <= 16, M <= 1024.
- * Returns 0, 2 (unsupported / invalid parameters) or 10 (CUDA error).
+ * Supports qam_order 4/16/64/256 without ZC precoding, targets_max <= 16, M <= 1024, as long
+ * as the on-chip draw ring (two rows of payload bits + one MT19937 block, about
+ * 16 (M - 1) log2(qam) bytes) fits the per-block shared memory: 256-QAM at M = 1024 does not.
+ * Returns 0, 2 (unsupported / invalid parameters, incl. that ring limit) or 10 (CUDA error).
+ * Stream-ordered: no host synchronisation or per-call allocation (ZC precoding uses
+ * stream-ordered cudaMallocAsync scratch).
  * Bit-exactness: the integer streams (symbols, scene) are exact; the fp64 channel and noise
  * use the GPU's sin/cos/log/pow, so a c64 value can differ from the CPU generator's by 1 ulp
  * in rare cells (tests/test_gpu_parity.py::test_gpu_generator_matches_cpu_generator). */
@@ -51,7 +55,7 @@ int ofdmr_gen_device(const ofdmr_gen_params* p, uint64_t base_seed, int64_t firs
  * Monte-Carlo callers use it (metrics.cpp:92-143): frame i of the batch uses the run seed
  * derive_seed(seed, first + i); targets (host arrays, <= 16) and SNR are fixed.  y, x_tx,
  * sigma2, status as for ofdmr_gen_device; h_true (may be NULL): device c128 [count][N][M],
- * true_channel of the realisation (channel.cpp:100-109).  Synchronous on `stream`. */
+ * true_channel of the realisation (channel.cpp:100-109).  Stream-ordered on `stream`. */
 int ofdmr_gen_device_explicit(const ofdmr_gen_params* p, uint64_t seed, int64_t first, int64_t count,
                               const double* target_ranges, const double* target_vels, int32_t n_targets,
                               double snr_db, void* y, void* x_tx, double* sigma2, int32_t* status, void* h_true,

@@ -141,6 +141,8 @@ def ref() -> C.CDLL:
         _ref.ref_sft_batch_c64.argtypes = [vp, i64, i64, i64, i64, vp, vp, d, i64, i64, vp, vp, vp, vp, vp, C.c_int]
         _ref.ref_make_frame_pair.argtypes = [i64, i64, d, d, i64, C.c_int, vp, vp, i64, d, C.c_uint64, vp, vp, vp]
         _ref.ref_rng_u64.argtypes = [C.c_uint64, i64, vp]
+        _ref.ref_bench_estimators.argtypes = [i64, i64, d, d, C.c_int, C.c_int, d, d, vp, C.c_int32, i64, i64,
+                                              C.c_uint64, vp, vp, vp, vp]
         _ref.ref_run_pipeline_sft.argtypes = [i64, i64, d, d, i64, C.c_int, C.c_int, vp, vp, C.c_int32, d, C.c_uint64,
                                               C.c_int, i64, i64, vp, vp, vp, vp, vp]
         _ref.ref_sft_noise_case.argtypes = [i64, i64, d, d, i64, vp, vp, C.c_int32, d, C.c_uint64, vp, vp]
@@ -435,3 +437,18 @@ def sft_pipeline_frame(y: np.ndarray, x: np.ndarray, sigma2: float, estimator: i
         s2 = estimate_noise_from_slice(h, noise_seed)
     spec = sft_iterate(h, sft_seed, s2, i_max=i_max, pfa=pfa)
     return detections_from_spectrum(spec["entries"], h.shape[0], h.shape[1], s2, pfa, max_targets), s2, spec
+
+
+def ref_bench_estimators(n, m, df, fc, qam, window, pfa, snr_db, sizes, k, repeats, seed):
+    """The reference's bench_estimators (metrics.cpp:145-253): rows (n, periodogram_ms, sft_ms,
+    speedup, samples_used); raises RuntimeError when its support precondition fails."""
+    sz = np.ascontiguousarray(sizes, np.int64)
+    pg, sf, sp = np.zeros(len(sz)), np.zeros(len(sz)), np.zeros(len(sz))
+    su = np.zeros(len(sz), np.int64)
+    rc = ref().ref_bench_estimators(n, m, df, fc, qam, window, pfa, snr_db, _p(sz), len(sz), k, repeats, seed,
+                                    _p(pg), _p(sf), _p(sp), _p(su))
+    if rc == 4:
+        raise RuntimeError("bench: detector support sets differ")
+    if rc:
+        raise ValueError(f"ref_bench_estimators failed ({rc})")
+    return [(int(sz[i]), float(pg[i]), float(sf[i]), float(sp[i]), int(su[i])) for i in range(len(sz))]

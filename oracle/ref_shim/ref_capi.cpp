@@ -383,6 +383,36 @@ int ref_run_pipeline_sft(int64_t n, int64_t m, double df, double fc, int64_t n_c
     }
 }
 
+/// The reference's own bench_estimators (metrics.cpp:145-253) on a base waveform; rows out as
+/// arrays (periodogram_ms, sft_ms, speedup, samples_used) per size.  Returns 4 when the
+/// reference's support precondition throws.
+int ref_bench_estimators(int64_t n, int64_t m, double df, double fc, int qam, int window, double pfa, double snr_db,
+                         const int64_t* sizes, int32_t count, int64_t k, int64_t repeats, uint64_t seed, double* pg_ms,
+                         double* sft_ms, double* speedup, int64_t* samples) {
+    try {
+        SimulationConfig cfg;
+        cfg.waveform = make_wave(std::size_t(n), std::size_t(m), std::size_t(n), std::size_t(m), df, fc,
+                                 std::size_t(n / 4), window, pfa);
+        cfg.waveform.qam_order = std::size_t(qam);
+        cfg.channel.snr_db = snr_db;
+        std::vector<std::size_t> sz(sizes, sizes + count);
+        const auto rows = bench_estimators(cfg, sz, std::size_t(k), std::size_t(repeats), seed);
+        for (std::size_t i = 0; i < rows.size(); ++i) {
+            pg_ms[i] = rows[i].periodogram_ms;
+            sft_ms[i] = rows[i].sft_ms;
+            speedup[i] = rows[i].speedup;
+            samples[i] = int64_t(rows[i].samples_used);
+        }
+        return 0;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (const std::runtime_error&) {
+        return 4;
+    } catch (...) {
+        return 3;
+    }
+}
+
 /// run_pipeline (pipeline.cpp:60-115) with the FPS-SFT detector in estimate-noise mode: the
 /// reference's own sigma2_used (= estimate_noise_from_slice(h, derive_seed(seed, 0x6e6573)),
 /// an anonymous-namespace function) and the channel estimate h it was computed from, rebuilt

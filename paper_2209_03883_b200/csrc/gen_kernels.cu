@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_frame_kernel(GenArgs a) {
         s.rej = rej;
         s.snr_db = snr;
         s.mp = a.uniform_power ? a.uniform_mp : 0.0;
-        a.n_targets[f] = cnt;
+        if (a.n_targets) a.n_targets[f] = cnt;
         if (a.snr_db) a.snr_db[f] = snr;
         for (int t = 0; t < cnt && t < a.max_targets; ++t) {
             if (a.ranges) a.ranges[(size_t)f * a.max_targets + t] = rg[t];
@@ -481,7 +481,7 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
                int32_t* status, void* stream, const double* exp_ranges, const double* exp_vels, int32_t exp_count,
                double exp_snr, void* h_true = nullptr) {
     using namespace ofdmr;
-    if (!p || !y || !x_tx || !sigma2 || !n_targets || !status || count < 0) return 2;
+    if (!p || !y || !x_tx || !sigma2 || !status || count < 0) return 2;  // n_targets may be null
     if (count == 0) return 0;
     int bps = 0;
     switch (p->qam_order) {
@@ -560,6 +560,14 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
     a.fph_rows = std::max(1, a.explicit_scene ? a.exp_count : p->targets_max);
     const size_t smem = ((sizeof(GenShared) + 15) & ~size_t(15)) + sizeof(double2) * a.fph_rows * p->m +
                         sizeof(double) * 2 * p->m + sizeof(uint64_t) * ring + (size_t)p->n;
+    {
+        // the draw ring holds two rows of payload bits plus one MT19937 block: high QAM orders at large
+        // M exceed the per-block shared memory (e.g. 256-QAM at M = 1024 needs 256 KiB): config error
+        int dev = 0, max_smem = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (smem > (size_t)max_smem) return 2;
+    }
     cudaError_t e = cudaFuncSetAttribute(gen_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return 10;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -585,7 +593,7 @@ int gen_launch(const ofdmr_gen_params* p, uint64_t base_seed, int64_t first, int
         b.y = a.y + c0 * cells;
         b.x = a.x + c0 * cells;
         b.sigma2 = a.sigma2 + c0;
-        b.n_targets = a.n_targets + c0;
+        b.n_targets = a.n_targets ? a.n_targets + c0 : nullptr;
         b.status = a.status + c0;
         if (a.ranges) b.ranges = a.ranges + c0 * a.max_targets;
         if (a.vels) b.vels = a.vels + c0 * a.max_targets;
@@ -618,14 +626,10 @@ extern "C" int ofdmr_gen_device_explicit(const ofdmr_gen_params* p, uint64_t see
                                          void* h_true, void* stream) {
     static const double kNone = 0.0;
     if (!p || n_targets < 0 || n_targets > 16) return 2;
-    int32_t* nt = nullptr;
-    if (cudaMalloc(&nt, sizeof(int32_t) * (size_t)(count > 0 ? count : 1)) != cudaSuccess) return 10;
-    const int rc = gen_launch(p, seed, first, count, y, x_tx, sigma2, nt, nullptr, nullptr, nullptr, 0, status, stream,
-                              n_targets > 0 ? target_ranges : &kNone, n_targets > 0 ? target_vels : &kNone,
-                              n_targets, snr_db, h_true);
-    cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
-    cudaFree(nt);
-    return rc;
+    // stream-ordered: no per-call scratch (the per-frame target count is the fixed scene's)
+    return gen_launch(p, seed, first, count, y, x_tx, sigma2, nullptr, nullptr, nullptr, nullptr, 0, status, stream,
+                      n_targets > 0 ? target_ranges : &kNone, n_targets > 0 ? target_vels : &kNone, n_targets, snr_db,
+                      h_true);
 }
 
 namespace {

@@ -677,8 +677,10 @@ def extract_peaks(p: torch.Tensor, eta: float, max_targets: int, rc: RadarConfig
     np_, mp = p.shape
     if max_targets > 64:
         raise ConfigError("extract_peaks: max_targets <= 64 on the GPU path")
-    r = _ctx(16, 16, max(np_, 16), max(mp, 16), WINDOW_RECT, EST_LS, 0, max_targets) if (np_ < 16 or mp < 16) \
-        else _ctx(np_, mp, np_, mp, WINDOW_RECT, EST_LS, 0, max_targets)
+    if np_ < 16 or mp < 16:
+        # the device contexts take power-of-two dimensions >= 16 (include/ofdmr_b200.h)
+        raise ConfigError("extract_peaks: maps smaller than 16 x 16 are not supported on the GPU path")
+    r = _ctx(np_, mp, np_, mp, WINDOW_RECT, EST_LS, 0, max_targets)
     d = r.extract_peaks(p, eta)
     out = [Detection(a, b, c) for a, b, c in d.frame(0)]
     if rc is not None:

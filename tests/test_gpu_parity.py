@@ -119,6 +119,15 @@ def test_reference_unit_analogues(cuda):
         assert r == 21 and c - m // 2 == 9
 
 
+def test_extract_peaks_small_map_rejected(cuda):
+    from paper_2209_03883_b200.receiver import extract_peaks
+
+    with pytest.raises(ConfigError):
+        extract_peaks(np.ones((8, 32), np.float32), 0.5, 3)
+    got = extract_peaks(np.pad(np.ones((1, 1), np.float32), ((5, 10), (7, 8))), 0.5, 3)
+    assert [(d.delay_bin, d.doppler_bin) for d in got] == [(5, 7 - 8)]
+
+
 def test_detect_on_shared_map_is_exact(cuda):
     # extract_peaks on the SAME fp32 map: GPU selection must equal the oracle's exactly
     cfg = configs.CFG1

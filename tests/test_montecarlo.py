@@ -86,3 +86,20 @@ def test_gpu_mse_sweep_matches_reference(cuda, estimator):
     ref = O.ref_mse_sweep(_scenario(cfg, ranges, vels), grid, trials, seed)
     got = np.array([r.channel_mse for r in rows])
     assert np.allclose(got, ref, rtol=1e-4, atol=0), (got, ref)
+
+
+@pytest.mark.gpu
+def test_gpu_rmse_sweep_partial_batches_match_reference(cuda):
+    """Several batches per SNR point, the last one partial (batch 5, 24 trials): the cross-SNR
+    two-slot pipelining of rmse_sweep (the host matches batch j - 1 while the GPU generates and
+    receives batch j, across SNR boundaries) gives the reference's rows."""
+    cfg = configs.CFG1
+    ranges = np.array([8.0, 17.5, 31.0])
+    vels = np.array([-35.0, 12.0, 60.0])
+    grid = [-15.0, 5.0]
+    trials, seed = 24, 777
+    rows = mc.rmse_sweep(cfg, ranges, vels, grid, trials, seed, batch=5)
+    ref_rows = O.ref_rmse_sweep(_scenario(cfg, ranges, vels), grid, trials, seed)
+    for row, ref in zip(rows, ref_rows):
+        got = np.array([row.range_rmse_m, row.velocity_rmse_mps, row.miss_rate])
+        assert np.allclose(got, ref, rtol=1e-9, atol=0), (row, ref)
