@@ -216,6 +216,34 @@ int ofdmr_pipeline_sft(ofdmr_context* ctx, const void* y, const void* x_tx, cons
 int ofdmr_sft_estimate_noise(ofdmr_context* ctx, const void* h, int32_t n, int32_t m, const uint64_t* seeds,
                              double* sigma2_out, int64_t frames);
 
+/* --- multi-device ---------------------------------------- */
+/* Frames are independent: a batch of F frames is split into contiguous shards
+ * [r F / G, (r + 1) F / G) over G devices (ofdmr_shard_range), each processed by its own context
+ * on its own host thread with no data-path exchange.  The one exchange is the gather of the
+ * fixed-size detection records: into the caller's host arrays (ofdmr_multi_pipeline_host) or onto
+ * the first device with cudaMemcpyPeerAsync over NVLink / NVSwitch (ofdmr_multi_pipeline).  A
+ * device may be listed more than once (several contexts share it). */
+typedef struct ofdmr_multi ofdmr_multi;
+void ofdmr_shard_range(int64_t frames, int32_t rank, int32_t world, int64_t* lo, int64_t* hi);
+int ofdmr_multi_create(const ofdmr_config* cfg, const int32_t* devices, int32_t ndev, ofdmr_multi** out);
+void ofdmr_multi_destroy(ofdmr_multi* m);
+int32_t ofdmr_multi_devices(const ofdmr_multi* m);
+/* The single-device context of shard `rank` (owned by m). */
+ofdmr_context* ofdmr_multi_context(ofdmr_multi* m, int32_t rank);
+const char* ofdmr_multi_last_error(void);
+/* ofdmr_pipeline_host over the devices: HOST y, x_tx, sigma2, k_per_frame (may be NULL), records
+ * [frames][K] written in place per shard.  Synchronous. */
+int ofdmr_multi_pipeline_host(ofdmr_multi* m, const void* y, const void* x_tx, const double* sigma2,
+                              const int32_t* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin, float* peak_power,
+                              int32_t* counts, int64_t frames);
+/* ofdmr_pipeline over device-resident shards: y[r], x_tx[r], sigma2[r], k_per_frame[r] (the array
+ * or its entries may be NULL) live on device r and hold shard r's frames; the records and status of
+ * all F frames are gathered into the arrays on the FIRST device ([F][K], [F]).  Synchronous on
+ * return (every shard's gather has landed). */
+int ofdmr_multi_pipeline(ofdmr_multi* m, const void* const* y, const void* const* x_tx, const double* const* sigma2,
+                         const int32_t* const* k_per_frame, int32_t* delay_bin, int32_t* doppler_bin,
+                         float* peak_power, int32_t* counts, int32_t* status, int64_t frames);
+
 #ifdef __cplusplus
 }
 #endif

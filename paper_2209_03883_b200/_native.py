@@ -111,6 +111,14 @@ RECEIVER_SYMBOLS = [
     ("ofdmr_pipeline_sft", i32, [vp, vp, vp, vp, vp, vp, C.POINTER(OfdmrSftConfig), vp, vp, vp, vp, vp, vp, vp,
                                  i64]),
     ("ofdmr_sft_estimate_noise", i32, [vp, vp, i32, i32, vp, vp, i64]),
+    ("ofdmr_shard_range", None, [i64, i32, i32, vp, vp]),
+    ("ofdmr_multi_create", i32, [C.POINTER(OfdmrConfig), vp, i32, vp]),
+    ("ofdmr_multi_destroy", None, [vp]),
+    ("ofdmr_multi_devices", i32, [vp]),
+    ("ofdmr_multi_context", vp, [vp, i32]),
+    ("ofdmr_multi_last_error", C.c_char_p, []),
+    ("ofdmr_multi_pipeline_host", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
+    ("ofdmr_multi_pipeline", i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64]),
 ]
 
 # include/ofdmr_gen.h, device side (in the CUDA library)

@@ -55,6 +55,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "ofdm_kernels": [],
         "io_kernels": [],
         "capi": [],
+        "multi": [],
         # exact fp64 rounding order (no FMA contraction) for bit-parity of SFT decisions
         "sft_kernels": ["-fmad=false"],
         # GPU frame generator: the CPU generator's fp64 operation order (no FMA contraction)

@@ -576,6 +576,89 @@ class Receiver:
         return out[0] if single else out
 
 
+class MultiReceiver:
+    """ofdmr_multi (include/ofdmr_b200.h): one context per listed device, frames sharded in
+    contiguous ranges (shard.shard_range), detections gathered to the host (pipeline_host) or to
+    the first device by peer copies (pipeline on per-device shards)."""
+
+    def __init__(self, rc: RadarConfig, devices, chunk_frames: int = 0):
+        self._lib = _native.lib()
+        cfg = _native.OfdmrConfig()
+        cfg.n_subcarriers, cfg.n_symbols, cfg.n_prime, cfg.m_prime = rc.n, rc.m, rc.n_prime, rc.m_prime
+        cfg.window, cfg.estimator, cfg.n_cp = rc.window, rc.estimator, rc.n_cp
+        cfg.max_targets, cfg.pfa, cfg.chunk_frames, cfg.device = rc.max_targets, rc.pfa, chunk_frames, 0
+        self.cfg = cfg
+        self.devices = [int(d) for d in devices]
+        arr = (C.c_int32 * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        rc_ = self._lib.ofdmr_multi_create(C.byref(cfg), arr, len(self.devices), C.byref(h))
+        if rc_:
+            msg = self._lib.ofdmr_multi_last_error().decode()
+            raise ConfigError(msg) if rc_ == 2 else CudaError(msg)
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.ofdmr_multi_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, rc_: int) -> None:
+        if rc_:
+            msg = self._lib.ofdmr_multi_last_error().decode()
+            raise ConfigError(msg) if rc_ == 2 else CudaError(msg)
+
+    def shard_range(self, frames: int, rank: int) -> tuple[int, int]:
+        lo, hi = C.c_int64(), C.c_int64()
+        self._lib.ofdmr_shard_range(frames, rank, len(self.devices), C.byref(lo), C.byref(hi))
+        return lo.value, hi.value
+
+    def pipeline_host(self, y: np.ndarray, x_tx: np.ndarray, sigma2, k_per_frame=None):
+        """ofdmr_multi_pipeline_host: numpy records (delay, doppler, power, counts)."""
+        F = y.shape[0]
+        y = np.ascontiguousarray(y, np.complex64)
+        x = np.ascontiguousarray(x_tx, np.complex64)
+        s2 = np.ascontiguousarray(sigma2, np.float64)
+        k = None if k_per_frame is None else np.ascontiguousarray(k_per_frame, np.int32)
+        K = self.cfg.max_targets
+        d, dp = np.zeros((F, K), np.int32), np.zeros((F, K), np.int32)
+        pw, cnt = np.zeros((F, K), np.float32), np.zeros(F, np.int32)
+        self._check(self._lib.ofdmr_multi_pipeline_host(self._h, y.ctypes.data, x.ctypes.data, s2.ctypes.data,
+                                                        k.ctypes.data if k is not None else None, d.ctypes.data,
+                                                        dp.ctypes.data, pw.ctypes.data, cnt.ctypes.data, F))
+        return d, dp, pw, cnt
+
+    def pipeline(self, ys, xs, s2s, ks=None) -> tuple[Detections, torch.Tensor]:
+        """ofdmr_multi_pipeline on per-device shards (lists of tensors, shard r on devices[r]);
+        returns the gathered Detections and status on the first device."""
+        F = sum(int(t.shape[0]) for t in ys)
+        for r, t in enumerate(ys):
+            lo, hi = self.shard_range(F, r)
+            if int(t.shape[0]) != hi - lo:
+                raise ConfigError("shard sizes must follow ofdmr_shard_range")
+        G = len(self.devices)
+        vp = C.c_void_p
+        arr = lambda ts: (vp * G)(*[t.data_ptr() if t is not None else None for t in ts])  # noqa: E731
+        dev0 = torch.device("cuda", self.devices[0])
+        K = self.cfg.max_targets
+        z = dict(device=dev0)
+        d = Detections(torch.zeros(F, K, dtype=torch.int32, **z), torch.zeros(F, K, dtype=torch.int32, **z),
+                       torch.zeros(F, K, dtype=torch.float32, **z), torch.zeros(F, dtype=torch.int32, **z))
+        st = torch.zeros(F, dtype=torch.int32, **z)
+        for dv in set(self.devices):
+            torch.cuda.synchronize(dv)  # inputs produced on torch's streams are ready
+        self._check(self._lib.ofdmr_multi_pipeline(self._h, arr(ys), arr(xs), arr(s2s),
+                                                   arr(ks) if ks is not None else None, d.delay_bin.data_ptr(),
+                                                   d.doppler_bin.data_ptr(), d.peak_power.data_ptr(),
+                                                   d.counts.data_ptr(), st.data_ptr(), F))
+        return d, st
+
+
 # ---------------------------------------------------------------------------------
 # Module-level functions with the reference's names (single frame, value semantics).
 

@@ -33,22 +33,23 @@ def unpack(rec: torch.Tensor, k: int):
 
 
 class DetectionGather:
-    """Pre-allocated gather of every rank's packed records to rank 0 (one all_gather of
-    equal-size padded shards; ~3K+1 int32 per frame, i.e. < 1 MB for cfg4)."""
+    """Pre-allocated gather of every rank's packed records to rank 0 (one dist.gather of
+    equal-size padded shards; ~3K+1 int32 per frame, i.e. < 1 MB for cfg4).  Only rank 0
+    receives the records."""
 
     def __init__(self, frames: int, k: int, rank: int, world: int, device: torch.device):
         self.frames, self.k, self.rank, self.world = frames, k, rank, world
         self.sizes = [b - a for a, b in (shard_range(frames, r, world) for r in range(world))]
         self.rows = max(self.sizes)
         self.local = torch.zeros(self.rows, 3 * k + 1, dtype=torch.int32, device=device)
-        self.bufs = [torch.empty_like(self.local) for _ in range(world)]
+        self.bufs = [torch.empty_like(self.local) for _ in range(world)] if rank == 0 else None
 
     def __call__(self, delay, doppler, power, counts) -> torch.Tensor | None:
         n = delay.shape[0]
         pack(delay, doppler, power, counts, out=self.local[:n])
         if self.world == 1:
             return self.local[:n]
-        dist.all_gather(self.bufs, self.local)
+        dist.gather(self.local, gather_list=self.bufs, dst=0)
         if self.rank != 0:
             return None
         return torch.cat([b[:s] for b, s in zip(self.bufs, self.sizes)])

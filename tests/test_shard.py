@@ -28,6 +28,21 @@ def test_shard_ranges_partition():
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
 
 
+def test_c_abi_shard_range_matches():
+    # the C-ABI's multi-device sharding (ofdmr_shard_range) is the same partition as shard.py's
+    import ctypes as C
+
+    from paper_2209_03883_b200 import _native
+
+    lib = _native.lib()
+    for frames in (1, 7, 8192, 8193, 10**9 + 7):
+        for world in (1, 2, 3, 8):
+            for r in range(world):
+                lo, hi = C.c_int64(), C.c_int64()
+                lib.ofdmr_shard_range(frames, r, world, C.byref(lo), C.byref(hi))
+                assert (lo.value, hi.value) == shard_range(frames, r, world)
+
+
 def test_pack_roundtrip():
     d = torch.randint(0, 1024, (5, 8), dtype=torch.int32)
     v = torch.randint(-128, 128, (5, 8), dtype=torch.int32)
