@@ -18,9 +18,12 @@
  * through the device `status` array (bit 0) — stream-ordered calls cannot throw; the
  * synchronous host entry point returns OFDMR_ERR_CONFIG for it.
  *
- * Sizes: N, M, N', M' must be powers of two in [16, 4096] (B200 design limit; the
- * reference also accepts other sizes through FFTW), N' >= N, M' >= M
- * (periodogram.cpp:43, ConfigError otherwise), max_targets <= 64.
+ * Sizes: N, M, N', M' in [2, 4096] whose prime factors are 2, 3, 5, 7, 11 or 13 (the reference
+ * accepts any length through FFTW; its presets use 2048 x 560, 2048 x 200, 512 x 140 and powers of
+ * two), N' >= N, M' >= M (periodogram.cpp:43, ConfigError otherwise), max_targets <= 64.
+ * Powers of two in [16, 4096] with N' in {N, 2N, 4N} run the specialised power-of-two kernels
+ * (and the fused ones at 1024 x 256); every other shape the mixed-radix kernels
+ * (csrc/mixed_kernels.cu).  The OFDM front end needs a power-of-two N; FPS-SFT see below.
  *
  * Threading: one context per host thread or stream (the reference functions are
  * reentrant; this context owns scratch buffers).

@@ -143,6 +143,8 @@ def ref() -> C.CDLL:
         _ref.ref_rng_u64.argtypes = [C.c_uint64, i64, vp]
         _ref.ref_bench_estimators.argtypes = [i64, i64, d, d, C.c_int, C.c_int, d, d, vp, C.c_int32, i64, i64,
                                               C.c_uint64, vp, vp, vp, vp]
+        _ref.ref_run_pipeline_q.argtypes = [i64, i64, i64, i64, d, d, i64, C.c_int, d, C.c_int, vp, vp, C.c_int32,
+                                            C.c_int, d, C.c_uint64, vp, vp, vp]
         _ref.ref_run_pipeline_sft.argtypes = [i64, i64, d, d, i64, C.c_int, C.c_int, vp, vp, C.c_int32, d, C.c_uint64,
                                               C.c_int, i64, i64, vp, vp, vp, vp, vp]
         _ref.ref_sft_noise_case.argtypes = [i64, i64, d, d, i64, vp, vp, C.c_int32, d, C.c_uint64, vp, vp]
@@ -452,3 +454,16 @@ def ref_bench_estimators(n, m, df, fc, qam, window, pfa, snr_db, sizes, k, repea
     if rc:
         raise ValueError(f"ref_bench_estimators failed ({rc})")
     return [(int(sz[i]), float(pg[i]), float(sf[i]), float(sp[i]), int(su[i])) for i in range(len(sz))]
+
+
+def ref_run_pipeline_qam(scn, qam: int, snr_db: float, seed: int):
+    """ref_run_pipeline with an explicit QAM order: (delay bins, doppler bins, None, None)."""
+    args, keep = ref_scenario_args(*scn)
+    k = max(args[-1], 1)
+    d = np.zeros(k, np.int64)
+    v = np.zeros(k, np.int64)
+    cnt = C.c_long()
+    rc = ref().ref_run_pipeline_q(*args, qam, snr_db, seed, _p(d), _p(v), C.byref(cnt))
+    if rc:
+        raise ValueError(f"ref_run_pipeline_q failed ({rc})")
+    return d[:cnt.value], v[:cnt.value], None, None

@@ -383,6 +383,28 @@ int ref_run_pipeline_sft(int64_t n, int64_t m, double df, double fc, int64_t n_c
     }
 }
 
+/// ref_run_pipeline with an explicit QAM order (table1 / fig8 use 16-QAM).
+int ref_run_pipeline_q(int64_t n, int64_t m, int64_t np, int64_t mp, double df, double fc, int64_t n_cp, int window,
+                       double pfa, int estimator, const double* ranges, const double* vels, int32_t count, int qam,
+                       double snr_db, uint64_t seed, long* delay, long* doppler, long* n_det) {
+    try {
+        SimulationConfig cfg = scenario(n, m, np, mp, df, fc, n_cp, window, pfa, estimator, ranges, vels, count);
+        cfg.waveform.qam_order = std::size_t(qam);
+        cfg.channel.snr_db = snr_db;
+        const auto res = run_pipeline(cfg, seed);
+        for (std::size_t i = 0; i < res.detections.size(); ++i) {
+            delay[i] = res.detections[i].delay_bin;
+            doppler[i] = res.detections[i].doppler_bin;
+        }
+        *n_det = long(res.detections.size());
+        return 0;
+    } catch (const ConfigError&) {
+        return 2;
+    } catch (...) {
+        return 3;
+    }
+}
+
 /// The reference's own bench_estimators (metrics.cpp:145-253) on a base waveform; rows out as
 /// arrays (periodogram_ms, sft_ms, speedup, samples_used) per size.  Returns 4 when the
 /// reference's support precondition throws.

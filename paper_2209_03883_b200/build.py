@@ -45,6 +45,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
     headers = list(CSRC.glob("*.cuh")) + [ROOT / "include" / "ofdmr_b200.h", ROOT / "include" / "ofdmr_gen.h"]
     units = {
         "radar_kernels": [],
+        "mixed_kernels": [],
         "fast_kernels": [],
         "fused_ce": [],
         "fused_pg": [],

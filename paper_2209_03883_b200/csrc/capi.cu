@@ -62,6 +62,8 @@ int fused_pg3_max_groups();
 size_t fused_pg3_counter_ints(int groups);
 size_t fused_pg3_scratch_elems(int groups);
 int fused_pg2_max_groups();
+bool mixed_size_supported(int len);
+int mixed_col_tile(int np, int m);
 size_t fused_pg2_counter_ints(int groups);
 size_t fused_pg2_scratch_elems(int groups);
 }  // namespace ofdmr
@@ -125,6 +127,10 @@ struct ofdmr_context {
     int pg2_groups = 0;               // warp-specialised periodogram: 16-CTA frame groups
     float2* pg2_scratch = nullptr;    // per group 2 x 1024 x 256 G (L2)
     int* pg2_counters = nullptr;      // per group progress counters
+    bool mixed = false;               // some size not a power of two: mixed-radix kernels (mixed_kernels.cu)
+    float2* tw_n = nullptr;           // e^{-j 2 pi t / L} tables of N, N', M' (mixed path)
+    float2* tw_np = nullptr;
+    float2* tw_mp = nullptr;
     int pg3_groups = 0;               // split-exchange periodogram (fused_pg3.cu)
     float2* pg3_scratch = nullptr;
     int* pg3_counters = nullptr;
@@ -234,13 +240,13 @@ struct StageTimer {
 
 int check_cfg(const ofdmr_config* c) {
     if (!c) return fail(OFDMR_ERR_CONFIG, "ofdmr_create: null config");
-    if (!pow2_in(c->n_subcarriers, 16, 4096) || !pow2_in(c->n_symbols, 16, 4096))
-        return fail(OFDMR_ERR_CONFIG, "N and M must be powers of two in [16, 4096]");
+    for (int v : {c->n_subcarriers, c->n_symbols, c->n_prime, c->m_prime})
+        if (!mixed_size_supported(v))
+            return fail(OFDMR_ERR_CONFIG,
+                        "N, M, N', M' must lie in [2, 4096] and factor into 2, 3, 5, 7, 11, 13 (got " +
+                            std::to_string(v) + ")");
     if (c->n_prime < c->n_subcarriers || c->m_prime < c->n_symbols)
         return fail(OFDMR_ERR_CONFIG, "periodogram: N' >= N and M' >= M required");
-    if (!pow2_in(c->n_prime, 16, 4096) || !pow2_in(c->m_prime, 16, 4096))
-        return fail(OFDMR_ERR_CONFIG, "N' and M' must be powers of two in [16, 4096]");
-    if (c->n_prime > 4 * c->n_subcarriers) return fail(OFDMR_ERR_CONFIG, "N' <= 4 N supported");
     if (c->window != OFDMR_WINDOW_RECT && c->window != OFDMR_WINDOW_HAMMING)
         return fail(OFDMR_ERR_CONFIG, "window must be rectangular or hamming");
     if (c->estimator != OFDMR_EST_LS && c->estimator != OFDMR_EST_DFT_CE)
@@ -277,7 +283,17 @@ ColArgs base_col(ofdmr_context* c) {
     a.tw = c->tw;
     a.m = c->cfg.n_symbols;
     a.ntiles = c->ntiles;
+    a.n = c->cfg.n_subcarriers;
+    a.np = c->cfg.n_prime;
+    a.tw_n = c->tw_n;    // non-null only on the mixed-radix path (launch_colpass dispatches on it)
+    a.tw_np = c->tw_np;
     return a;
+}
+
+// row-pass arguments of the mixed-radix path (launch_rowpass dispatches on tw_mp)
+void row_mixed(ofdmr_context* c, RowArgs& r) {
+    r.mp = c->cfg.m_prime;
+    r.tw_mp = c->tw_mp;
 }
 
 int launch_col(ofdmr_context* c, const ColArgs& a, int np, int64_t frames, cudaStream_t st) {
@@ -392,6 +408,7 @@ int run_pipeline_chunk(ofdmr_context* c, int si, const float2* y, const float2* 
     cudaError_t e;
     {
         StageTimer t(c, 1, s.stream);
+        row_mixed(c, r);
         e = launch_rowpass(r, g.m_prime, int(nf), s.stream);
     }
     if (e != cudaSuccess) return cuda_fail(e, "rowpass");
@@ -550,17 +567,21 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
     c->cfg = *cfg;
     c->device = cfg->device;
     const int n = cfg->n_subcarriers, m = cfg->n_symbols, np = cfg->n_prime, mp = cfg->m_prime;
-    c->shortcut = cfg->estimator == OFDMR_EST_DFT_CE && cfg->window == OFDMR_WINDOW_RECT && np == n;
+    // power-of-two kernels (radar_kernels.cu templates and the fused / fast specialisations) for
+    // sizes in [16, 4096] with N' in {N, 2N, 4N}; every other shape runs the mixed-radix path
+    c->mixed = !(pow2_in(n, 16, 4096) && pow2_in(m, 16, 4096) && pow2_in(np, 16, 4096) && pow2_in(mp, 16, 4096) &&
+                 (np == n || np == 2 * n || np == 4 * n));
+    c->shortcut = !c->mixed && cfg->estimator == OFDMR_EST_DFT_CE && cfg->window == OFDMR_WINDOW_RECT && np == n;
     c->g_rows = c->shortcut ? cfg->n_cp : np;
     if (c->shortcut && c->g_rows == 0) c->g_rows = 1;  // L = 0: all-zero estimate, keep one zero row
-    c->ntiles = m / colpass_tile_cols(np);
-    c->rows_per_block = rowpass_rows(mp, np, m);
+    c->ntiles = m / (c->mixed ? mixed_col_tile(np, m) : colpass_tile_cols(np));
+    c->rows_per_block = c->mixed ? rowpass_rows(mp, np, 0) : rowpass_rows(mp, np, m);
     c->nblk = (np + c->rows_per_block - 1) / c->rows_per_block;
     c->log_pfa = std::log(cfg->pfa);
     c->pf = power_factor_d(cfg->window, n, m);
     c->inv_count = 1.0 / double(size_t(n) * size_t(m));
     c->scale = float(1.0 / (double(n) * double(m)));
-    c->fast = n == 1024 && np == 1024 && m == 256 && mp == 256;
+    c->fast = !c->mixed && n == 1024 && np == 1024 && m == 256 && mp == 256;
     c->fused = c->fast && cfg->estimator == OFDMR_EST_DFT_CE && cfg->n_cp > 0 && cfg->n_cp <= 128;
     if (c->fast) {
         c->rows_per_block = fast_rows_per_block();
@@ -595,6 +616,21 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         for (int q = 0; q < 128; ++q) zt[4 * 512 + q] = tw[32 * q];
         e = cudaMalloc(&c->zp_tw, sizeof(float2) * zt.size());
         if (e == cudaSuccess) e = cudaMemcpy(c->zp_tw, zt.data(), sizeof(float2) * zt.size(), cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess && c->mixed) {  // per-length twiddle tables of the mixed-radix engine
+        auto table = [&](int len, float2** out) {
+            std::vector<float2> t(len);
+            for (int i = 0; i < len; ++i) {
+                const double a = -kTwoPi * double(i) / double(len);
+                t[i] = make_float2(float(std::cos(a)), float(std::sin(a)));
+            }
+            cudaError_t ee = cudaMalloc(out, sizeof(float2) * len);
+            if (ee == cudaSuccess) ee = cudaMemcpy(*out, t.data(), sizeof(float2) * len, cudaMemcpyHostToDevice);
+            return ee;
+        };
+        e = table(n, &c->tw_n);
+        if (e == cudaSuccess) e = table(np, &c->tw_np);
+        if (e == cudaSuccess) e = table(mp, &c->tw_mp);
     }
     if (e == cudaSuccess && cfg->window == OFDMR_WINDOW_HAMMING) {
         std::vector<double> wk(n), wl(m);
@@ -685,6 +721,9 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaSetDevice(c->device);
     cudaFree(c->tw);
     cudaFree(c->zp_tw);
+    cudaFree(c->tw_n);
+    cudaFree(c->tw_np);
+    cudaFree(c->tw_mp);
     cudaFree(c->wk);
     cudaFree(c->wk_s);
     cudaFree(c->wl);
@@ -1037,7 +1076,8 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
         cudaError_t e;
         {
             StageTimer t(c, 1, s.stream);
-            e = launch_rowpass(r, g.m_prime, int(nf), s.stream);
+            row_mixed(c, r);
+        e = launch_rowpass(r, g.m_prime, int(nf), s.stream);
         }
         if (e != cudaSuccess) return cuda_fail(e, "rowpass");
         ++c->launches;
@@ -1074,6 +1114,7 @@ static int detect_impl(ofdmr_context* c, const float* p, const double* sigma2_h,
         r.kmax = K;
         r.cand = c->cand;
         r.detect = 1;
+        row_mixed(c, r);
         cudaError_t e = launch_rowpass(r, g.m_prime, int(nf), c->stream);
         if (e != cudaSuccess) return cuda_fail(e, "rowpass(detect)");
         ++c->launches;
@@ -1113,6 +1154,8 @@ static int ofdm_impl(ofdmr_context* c, bool inverse, const void* in, void* out, 
     if (frames <= 0) return OFDMR_OK;
     const ofdmr_config& g = c->cfg;
     if (g.n_cp < 0 || g.n_cp > g.n_subcarriers) return fail(OFDMR_ERR_CONFIG, "n_cp must lie in [0, N]");
+    if (!pow2_in(g.n_subcarriers, 16, 4096))
+        return fail(OFDMR_ERR_CONFIG, std::string(what) + ": N must be a power of two in [16, 4096] on the GPU path");
     OFDMR_CUDA(cudaSetDevice(c->device));
     const cudaError_t e = ofdmr::launch_ofdm(inverse, static_cast<const float2*>(in), static_cast<float2*>(out),
                                              g.n_subcarriers, g.n_symbols, g.n_cp, frames, c->tw, c->stream);

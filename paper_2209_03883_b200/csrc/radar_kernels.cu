@@ -342,7 +342,11 @@ cudaError_t launch_colpass_n(const ColArgs& a, int np, int frames, cudaStream_t 
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_colpass_mixed(const ColArgs& a, int frames, cudaStream_t st);
+cudaError_t launch_rowpass_mixed(const RowArgs& a, int frames, cudaStream_t st);
+
 cudaError_t launch_colpass(const ColArgs& a, int n, int np, int frames, cudaStream_t st) {
+    if (a.tw_n != nullptr) return launch_colpass_mixed(a, frames, st);  // sizes not powers of two
     switch (n) {
         case 16: return launch_colpass_n<16>(a, np, frames, st);
         case 32: return launch_colpass_n<32>(a, np, frames, st);
@@ -392,6 +396,7 @@ cudaError_t launch_rowpass_t(const RowArgs& a, int frames, cudaStream_t st) {
 }
 
 cudaError_t launch_rowpass(const RowArgs& a, int mp, int frames, cudaStream_t st) {
+    if (a.tw_mp != nullptr) return launch_rowpass_mixed(a, frames, st);  // M' not a power of two
     if (rowpass_zp_applies(a, mp)) return launch_rowpass_zp(a, frames, st);
     switch (mp) {
         case 16: return launch_rowpass_t<16>(a, frames, st);

@@ -56,6 +56,11 @@ struct ColArgs {
     int shortcut;           // rect window, N' = N, DFT-CE: G = IFFT_N(H) rows < L
     int g_rows;             // rows of G written per frame
     int ntiles;             // M / C
+    // mixed-radix path (N or N' not a power of two, mixed_kernels.cu): runtime sizes and the
+    // e^{-j 2 pi t / L} tables of the two transform lengths
+    int n, np;
+    const float2* tw_n;
+    const float2* tw_np;
 };
 
 // Row (symbol / Doppler axis) pass over blocks of R rows of one frame (+ 1 halo row
@@ -81,6 +86,8 @@ struct RowArgs {
     unsigned long long* cand;  // [frame][nblk][kmax] packed keys
     int detect;             // 0 = map only
     const float2* zp_tw;    // rowpass_zp twiddles: W_2048^{j (4 k1 + m1)} [4][32][16], then W_128^q [128]
+    int mp;                 // mixed-radix path: M' (runtime) and its e^{-j 2 pi t / M'} table
+    const float2* tw_mp;
 };
 
 struct MergeArgs {
