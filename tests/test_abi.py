@@ -71,9 +71,11 @@ def test_host_helpers_match_reference_formulas():
 
 def test_create_rejects_bad_config_without_gpu():
     lib = _native.lib()
-    cfg = _native.OfdmrConfig(1000, 256, 1000, 256, 0, 0, 0, 3, 1e-2, 0, 0)
+    cfg = _native.OfdmrConfig(17 * 19, 256, 17 * 19, 256, 0, 0, 0, 3, 1e-2, 0, 0)
     h = C.c_void_p()
-    assert lib.ofdmr_create(C.byref(cfg), C.byref(h)) == 2   # not a power of two: ConfigError
+    assert lib.ofdmr_create(C.byref(cfg), C.byref(h)) == 2   # prime factors beyond 13: ConfigError
+    cfg = _native.OfdmrConfig(1024, 8192, 1024, 8192, 0, 0, 0, 3, 1e-2, 0, 0)
+    assert lib.ofdmr_create(C.byref(cfg), C.byref(h)) == 2   # above 4096: ConfigError
     cfg = _native.OfdmrConfig(1024, 256, 512, 256, 0, 0, 0, 3, 1e-2, 0, 0)
     assert lib.ofdmr_create(C.byref(cfg), C.byref(h)) == 2   # N' < N (periodogram.cpp:43)
     assert "N'" in _native.last_error()
