@@ -168,7 +168,12 @@ typedef struct ofdmr_sft_config {
     int32_t max_entries;     /* entries kept per frame (<= 64) */
 } ofdmr_sft_config;
 
-/* sft_iterate (sft.cpp:185-459) over a batch of N x M c64 grids h (device).  seeds[f] =
+/* FPS-SFT sizes: N, M in [2, 4096], Q = lcm(N, M) <= 2^20.  Power-of-two Q <= 2048 runs one CTA
+ * per frame in shared memory; any other Q (e.g. table1's 2048 x 560, Q = 71680) keeps each frame's
+ * work arrays in global memory and takes the slice FFTs by Bluestein in the oracle's exact
+ * operation order (oracle.c fft_bluestein), so spectra and decisions stay bit-identical.
+ *
+ * sft_iterate (sft.cpp:185-459) over a batch of N x M c64 grids h (device).  seeds[f] =
  * SftConfig.seed, sigma2[f] = SftConfig.sigma2 (host arrays; the slope / offset draws are made on
  * the device from the seeds).  Outputs (device, [frame][max_entries]): k, l, amplitude (complex
  * double re/im interleaved), n_entries, and per-frame stats (iterations, samples_used, converged,
@@ -215,7 +220,7 @@ int ofdmr_pipeline_sft(ofdmr_context* ctx, const void* y, const void* x_tx, cons
 /* estimate_noise_from_slice, pipeline.cpp:26-43 (run_pipeline's FPS-SFT estimate-noise mode,
  * pipeline.cpp:97-98): per frame, Rng(seeds[f]) draws the admissible slope, the slice of
  * length Q = lcm(N, M) through (0, 0) is FFT'd, sigma2_out[f] = median(|S|^2 / Q^2) * Q / ln 2.
- * seeds on the host, h and sigma2_out on the device (power-of-two N, M, Q <= 2048). */
+ * seeds on the host, h and sigma2_out on the device (sizes as for ofdmr_sft). */
 int ofdmr_sft_estimate_noise(ofdmr_context* ctx, const void* h, int32_t n, int32_t m, const uint64_t* seeds,
                              double* sigma2_out, int64_t frames);
 

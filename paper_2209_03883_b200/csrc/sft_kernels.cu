@@ -51,6 +51,16 @@ struct SftArgs {
     double* residual;
     int32_t* err;     // per-frame overflow flag (synchronous API), or null
     int32_t* status;  // per-frame status, bit 2 = overflow (stream-ordered API), or null
+    // general sizes (Q not a power of two <= 2048): per-CTA work arrays in global memory
+    // (gbuf + blockIdx.x * gstride bytes) and the slice FFT by Bluestein exactly as oracle.c
+    // fft_bluestein: chirp[q], FFT_m of the kernel bker[m], radix-2 twiddles of m for both signs
+    char* gbuf;
+    size_t gstride;
+    int blu_m, blu_logm;
+    const double2* chirp;
+    const double2* bker;
+    const double2* twm_f;
+    const double2* twm_i;
 };
 
 __device__ __forceinline__ double2 dmul(double2 a, double2 b) {
@@ -83,22 +93,27 @@ __device__ __forceinline__ long long pmod(long long a, long long m) {
 }
 
 __device__ __forceinline__ int tone_bin(long long k, long long l, long long v1, long long v2, int n, int m, int q) {
-    // (v1 k Q/N + v2 l Q/M) mod Q with N, M, Q powers of two (the GPU path's precondition):
-    // v1 k (Q/N) mod Q = (Q/N) ((v1 k) mod N), and k < N, v1 < N <= 2048 keep v1 k in 32 bits
-    const unsigned qn = (unsigned)(q / n), qm = (unsigned)(q / m);
-    const unsigned f = (qn * (((unsigned)v1 * (unsigned)k) & (unsigned)(n - 1)) +
-                        qm * (((unsigned)v2 * (unsigned)l) & (unsigned)(m - 1))) &
-                       (unsigned)(q - 1);
+    // sft.cpp:71-81: (v1 k Q/N + v2 l Q/M) mod Q in unsigned 64-bit (k < N, l < M, v < 4096, Q < 2^21:
+    // no overflow); v1 k (Q/N) = (Q/N)((v1 k) mod N) mod Q, so the reduced form is the same value
+    if ((q & (q - 1)) == 0 && q <= 2048) {  // powers of two (N, M | Q): 32-bit masks, same value
+        const unsigned qn = (unsigned)(q / n), qm = (unsigned)(q / m);
+        return (int)((qn * (((unsigned)v1 * (unsigned)k) & (unsigned)(n - 1)) +
+                      qm * (((unsigned)v2 * (unsigned)l) & (unsigned)(m - 1))) &
+                     (unsigned)(q - 1));
+    }
+    const unsigned long long qn = (unsigned long long)(q / n), qm = (unsigned long long)(q / m);
+    const unsigned long long f = ((unsigned long long)v1 * (unsigned long long)k * qn +
+                                  (unsigned long long)v2 * (unsigned long long)l * qm) %
+                                 (unsigned long long)q;
     return (int)f;
 }
 
 __device__ long long egcd(long long a, long long b, long long* x, long long* y) {
-    // iterative form of sft.cpp:85-96 (same Bezout coefficients); the operands here are < Q <= 2048,
-    // so the quotients and the coefficients (|x|, |y| <= Q) are exact in 32-bit arithmetic
-    int aa = (int)a, bb = (int)b, x0 = 1, y0 = 0, x1 = 0, y1 = 1;
+    // iterative form of sft.cpp:85-96 (same Bezout coefficients), 64-bit
+    long long aa = a, bb = b, x0 = 1, y0 = 0, x1 = 0, y1 = 1;
     while (bb != 0) {
-        const int qt = aa / bb;
-        int t = aa - qt * bb; aa = bb; bb = t;
+        const long long qt = aa / bb;
+        long long t = aa - qt * bb; aa = bb; bb = t;
         t = x0 - qt * x1; x0 = x1; x1 = t;
         t = y0 - qt * y1; y0 = y1; y1 = t;
     }
@@ -250,10 +265,37 @@ __device__ double2 targeted(const double2* smp, int cnt, int stride, int f, int 
     return make_double2(acc.x / (double)cnt, acc.y / (double)cnt);
 }
 
+// The forward slice FFT (fft.hpp forward, unscaled) of q points: the oracle's radix-2 schedule
+// for powers of two, otherwise Bluestein in oracle.c fft_bluestein's operation order (chirp
+// multiply, radix-2 FFT_m, kernel multiply, inverse radix-2 FFT_m, 1/m, chirp) on the CTA's
+// global work array: bit-identical spectra for every Q.
+__device__ void sft_fft(double2* x, double2* work, const SftArgs& a) {
+    const int q = a.q;
+    if (a.blu_m == 0) {
+        fft_r2(x, q, a.logq, a.tw_fft);
+        return;
+    }
+    const int mm = a.blu_m;
+    for (int k = threadIdx.x; k < mm; k += kSftNT) work[k] = k < q ? dmul(x[k], a.chirp[k]) : make_double2(0.0, 0.0);
+    __syncthreads();
+    fft_r2(work, mm, a.blu_logm, a.twm_f);
+    for (int k = threadIdx.x; k < mm; k += kSftNT) work[k] = dmul(work[k], a.bker[k]);
+    __syncthreads();
+    fft_r2(work, mm, a.blu_logm, a.twm_i);
+    const double inv_m = 1.0 / (double)mm;
+    for (int k = threadIdx.x; k < q; k += kSftNT) {
+        const double2 c = make_double2(work[k].x * inv_m, work[k].y * inv_m);
+        x[k] = dmul(c, a.chirp[k]);
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int q = a.q, n = a.n, m = a.m;
-    double2* spec = reinterpret_cast<double2*>(smem_raw);   // [q]
+    // work arrays: shared memory for power-of-two Q <= 2048, else this CTA's global slice
+    unsigned char* wbase = a.gbuf ? reinterpret_cast<unsigned char*>(a.gbuf) + (size_t)blockIdx.x * a.gstride : smem_raw;
+    double2* spec = reinterpret_cast<double2*>(wbase);       // [q]
     double2* sp1 = spec + q;                                  // [q] offset spectrum / full slice
     double2* sp2 = sp1 + q;                                   // [q]
     double2* s1d = sp2 + q;                                   // [q/2]
@@ -261,6 +303,8 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
     double* pw = reinterpret_cast<double*>(s2d + q / 2);      // [q]
     int* clist = reinterpret_cast<int*>(pw + q);              // [q]
     int* alias = clist + q;                                   // [q]
+    double2* bwork = reinterpret_cast<double2*>(alias + q + (q & 1));  // [blu_m] Bluestein work (global mode)
+    const bool p2 = ((n & (n - 1)) == 0) && ((m & (m - 1)) == 0);
     __shared__ int s_cand[kMaxCand];
     __shared__ double2 s_c1[kMaxCand], s_c2[kMaxCand];
     __shared__ int s_dkl[kMaxCand];  // decoded (k << 12) | l per candidate, -1 = rejected
@@ -298,12 +342,13 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
 
         // (2) reference slice s0[q] = H[(a1 + v1 q) mod N, (a2 + v2 q) mod M], FFT, 1/Q
         for (int t = tid; t < q; t += kSftNT) {
-            const int r = (int)((a1 + (long long)rs * t) & (n - 1)), c = (int)((a2 + (long long)cs * t) & (m - 1));
+            const long long rr = a1 + (long long)rs * t, cc = a2 + (long long)cs * t;
+            const int r = (int)(p2 ? (rr & (n - 1)) : rr % n), c = (int)(p2 ? (cc & (m - 1)) : cc % m);
             const float2 v = h[(size_t)r * m + c];
             spec[t] = make_double2((double)v.x, (double)v.y);
         }
         __syncthreads();
-        fft_r2(spec, q, a.logq, a.tw_fft);
+        sft_fft(spec, bwork, a);
         for (int t = tid; t < q; t += kSftNT) spec[t] = make_double2(spec[t].x * inv_q, spec[t].y * inv_q);
         // (3) accepted tones' bins and phasors in parallel (s_dkl / s_c1 are free here) ...
         for (int i = tid; i < s_ncomp; i += kSftNT) {
@@ -409,7 +454,8 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
         // (9) offset slices at (r+1, c) and (r, c+1)
         if (g == 1 || s_full) {
             for (int t = tid; t < q; t += kSftNT) {
-                const int r = (int)((a1 + (long long)rs * t) & (n - 1)), c = (int)((a2 + (long long)cs * t) & (m - 1));
+                const long long rr = a1 + (long long)rs * t, cc = a2 + (long long)cs * t;
+                const int r = (int)(p2 ? (rr & (n - 1)) : rr % n), c = (int)(p2 ? (cc & (m - 1)) : cc % m);
                 const int r1 = r + 1 == n ? 0 : r + 1, c1 = c + 1 == m ? 0 : c + 1;
                 const float2 u = h[(size_t)r1 * m + c], w = h[(size_t)r * m + c1];
                 sp1[t] = make_double2((double)u.x, (double)u.y);
@@ -419,7 +465,8 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
         if (g > 1) {
             const int rsd = (int)((v1 * g) % n), csd = (int)((v2 * g) % m);
             for (int t = tid; t < qd; t += kSftNT) {
-                const int r = (int)((a1 + (long long)rsd * t) & (n - 1)), c = (int)((a2 + (long long)csd * t) & (m - 1));
+                const long long rr = a1 + (long long)rsd * t, cc = a2 + (long long)csd * t;
+                const int r = (int)(p2 ? (rr & (n - 1)) : rr % n), c = (int)(p2 ? (cc & (m - 1)) : cc % m);
                 const int r1 = r + 1 == n ? 0 : r + 1, c1 = c + 1 == m ? 0 : c + 1;
                 const float2 u = h[(size_t)r1 * m + c], w = h[(size_t)r * m + c1];
                 s1d[t] = make_double2((double)u.x, (double)u.y);
@@ -428,8 +475,8 @@ __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
         }
         __syncthreads();
         if (g == 1) {
-            fft_r2(sp1, q, a.logq, a.tw_fft);
-            fft_r2(sp2, q, a.logq, a.tw_fft);
+            sft_fft(sp1, bwork, a);
+            sft_fft(sp2, bwork, a);
             for (int t = tid; t < q; t += kSftNT) {
                 sp1[t] = make_double2(sp1[t].x * inv_q, sp1[t].y * inv_q);
                 sp2[t] = make_double2(sp2[t].x * inv_q, sp2[t].y * inv_q);
@@ -736,16 +783,22 @@ __global__ void __launch_bounds__(256) division_noise_kernel(const float2* __res
 }
 
 // pipeline.cpp:26-43 estimate_noise_from_slice: one CTA per frame; the slice through (0, 0)
-// along the host-drawn slope, the oracle's radix-2 fp64 FFT (bit-identical spectrum),
-// p = |s|^2 / Q^2, bitonic sort, p[Q/2] * Q / ln 2.
-__global__ void __launch_bounds__(kSftNT) slice_noise_kernel(const float2* __restrict__ hall, int n, int m, int q,
-                                                             int logq, const int32_t* __restrict__ slopes,
-                                                             const double2* __restrict__ tw, double* __restrict__ out) {
+// along the device-drawn slope, the slice FFT with the oracle's schedule (sft_fft: radix-2 or
+// Bluestein, bit-identical spectrum), p = |s|^2 / Q^2, bitonic sort (padded with +inf to a power
+// of two), p[Q/2] * Q / ln 2.  Work arrays in shared memory for power-of-two Q <= 2048, else in
+// this CTA's slice of a.gbuf.
+__global__ void __launch_bounds__(kSftNT) slice_noise_kernel(SftArgs a, const int32_t* __restrict__ slopes,
+                                                             double* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* sp = reinterpret_cast<double2*>(smem_raw);  // [q]
-    double* pw = reinterpret_cast<double*>(sp + q);       // [q]
+    const int q = a.q, n = a.n, m = a.m;
+    int qp = 1;
+    while (qp < q) qp <<= 1;
+    unsigned char* wbase = a.gbuf ? reinterpret_cast<unsigned char*>(a.gbuf) + (size_t)blockIdx.x * a.gstride : smem_raw;
+    double2* sp = reinterpret_cast<double2*>(wbase);  // [q]
+    double* pw = reinterpret_cast<double*>(sp + q);   // [qp]
+    double2* bwork = reinterpret_cast<double2*>(pw + qp + (qp & 1));
     const int fr = blockIdx.x;
-    const float2* h = hall + (size_t)fr * n * m;
+    const float2* h = a.h + (size_t)fr * n * m;
     const long long v1 = slopes[2 * fr], v2 = slopes[2 * fr + 1];
     for (int t = threadIdx.x; t < q; t += kSftNT) {
         const int r = (int)((v1 * t) % n), c = (int)((v2 * t) % m);
@@ -753,13 +806,13 @@ __global__ void __launch_bounds__(kSftNT) slice_noise_kernel(const float2* __res
         sp[t] = make_double2((double)v.x, (double)v.y);
     }
     __syncthreads();
-    fft_r2(sp, q, logq, tw);
+    sft_fft(sp, bwork, a);
     const double qq = (double)q * (double)q;
-    for (int t = threadIdx.x; t < q; t += kSftNT) pw[t] = dnorm(sp[t]) / qq;
+    for (int t = threadIdx.x; t < qp; t += kSftNT) pw[t] = t < q ? dnorm(sp[t]) / qq : __longlong_as_double(0x7ff0000000000000LL);
     __syncthreads();
-    for (int k = 2; k <= q; k <<= 1)
+    for (int k = 2; k <= qp; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < q; i += kSftNT) {
+            for (int i = threadIdx.x; i < qp; i += kSftNT) {
                 const int ixj = i ^ j;
                 if (ixj > i) {
                     const double a0 = pw[i], a1 = pw[ixj];
@@ -793,23 +846,71 @@ void sft_free(SftScratch& s) {
     cudaFree(s.seeds);
     cudaFree(s.sigma2);
     cudaFree(s.err);
+    cudaFree(s.gbuf);
     for (auto& t : s.tables) {
-        cudaFree(t.second.first);
-        cudaFree(t.second.second);
+        cudaFree(t.second.tw_ref);
+        cudaFree(t.second.tw_fft);
+        cudaFree(t.second.chirp);
+        cudaFree(t.second.bker);
+        cudaFree(t.second.twm_f);
+        cudaFree(t.second.twm_i);
     }
     s = SftScratch{};
 }
 
 namespace {
 
-// Twiddle tables of one Q, built once on the host with the reference's / oracle's libm calls and
-// kept for the life of the context (never rewritten, so stream-ordered launches may use them):
-// first = the rotation table of sft.cpp:29-44 (exact std::polar resync every 256), second = the
-// radix-2 butterfly twiddles of oracle.c fft_pow2.
-int sft_tables(SftScratch& s, int q, const double2** tw_ref, const double2** tw_fft, std::string& err) {
+// radix-2 twiddles of an n-point transform, oracle.c pow2_twiddles: (cos, sin)(sign 2 pi k / n)
+std::vector<double2> r2_twiddles(int n, int sign) {
+    std::vector<double2> t(n / 2 > 0 ? n / 2 : 1);
+    for (int k = 0; k < n / 2; ++k) {
+        const double ang = (double)sign * kTwoPiD * (double)k / (double)n;
+        t[k] = make_double2(std::cos(ang), std::sin(ang));
+    }
+    return t;
+}
+
+// In-place radix-2 FFT with the oracle's schedule (oracle.c fft_pow2: bit reversal, then levels
+// with the top-level twiddles at stride n / len), on the host: the Bluestein kernel transform
+// is built once per Q exactly as the oracle builds it.
+void host_fft_pow2(std::vector<double2>& a, int sign) {
+    const size_t n = a.size();
+    for (size_t i = 1, j = 0; i < n; i++) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    const std::vector<double2> tw = r2_twiddles(int(n), sign);
+    for (size_t len = 2; len <= n; len <<= 1) {
+        const size_t half = len / 2, step = n / len;
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < half; k++) {
+                const double wr = tw[k * step].x, wi = tw[k * step].y;
+                double2& u = a[i + k];
+                double2& v = a[i + k + half];
+                const double vr = v.x * wr - v.y * wi;
+                const double vi = v.x * wi + v.y * wr;
+                v = make_double2(u.x - vr, u.y - vi);
+                u = make_double2(u.x + vr, u.y + vi);
+            }
+    }
+}
+
+template <typename T>
+cudaError_t upload(T** d, const std::vector<T>& h) {
+    cudaError_t e = cudaMalloc(d, sizeof(T) * (h.empty() ? 1 : h.size()));
+    if (e == cudaSuccess && !h.empty()) e = cudaMemcpy(*d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice);
+    return e;
+}
+
+// Tables of one Q, built once on the host with the reference's / oracle's libm calls and kept for
+// the life of the context (never rewritten, so stream-ordered launches may use them).
+int sft_tables(SftScratch& s, int q, const SftScratch::Tables** out, std::string& err) {
     auto it = s.tables.find(q);
     if (it == s.tables.end()) {
-        std::vector<double2> twr(q), twf(q / 2);
+        SftScratch::Tables t;
+        std::vector<double2> twr(q);
         const double sa = -kTwoPiD / double(q);
         double cr = 1.0, ci = 0.0;
         const double sr = std::cos(sa), si = std::sin(sa);
@@ -824,25 +925,76 @@ int sft_tables(SftScratch& s, int q, const double2** tw_ref, const double2** tw_
             cr = nr;
             ci = ni;
         }
-        for (int k = 0; k < q / 2; ++k) {
-            const double ang = (double)(-1) * kTwoPiD * (double)k / (double)q;
-            twf[k] = make_double2(std::cos(ang), std::sin(ang));
+        cudaError_t e = upload(&t.tw_ref, twr);
+        if ((q & (q - 1)) == 0) {
+            if (e == cudaSuccess) e = upload(&t.tw_fft, r2_twiddles(q, -1));
+        } else {
+            // oracle.c fft_bluestein: m, chirp e^{-j pi (k^2 mod 2Q) / Q}, kernel conj(chirp) at k and m - k
+            int mm = 1, lg = 0;
+            while (mm < 2 * q - 1) {
+                mm <<= 1;
+                ++lg;
+            }
+            t.blu_m = mm;
+            t.blu_logm = lg;
+            std::vector<double2> w(q), b(mm, make_double2(0.0, 0.0));
+            for (int k = 0; k < q; k++) {
+                const unsigned long long k2 = ((unsigned long long)k * k) % (2ULL * q);
+                const double ang = (double)(-1) * kTwoPiD * 0.5 * (double)k2 / (double)q;
+                w[k] = make_double2(std::cos(ang), std::sin(ang));
+            }
+            b[0] = make_double2(w[0].x, -w[0].y);
+            for (int k = 1; k < q; k++) b[k] = b[mm - k] = make_double2(w[k].x, -w[k].y);
+            host_fft_pow2(b, -1);
+            if (e == cudaSuccess) e = upload(&t.chirp, w);
+            if (e == cudaSuccess) e = upload(&t.bker, b);
+            if (e == cudaSuccess) e = upload(&t.twm_f, r2_twiddles(mm, -1));
+            if (e == cudaSuccess) e = upload(&t.twm_i, r2_twiddles(mm, +1));
         }
-        double2 *dr = nullptr, *df = nullptr;
-        cudaError_t e = cudaMalloc(&dr, sizeof(double2) * q);
-        if (e == cudaSuccess) e = cudaMalloc(&df, sizeof(double2) * (q / 2 > 0 ? q / 2 : 1));
-        if (e == cudaSuccess) e = cudaMemcpy(dr, twr.data(), sizeof(double2) * q, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemcpy(df, twf.data(), sizeof(double2) * (q / 2), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
-            cudaFree(dr);
-            cudaFree(df);
+            cudaFree(t.tw_ref);
+            cudaFree(t.tw_fft);
+            cudaFree(t.chirp);
+            cudaFree(t.bker);
+            cudaFree(t.twm_f);
+            cudaFree(t.twm_i);
             err = std::string("sft: twiddle tables: ") + cudaGetErrorString(e);
             return OFDMR_ERR_CUDA;
         }
-        it = s.tables.emplace(q, std::make_pair(dr, df)).first;
+        it = s.tables.emplace(q, t).first;
     }
-    *tw_ref = it->second.first;
-    *tw_fft = it->second.second;
+    *out = &it->second;
+    return OFDMR_OK;
+}
+
+// Q handled in shared memory (power of two <= 2048, one CTA per frame); otherwise the CTA's work
+// arrays live in global memory and frames are launched in chunks of kGlobalChunk CTAs
+bool sft_smem_q(int q) { return (q & (q - 1)) == 0 && q <= 2048; }
+constexpr int64_t kGlobalChunk = 296;
+
+size_t sft_gstride(int q, int blu_m) {
+    const size_t bytes = sizeof(double2) * (3 * size_t(q) + size_t(q)) + sizeof(double) * q + sizeof(int) * 2 * q +
+                         8 + sizeof(double2) * size_t(blu_m);
+    return (bytes + 255) & ~size_t(255);
+}
+size_t noise_gstride(int q, int blu_m) {
+    size_t qp = 1;
+    while (qp < size_t(q)) qp <<= 1;
+    const size_t bytes = sizeof(double2) * q + sizeof(double) * qp + 8 + sizeof(double2) * size_t(blu_m);
+    return (bytes + 255) & ~size_t(255);
+}
+
+int ensure_gbuf(SftScratch& s, size_t bytes, std::string& err) {
+    if (s.gbuf && s.cap_gbuf >= int64_t(bytes)) return OFDMR_OK;
+    cudaFree(s.gbuf);
+    s.gbuf = nullptr;
+    s.cap_gbuf = 0;
+    const cudaError_t e = cudaMalloc(&s.gbuf, bytes);
+    if (e != cudaSuccess) {
+        err = std::string("sft: work arrays: ") + cudaGetErrorString(e);
+        return OFDMR_ERR_CUDA;
+    }
+    s.cap_gbuf = int64_t(bytes);
     return OFDMR_OK;
 }
 
@@ -859,21 +1011,35 @@ int upload_seeds(SftScratch& s, cudaStream_t st, const uint64_t* seeds, int64_t 
 
 }  // namespace
 
+namespace {
+int sft_size_check(int n, int m, int q, const char* what, std::string& err) {
+    if (n < 2 || m < 2 || n > 4096 || m > 4096) {
+        err = std::string(what) + ": N and M must lie in [2, 4096] on the GPU path";
+        return OFDMR_ERR_CONFIG;
+    }
+    if (q < 16 || q > (1 << 20)) {
+        err = std::string(what) + ": Q = lcm(N, M) must lie in [16, 2^20] on the GPU path";
+        return OFDMR_ERR_CONFIG;
+    }
+    return OFDMR_OK;
+}
+}  // namespace
+
 int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const ofdmr_sft_config& cfg,
             const uint64_t* seeds, const double* sigma2, bool sigma2_on_device, int32_t* k_out, int32_t* l_out,
             double* amp_out, int32_t* n_entries, int32_t* iterations, int64_t* samples_used, int32_t* converged,
             double* residual, int32_t* status, int64_t frames, int64_t* launches, std::string& err) {
-    auto pow2 = [](int v) { return v >= 2 && (v & (v - 1)) == 0; };
-    if (!pow2(n) || !pow2(m)) { err = "sft: N and M must be powers of two on the GPU path"; return OFDMR_ERR_CONFIG; }
-    const int q = int(lcm_ll(n, m));
-    if (q > 2048 || q < 16) { err = "sft: Q = lcm(N, M) must lie in [16, 2048] on the GPU path"; return OFDMR_ERR_CONFIG; }
+    const long long ql = lcm_ll(n, m);
+    const int q = ql > (1 << 21) ? (1 << 21) : int(ql);
+    int rc = sft_size_check(n, m, q, "sft", err);
+    if (rc) return rc;
     if (cfg.i_max < 0 || cfg.max_entries < 1 || cfg.max_entries > 64 || frames > 65535 * 32) {
         err = "sft: bad i_max / max_entries";
         return OFDMR_ERR_CONFIG;
     }
     const int i_max = cfg.i_max;
     const int iters = i_max > 0 ? i_max : 1;
-    int rc = upload_seeds(s, st, seeds, frames, err);
+    rc = upload_seeds(s, st, seeds, frames, err);
     if (rc) return rc;
     cudaError_t e = ensure(&s.draws, s.cap_draws, frames * iters * 4);
     int64_t cap_s2 = s.cap_frames, cap_err = s.cap_frames;
@@ -893,12 +1059,11 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
         if (e != cudaSuccess) { err = std::string("sft: upload: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
         s2 = s.sigma2;
     }
-    const double2 *tw_ref = nullptr, *tw_fft = nullptr;
-    rc = sft_tables(s, q, &tw_ref, &tw_fft, err);
+    const SftScratch::Tables* tb = nullptr;
+    rc = sft_tables(s, q, &tb, err);
     if (rc) return rc;
 
     SftArgs a{};
-    a.h = h;
     a.n = n;
     a.m = m;
     a.q = q;
@@ -911,27 +1076,50 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
     a.amp_tol = cfg.amp_tol;
     a.decimation = cfg.decimation;
     a.max_entries = cfg.max_entries;
-    a.draws = s.draws;
-    a.sigma2 = s2;
-    a.tw_ref = tw_ref;
-    a.tw_fft = tw_fft;
-    a.k_out = k_out;
-    a.l_out = l_out;
-    a.amp_out = amp_out;
-    a.n_entries = n_entries;
-    a.iterations = iterations;
-    a.samples_used = samples_used;
-    a.converged = converged;
-    a.residual = residual;
-    a.err = status ? nullptr : s.err;
-    a.status = status;
-    const size_t smem = sizeof(double2) * (3 * size_t(q) + size_t(q)) + sizeof(double) * q + sizeof(int) * 2 * q;
+    a.tw_ref = tb->tw_ref;
+    a.tw_fft = tb->tw_fft;
+    a.blu_m = tb->blu_m;
+    a.blu_logm = tb->blu_logm;
+    a.chirp = tb->chirp;
+    a.bker = tb->bker;
+    a.twm_f = tb->twm_f;
+    a.twm_i = tb->twm_i;
+    const bool smem_mode = sft_smem_q(q);
+    size_t smem = 0;
+    int64_t chunk = frames;
+    if (smem_mode) {
+        smem = sizeof(double2) * (3 * size_t(q) + size_t(q)) + sizeof(double) * q + sizeof(int) * 2 * q;
+    } else {
+        a.gstride = sft_gstride(q, tb->blu_m);
+        chunk = std::min<int64_t>(frames, kGlobalChunk);
+        rc = ensure_gbuf(s, a.gstride * size_t(chunk), err);
+        if (rc) return rc;
+        a.gbuf = s.gbuf;
+    }
     e = cudaFuncSetAttribute(sft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) { err = std::string("sft: smem attr: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    sft_kernel<<<unsigned(frames), kSftNT, smem, st>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) { err = std::string("sft: launch: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    if (launches) ++*launches;
+    const int me = cfg.max_entries;
+    for (int64_t f0 = 0; f0 < frames; f0 += chunk) {
+        const int64_t nf = std::min<int64_t>(chunk, frames - f0);
+        SftArgs b = a;
+        b.h = h + f0 * int64_t(n) * m;
+        b.draws = s.draws + f0 * iters * 4;
+        b.sigma2 = s2 + f0;
+        b.k_out = k_out + f0 * me;
+        b.l_out = l_out + f0 * me;
+        b.amp_out = amp_out + 2 * f0 * me;
+        b.n_entries = n_entries + f0;
+        b.iterations = iterations ? iterations + f0 : nullptr;
+        b.samples_used = samples_used ? samples_used + f0 : nullptr;
+        b.converged = converged ? converged + f0 : nullptr;
+        b.residual = residual ? residual + f0 : nullptr;
+        b.err = status ? nullptr : s.err + f0;
+        b.status = status ? status + f0 : nullptr;
+        sft_kernel<<<unsigned(nf), kSftNT, smem, st>>>(b);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) { err = std::string("sft: launch: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
+        if (launches) ++*launches;
+    }
     if (status) return OFDMR_OK;  // stream-ordered: overflow reported in status bit 2
     // no status array: the reference's exception needs the flags now (synchronous)
     std::vector<int32_t> ef(frames);
@@ -945,26 +1133,53 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
 
 int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const uint64_t* seeds,
                     double* sigma2_out, int64_t frames, int64_t* launches, std::string& err) {
-    auto pow2 = [](int v) { return v >= 2 && (v & (v - 1)) == 0; };
-    if (!pow2(n) || !pow2(m)) { err = "estimate_noise_from_slice: N and M must be powers of two on the GPU path"; return OFDMR_ERR_CONFIG; }
-    const int q = int(lcm_ll(n, m));
-    if (q > 2048 || q < 16) { err = "estimate_noise_from_slice: Q = lcm(N, M) must lie in [16, 2048]"; return OFDMR_ERR_CONFIG; }
+    const long long ql = lcm_ll(n, m);
+    const int q = ql > (1 << 21) ? (1 << 21) : int(ql);
+    int rc = sft_size_check(n, m, q, "estimate_noise_from_slice", err);
+    if (rc) return rc;
     if (frames > 0x7fffffff) { err = "estimate_noise_from_slice: too many frames"; return OFDMR_ERR_CONFIG; }
-    int rc = upload_seeds(s, st, seeds, frames, err);
+    rc = upload_seeds(s, st, seeds, frames, err);
     if (rc) return rc;
     cudaError_t e = ensure(&s.draws, s.cap_draws, frames * 4);
     if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    const double2 *tw_ref = nullptr, *tw_fft = nullptr;
-    rc = sft_tables(s, q, &tw_ref, &tw_fft, err);
+    const SftScratch::Tables* tb = nullptr;
+    rc = sft_tables(s, q, &tb, err);
     if (rc) return rc;
     sft_draws_kernel<<<unsigned((frames + 63) / 64), 64, 0, st>>>(s.seeds, int(frames), n, m, 1, 1, s.draws);
-    int logq = 0;
-    while ((1 << logq) < q) ++logq;
-    const size_t smem = sizeof(double2) * q + sizeof(double) * q;
-    slice_noise_kernel<<<unsigned(frames), kSftNT, smem, st>>>(h, n, m, q, logq, s.draws, tw_fft, sigma2_out);
-    e = cudaGetLastError();
+    SftArgs a{};
+    a.n = n;
+    a.m = m;
+    a.q = q;
+    while ((1 << a.logq) < q) ++a.logq;
+    a.tw_fft = tb->tw_fft;
+    a.blu_m = tb->blu_m;
+    a.blu_logm = tb->blu_logm;
+    a.chirp = tb->chirp;
+    a.bker = tb->bker;
+    a.twm_f = tb->twm_f;
+    a.twm_i = tb->twm_i;
+    size_t smem = 0;
+    int64_t chunk = frames;
+    if (sft_smem_q(q)) {
+        smem = sizeof(double2) * q + sizeof(double) * q;
+    } else {
+        a.gstride = noise_gstride(q, tb->blu_m);
+        chunk = std::min<int64_t>(frames, kGlobalChunk);
+        rc = ensure_gbuf(s, a.gstride * size_t(chunk), err);
+        if (rc) return rc;
+        a.gbuf = s.gbuf;
+    }
+    e = cudaFuncSetAttribute(slice_noise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    for (int64_t f0 = 0; f0 < frames && e == cudaSuccess; f0 += chunk) {
+        const int64_t nf = std::min<int64_t>(chunk, frames - f0);
+        SftArgs b = a;
+        b.h = h + f0 * int64_t(n) * m;
+        slice_noise_kernel<<<unsigned(nf), kSftNT, smem, st>>>(b, s.draws + 2 * f0, sigma2_out + f0);
+        e = cudaGetLastError();
+        if (launches) ++*launches;
+    }
     if (e != cudaSuccess) { err = std::string("estimate_noise_from_slice: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
-    if (launches) *launches += 2;
+    if (launches) ++*launches;
     return OFDMR_OK;
 }
 

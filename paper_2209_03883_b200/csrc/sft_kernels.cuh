@@ -22,7 +22,18 @@ struct SftScratch {
     int64_t cap_frames = 0;
     int64_t cap_draws = 0;
     int64_t cap_seeds = 0;
-    std::map<int, std::pair<double2*, double2*>> tables;  // Q -> (rotation table, radix-2 twiddles)
+    struct Tables {
+        double2* tw_ref = nullptr;  // [Q] rotation table (sft.cpp:29-44)
+        double2* tw_fft = nullptr;  // [Q/2] radix-2 twiddles (power-of-two Q)
+        int blu_m = 0, blu_logm = 0;  // Bluestein (other Q): FFT length m = 2^ceil(log2(2Q - 1))
+        double2* chirp = nullptr;   // [Q]
+        double2* bker = nullptr;    // [m] FFT_m of the conjugate-chirp kernel
+        double2* twm_f = nullptr;   // [m/2] radix-2 twiddles, both signs
+        double2* twm_i = nullptr;
+    };
+    std::map<int, Tables> tables;   // per Q, built once
+    char* gbuf = nullptr;           // per-CTA global work arrays (general Q)
+    int64_t cap_gbuf = 0;           // bytes
 };
 
 void sft_free(SftScratch& s);
