@@ -290,11 +290,13 @@ __device__ void sft_fft(double2* x, double2* work, const SftArgs& a) {
     __syncthreads();
 }
 
+// GMEM: work arrays in this CTA's global slice (general Q) instead of shared memory (power-of-two
+// Q <= 2048); a compile-time choice so the shared-memory build keeps LDS/STS addressing
+template <bool GMEM>
 __global__ void __launch_bounds__(kSftNT) sft_kernel(SftArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int q = a.q, n = a.n, m = a.m;
-    // work arrays: shared memory for power-of-two Q <= 2048, else this CTA's global slice
-    unsigned char* wbase = a.gbuf ? reinterpret_cast<unsigned char*>(a.gbuf) + (size_t)blockIdx.x * a.gstride : smem_raw;
+    unsigned char* wbase = GMEM ? reinterpret_cast<unsigned char*>(a.gbuf) + (size_t)blockIdx.x * a.gstride : smem_raw;
     double2* spec = reinterpret_cast<double2*>(wbase);       // [q]
     double2* sp1 = spec + q;                                  // [q] offset spectrum / full slice
     double2* sp2 = sp1 + q;                                   // [q]
@@ -787,13 +789,14 @@ __global__ void __launch_bounds__(256) division_noise_kernel(const float2* __res
 // Bluestein, bit-identical spectrum), p = |s|^2 / Q^2, bitonic sort (padded with +inf to a power
 // of two), p[Q/2] * Q / ln 2.  Work arrays in shared memory for power-of-two Q <= 2048, else in
 // this CTA's slice of a.gbuf.
+template <bool GMEM>
 __global__ void __launch_bounds__(kSftNT) slice_noise_kernel(SftArgs a, const int32_t* __restrict__ slopes,
                                                              double* __restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int q = a.q, n = a.n, m = a.m;
     int qp = 1;
     while (qp < q) qp <<= 1;
-    unsigned char* wbase = a.gbuf ? reinterpret_cast<unsigned char*>(a.gbuf) + (size_t)blockIdx.x * a.gstride : smem_raw;
+    unsigned char* wbase = GMEM ? reinterpret_cast<unsigned char*>(a.gbuf) + (size_t)blockIdx.x * a.gstride : smem_raw;
     double2* sp = reinterpret_cast<double2*>(wbase);  // [q]
     double* pw = reinterpret_cast<double*>(sp + q);   // [qp]
     double2* bwork = reinterpret_cast<double2*>(pw + qp + (qp & 1));
@@ -1096,7 +1099,8 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
         if (rc) return rc;
         a.gbuf = s.gbuf;
     }
-    e = cudaFuncSetAttribute(sft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    auto kern = smem_mode ? sft_kernel<false> : sft_kernel<true>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) { err = std::string("sft: smem attr: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
     const int me = cfg.max_entries;
     for (int64_t f0 = 0; f0 < frames; f0 += chunk) {
@@ -1115,7 +1119,7 @@ int sft_run(SftScratch& s, cudaStream_t st, const float2* h, int n, int m, const
         b.residual = residual ? residual + f0 : nullptr;
         b.err = status ? nullptr : s.err + f0;
         b.status = status ? status + f0 : nullptr;
-        sft_kernel<<<unsigned(nf), kSftNT, smem, st>>>(b);
+        kern<<<unsigned(nf), kSftNT, smem, st>>>(b);
         e = cudaGetLastError();
         if (e != cudaSuccess) { err = std::string("sft: launch: ") + cudaGetErrorString(e); return OFDMR_ERR_CUDA; }
         if (launches) ++*launches;
@@ -1160,7 +1164,9 @@ int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int 
     a.twm_i = tb->twm_i;
     size_t smem = 0;
     int64_t chunk = frames;
-    if (sft_smem_q(q)) {
+    const bool smem_mode = sft_smem_q(q);
+    auto kern = smem_mode ? slice_noise_kernel<false> : slice_noise_kernel<true>;
+    if (smem_mode) {
         smem = sizeof(double2) * q + sizeof(double) * q;
     } else {
         a.gstride = noise_gstride(q, tb->blu_m);
@@ -1169,12 +1175,12 @@ int sft_slice_noise(SftScratch& s, cudaStream_t st, const float2* h, int n, int 
         if (rc) return rc;
         a.gbuf = s.gbuf;
     }
-    e = cudaFuncSetAttribute(slice_noise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     for (int64_t f0 = 0; f0 < frames && e == cudaSuccess; f0 += chunk) {
         const int64_t nf = std::min<int64_t>(chunk, frames - f0);
         SftArgs b = a;
         b.h = h + f0 * int64_t(n) * m;
-        slice_noise_kernel<<<unsigned(nf), kSftNT, smem, st>>>(b, s.draws + 2 * f0, sigma2_out + f0);
+        kern<<<unsigned(nf), kSftNT, smem, st>>>(b, s.draws + 2 * f0, sigma2_out + f0);
         e = cudaGetLastError();
         if (launches) ++*launches;
     }
