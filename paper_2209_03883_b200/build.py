@@ -48,7 +48,6 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
         "mixed_kernels": [],
         "fast_kernels": [],
         "fused_ce": [],
-        "fused_pg": [],
         "fused_pg2": [],
         "fused_pg3": [],
         "rowpass_zp": [],

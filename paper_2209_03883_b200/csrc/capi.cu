@@ -46,9 +46,6 @@ struct PersistArgs {
 cudaError_t launch_pgram_persist(const PersistArgs& pa, bool ls, bool win, int grid, cudaStream_t st);
 
 cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st);
-cudaError_t launch_fused_pg(const PgArgs& a, bool hamming, int grid, cudaStream_t st);
-int fused_pg_max_clusters();
-int fused_pg_cluster();
 size_t noise_select_scratch_bytes(int64_t frames);
 cudaError_t launch_map_pgm(const float* p, int64_t count, uint8_t* out, int64_t frames, double* scratch,
                            cudaStream_t st, int64_t* launches);
@@ -64,6 +61,8 @@ size_t fused_pg3_scratch_elems(int groups);
 int fused_pg2_max_groups();
 bool mixed_size_supported(int len);
 int mixed_col_tile(int np, int m);
+cudaError_t launch_ofdm_mixed(bool inverse, const float2* in, float2* out, int n, int m, int ncp, int64_t frames,
+                              const float2* tw_n, cudaStream_t st);
 size_t fused_pg2_counter_ints(int groups);
 size_t fused_pg2_scratch_elems(int groups);
 }  // namespace ofdmr
@@ -121,9 +120,6 @@ struct ofdmr_context {
     bool fused = false;          // + DFT-CE with 0 < L <= 128: persistent one-frame-per-CTA kernel
     bool force_general = false;  // set by ofdmr_pipeline_general for one call
     int fused_grid = 0;
-    int pg_clusters = 0;              // fused periodogram: co-resident 8-CTA clusters
-    float2* pg_scratch = nullptr;     // fused periodogram: per-cluster 1024 x 256 G (L2)
-    int* pg_counters = nullptr;       // fused periodogram: per-group barrier counters
     int pg2_groups = 0;               // warp-specialised periodogram: 16-CTA frame groups
     float2* pg2_scratch = nullptr;    // per group 2 x 1024 x 256 G (L2)
     int* pg2_counters = nullptr;      // per group progress counters
@@ -737,8 +733,6 @@ void ofdmr_destroy(ofdmr_context* c) {
     cudaFree(c->tw1024_t);
     cudaFree(c->tw256_t);
     cudaFree(c->dscratch);
-    cudaFree(c->pg_scratch);
-    cudaFree(c->pg_counters);
     cudaFree(c->pg2_scratch);
     cudaFree(c->pg2_counters);
     cudaFree(c->pg3_scratch);
@@ -904,7 +898,7 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
     (void)chunk;
     const bool pg_shape = c->fast && g.n_subcarriers == 1024 && g.n_symbols == 256 && g.n_prime == 1024 &&
                           g.m_prime == 256 && getenv("OFDMR_PG_PERSIST") == nullptr;
-    if (pg_shape && getenv("OFDMR_PG_V1") == nullptr && getenv("OFDMR_PG2") == nullptr) {
+    if (pg_shape && getenv("OFDMR_PG2") == nullptr) {
         // split-radix exchange periodogram (fused_pg3.cu): column warps DFT_32 + twiddle, row
         // warps DFT_32 + FFT_256, 8-CTA frame groups, double-buffered G in L2
         if (!c->pg3_scratch) {
@@ -939,9 +933,9 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
         }
         return OFDMR_OK;
     }
-    if (pg_shape && getenv("OFDMR_PG_V1") == nullptr) {
-        // warp-specialised single-launch periodogram (16-CTA frame groups, column and row
-        // warps concurrent, double-buffered G in L2)
+    if (pg_shape) {
+        // OFDMR_PG2=1: the previous warp-specialised kernel (whole IFFT_1024 on the column warps),
+        // kept as an independent cross-check of fused_pg3 (tests/test_gpu_parity.py)
         if (!c->pg2_scratch) {
             c->pg2_groups = fused_pg2_max_groups();
             if (c->pg2_groups <= 0) return fail(OFDMR_ERR_CUDA, "fused periodogram: no co-resident frame group");
@@ -970,41 +964,6 @@ int ofdmr_periodogram(ofdmr_context* c, const void* h, float* p, int64_t frames)
                 e = launch_fused_pg2(pa, win, int(std::min<int64_t>(c->pg2_groups, nf)), c->pg2_groups, c->stream);
             }
             if (e != cudaSuccess) return cuda_fail(e, "fused_pg2");
-            ++c->launches;
-        }
-        return OFDMR_OK;
-    }
-    if (pg_shape) {
-        // fused single-launch periodogram (8-CTA cluster per frame, G in L2)
-        if (!c->pg_scratch) {
-            c->pg_clusters = fused_pg_max_clusters();
-            if (c->pg_clusters <= 0) return fail(OFDMR_ERR_CUDA, "fused periodogram: no co-resident cluster");
-            OFDMR_CUDA(cudaMalloc(&c->pg_scratch, sizeof(float2) * 1024 * 256 * size_t(c->pg_clusters)));
-            OFDMR_CUDA(cudaMalloc(&c->pg_counters, sizeof(int) * size_t(c->pg_clusters)));
-        }
-        OFDMR_CUDA(cudaMemsetAsync(c->pg_counters, 0, sizeof(int) * size_t(c->pg_clusters), c->stream));
-        PgArgs pa{};
-        pa.h = static_cast<const float2*>(h);
-        pa.p = p;
-        const bool win = g.window == OFDMR_WINDOW_HAMMING;
-        pa.wk = win ? c->wk : nullptr;
-        pa.wl = win ? c->wl : nullptr;
-        pa.tw1024_t = c->tw1024_t;
-        pa.tw256_t = c->tw256_t;
-        pa.gscratch = c->pg_scratch;
-        pa.group_counters = c->pg_counters;
-        pa.scale = c->scale;
-        for (int64_t f0 = 0; f0 < frames; f0 += (int64_t)1 << 30) {
-            const int64_t nf = std::min<int64_t>((int64_t)1 << 30, frames - f0);
-            pa.h = static_cast<const float2*>(h) + fc * f0;
-            pa.p = p + pframe * f0;
-            pa.frames = int(nf);
-            cudaError_t e;
-            {
-                StageTimer t(c, 0, c->stream);
-                e = launch_fused_pg(pa, win, fused_pg_cluster() * int(std::min<int64_t>(c->pg_clusters, nf)), c->stream);
-            }
-            if (e != cudaSuccess) return cuda_fail(e, "fused_pg");
             ++c->launches;
         }
         return OFDMR_OK;
@@ -1154,11 +1113,13 @@ static int ofdm_impl(ofdmr_context* c, bool inverse, const void* in, void* out, 
     if (frames <= 0) return OFDMR_OK;
     const ofdmr_config& g = c->cfg;
     if (g.n_cp < 0 || g.n_cp > g.n_subcarriers) return fail(OFDMR_ERR_CONFIG, "n_cp must lie in [0, N]");
-    if (!pow2_in(g.n_subcarriers, 16, 4096))
-        return fail(OFDMR_ERR_CONFIG, std::string(what) + ": N must be a power of two in [16, 4096] on the GPU path");
     OFDMR_CUDA(cudaSetDevice(c->device));
-    const cudaError_t e = ofdmr::launch_ofdm(inverse, static_cast<const float2*>(in), static_cast<float2*>(out),
-                                             g.n_subcarriers, g.n_symbols, g.n_cp, frames, c->tw, c->stream);
+    const cudaError_t e =
+        pow2_in(g.n_subcarriers, 16, 4096)
+            ? ofdmr::launch_ofdm(inverse, static_cast<const float2*>(in), static_cast<float2*>(out), g.n_subcarriers,
+                                 g.n_symbols, g.n_cp, frames, c->tw, c->stream)
+            : ofdmr::launch_ofdm_mixed(inverse, static_cast<const float2*>(in), static_cast<float2*>(out),
+                                       g.n_subcarriers, g.n_symbols, g.n_cp, frames, c->tw_n, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, what);
     ++c->launches;
     return OFDMR_OK;
@@ -1583,9 +1544,7 @@ int ofdmr_pipeline_sft(ofdmr_context* c, const void* y, const void* x_tx, const 
 extern "C" long long ofdmr_debug_info(ofdmr_context* c, const char* key) {
     if (!c || !key) return -1;
     const std::string k(key);
-    if (k == "pg_clusters") return c->pg_clusters;
     if (k == "fused_grid") return c->fused_grid;
-    if (k == "pg_max_clusters") return ofdmr::fused_pg_max_clusters();
     if (k == "pg2_max_groups") return ofdmr::fused_pg2_max_groups();
     return -1;
 }

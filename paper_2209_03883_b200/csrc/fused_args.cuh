@@ -39,20 +39,6 @@ constexpr int kFusedPend = 2048;  // pending edge candidates per CTA per frame
 
 namespace ofdmr {
 
-// Launch arguments of the fused batched periodogram (fused_pg.cu).
-struct PgArgs {
-    const float2* h;           // [frames][1024][256] channel estimates
-    float* p;                  // [frames][1024][256] periodogram (Doppler fftshifted)
-    const float* wk;           // subcarrier / symbol windows (Hamming only)
-    const float* wl;
-    const float2* tw1024_t;
-    const float2* tw256_t;
-    float2* gscratch;          // per cluster 1024 x 256 intermediate (L2 resident)
-    int* group_counters;       // per frame group barrier counter (zeroed before each launch)
-    int frames;
-    float scale;               // 1 / (N M)
-};
-
 // Launch arguments of the warp-specialised batched periodogram (fused_pg2.cu).
 struct Pg2Args {
     const float2* h;           // [frames][1024][256] channel estimates

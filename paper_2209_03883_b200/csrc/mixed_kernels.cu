@@ -7,6 +7,7 @@
 // mixed-radix Stockham engine in shared memory: radices 8, 4, 2, 3, 5, 7, 11, 13 (each pass a
 // compile-time radix picked by a switch), twiddles from a per-length fp32 table
 // e^{-j 2 pi t / L} built in fp64 on the host.  Lengths must factor into those primes.
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -308,6 +309,51 @@ __global__ void __launch_bounds__(kMrNT) mr_rowpass_kernel(RowArgs a, MrPlan pmp
     for (int i = threadIdx.x; i < a.kmax; i += kMrNT) out[i] = s_top[i];
 }
 
+// OFDM front end (waveform.cpp:133-166) for a non-power-of-two N: one CTA per (frame, tile of
+// C symbols), demodulate = strip the cyclic prefix + unscaled FFT_N, modulate = IFFT_N x 1/N with
+// the last n_cp samples as prefix (see ofdm_kernels.cu for the power-of-two version)
+__global__ void __launch_bounds__(kMrNT) mr_ofdm_kernel(bool inverse, const float2* __restrict__ in,
+                                                        float2* __restrict__ out, int n, int m, int ncp, int ntiles,
+                                                        int C, MrPlan pn, const float2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int VS = n + 1;
+    float2* bufA = reinterpret_cast<float2*>(smem_raw);
+    float2* bufB = bufA + (size_t)C * VS;
+    const int64_t frame = blockIdx.x / ntiles;
+    const int l0 = (int)(blockIdx.x % ntiles) * C;
+    const int64_t ns = n + ncp;
+    if (!inverse) {
+        const float2* src = in + frame * (int64_t)m * ns;
+        for (int idx = threadIdx.x; idx < C * n; idx += kMrNT) {
+            const int c = idx / n, i = idx - c * n, l = l0 + c;
+            bufA[c * VS + i] = l < m ? src[(int64_t)l * ns + ncp + i] : make_float2(0.f, 0.f);
+        }
+        __syncthreads();
+        const float2* res = mr_fft<false>(bufA, bufB, VS, C, pn, tw);
+        float2* dst = out + frame * (int64_t)n * m;
+        for (int idx = threadIdx.x; idx < C * n; idx += kMrNT) {
+            const int k = idx / C, c = idx - k * C, l = l0 + c;
+            if (l < m) dst[(int64_t)k * m + l] = res[c * VS + k];
+        }
+    } else {
+        const float2* src = in + frame * (int64_t)n * m;
+        for (int idx = threadIdx.x; idx < C * n; idx += kMrNT) {
+            const int k = idx / C, c = idx - k * C, l = l0 + c;
+            bufA[c * VS + k] = l < m ? src[(int64_t)k * m + l] : make_float2(0.f, 0.f);
+        }
+        __syncthreads();
+        const float2* res = mr_fft<true>(bufA, bufB, VS, C, pn, tw);
+        const float inv_n = 1.0f / float(n);
+        float2* dst = out + frame * (int64_t)m * ns;
+        for (int idx = threadIdx.x; idx < C * (int)ns; idx += kMrNT) {
+            const int c = idx / (int)ns, j = idx - c * (int)ns, l = l0 + c;
+            if (l >= m) continue;
+            const int i = j < ncp ? n - ncp + j : j - ncp;
+            dst[(int64_t)l * ns + j] = cscale(res[c * VS + i], inv_n);
+        }
+    }
+}
+
 bool mr_factor(int len, MrPlan& p) {
     p.len = len;
     p.npass = 0;
@@ -361,6 +407,31 @@ cudaError_t launch_rowpass_mixed(const RowArgs& a, int frames, cudaStream_t st) 
     if (e != cudaSuccess) return e;
     mr_rowpass_kernel<<<dim3((a.n_prime + a.rows_per_block - 1) / a.rows_per_block, frames), kMrNT, smem, st>>>(
         a, p, a.mp + 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ofdm_mixed(bool inverse, const float2* in, float2* out, int n, int m, int ncp, int64_t frames,
+                              const float2* tw_n, cudaStream_t st) {
+    MrPlan pn;
+    if (!mr_factor(n, pn) || !tw_n) return cudaErrorInvalidValue;
+    int C = 1;
+    for (int c : {8, 4, 2})
+        if (size_t(2) * c * (n + 1) * sizeof(float2) <= 100 * 1024) {
+            C = c;
+            break;
+        }
+    const int ntiles = (m + C - 1) / C;
+    const size_t smem = size_t(2) * C * (n + 1) * sizeof(float2);
+    cudaError_t e = cudaFuncSetAttribute(mr_ofdm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    for (int64_t f0 = 0; f0 < frames;) {
+        const int64_t nf = std::min<int64_t>(frames - f0, (int64_t)(0x7fffffff / ntiles));
+        const int64_t in_stride = inverse ? (int64_t)n * m : (int64_t)m * (n + ncp);
+        const int64_t out_stride = inverse ? (int64_t)m * (n + ncp) : (int64_t)n * m;
+        mr_ofdm_kernel<<<(unsigned)(nf * ntiles), kMrNT, smem, st>>>(inverse, in + f0 * in_stride, out + f0 * out_stride,
+                                                                    n, m, ncp, ntiles, C, pn, tw_n);
+        f0 += nf;
+    }
     return cudaGetLastError();
 }
 

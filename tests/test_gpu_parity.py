@@ -454,16 +454,16 @@ def test_gpu_generator_matches_cpu_generator(cuda, cfg):
 
 @pytest.mark.parametrize("window,F", [(0, 5), (1, 300)])
 def test_fused_periodogram_matches_two_pass_kernel(cuda, window, F, monkeypatch):
-    """The warp-specialised TMA periodogram (default at 1024 x 256) against the previous
-    single-launch kernel (OFDMR_PG_V1) on every frame: fewer frames than frame groups, and
-    many frames per group (double-buffered G reused ~16 times)."""
+    """The split-exchange periodogram (fused_pg3, default at 1024 x 256) against the previous
+    warp-specialised kernel (fused_pg2, OFDMR_PG2) on every frame: fewer frames than frame
+    groups, and many frames per group (double-buffered G reused ~16 times)."""
     n, m = 1024, 256
     rng = np.random.default_rng(5 + F)
     base = (rng.standard_normal((min(F, 37), n, m)) + 1j * rng.standard_normal((min(F, 37), n, m))).astype(np.complex64)
     h = np.concatenate([base] * (-(-F // len(base))))[:F] * np.linspace(0.5, 2.0, F, dtype=np.float32)[:, None, None]
     with Receiver(n, m, window=window) as rx:
         p = rx.periodogram(h).cpu().numpy()
-        monkeypatch.setenv("OFDMR_PG_V1", "1")
+        monkeypatch.setenv("OFDMR_PG2", "1")
         q = rx.periodogram(h).cpu().numpy()
     for f in range(F):
         assert np.abs(p[f] - q[f]).max() / q[f].max() <= MAP_TOL, f
@@ -525,7 +525,7 @@ def _estimate_noise_parity(cfg):
 
 
 @pytest.mark.parametrize("n,m,ncp", [(1024, 256, 128), (2048, 16, 256), (4096, 16, 1024), (16, 16, 0), (64, 16, 64),
-                                     (256, 32, 7)])
+                                     (256, 32, 7), (560, 28, 140), (2048, 20, 512), (200, 16, 50)])
 def test_ofdm_front_end_matches_oracle(cuda, n, m, ncp):
     """§8(f) item 3, the OFDM time-domain front end (waveform.cpp:133-166): GPU ofdm_modulate
     and ofdm_demodulate against the oracle restatement on identical c64 inputs (fp32 FFT:
@@ -646,7 +646,7 @@ def test_fused_periodogram_many_frames_on_device(cuda, window, monkeypatch):
     h *= torch.linspace(0.5, 2.0, F, device="cuda")[:, None, None]
     with Receiver(n, m, window=window) as rx:
         p = rx.periodogram(h)
-        monkeypatch.setenv("OFDMR_PG_V1", "1")
+        monkeypatch.setenv("OFDMR_PG2", "1")
         q = rx.periodogram(h)
     err = ((p - q).abs().amax(dim=(1, 2)) / q.amax(dim=(1, 2))).max().item()
     assert err <= MAP_TOL, err

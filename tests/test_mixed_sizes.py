@@ -102,7 +102,7 @@ def test_mixed_limits_are_config_errors(cuda):
     with pytest.raises(ConfigError):
         Receiver(17 * 19, 32)  # prime factors outside 2, 3, 5, 7, 11, 13
     with Receiver(560, 32, n_cp=16) as rx:
-        with pytest.raises(ConfigError):
-            rx.ofdm_demodulate(torch.zeros(32 * (560 + 16), dtype=torch.complex64))
-        with pytest.raises(ConfigError):
-            rx.sft(torch.zeros(560, 32, dtype=torch.complex64), [1], [0.1])
+        with pytest.raises(ConfigError):  # N above 4096 on the FPS-SFT path
+            rx.sft(torch.zeros(4100, 2, dtype=torch.complex64), [1], [0.1])
+        with pytest.raises(ConfigError):  # Q = lcm(N, M) = 4093 x 4091 above 2^20
+            rx.sft(torch.zeros(4093, 4091, dtype=torch.complex64), [1], [0.1])
