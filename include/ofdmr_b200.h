@@ -23,7 +23,7 @@
  * two), N' >= N, M' >= M (periodogram.cpp:43, ConfigError otherwise), max_targets <= 64.
  * Powers of two in [16, 4096] with N' in {N, 2N, 4N} run the specialised power-of-two kernels
  * (and the fused ones at 1024 x 256); every other shape the mixed-radix kernels
- * (csrc/mixed_kernels.cu).  The OFDM front end needs a power-of-two N; FPS-SFT see below.
+ * (csrc/mixed_kernels.cu), the OFDM front end included; FPS-SFT limits see below.
  *
  * Threading: one context per host thread or stream (the reference functions are
  * reentrant; this context owns scratch buffers).
