@@ -46,6 +46,7 @@ def build_cuda(force: bool = False, verbose_ptxas: bool = False) -> Path:
     units = {
         "radar_kernels": [],
         "mixed_kernels": [],
+        "colpass2048": [],
         "fast_kernels": [],
         "fused_ce": [],
         "fused_pg2": [],

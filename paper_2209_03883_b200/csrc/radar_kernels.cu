@@ -14,6 +14,8 @@
 //     strict local maxima are never 8-adjacent; SURVEY.md §7 hard part 1).
 //   merge: per-frame top-K over the block candidates -> detection records.
 #include "fft_smem.cuh"
+#include <cstdlib>
+
 #include "radar_kernels.cuh"
 
 namespace ofdmr {
@@ -345,8 +347,15 @@ cudaError_t launch_colpass_n(const ColArgs& a, int np, int frames, cudaStream_t 
 cudaError_t launch_colpass_mixed(const ColArgs& a, int frames, cudaStream_t st);
 cudaError_t launch_rowpass_mixed(const RowArgs& a, int frames, cudaStream_t st);
 
+bool colpass2048_applies(const ColArgs& a, int n, int np);
+cudaError_t launch_colpass2048(const ColArgs& a, int frames, cudaStream_t st);
+
 cudaError_t launch_colpass(const ColArgs& a, int n, int np, int frames, cudaStream_t st) {
     if (a.tw_n != nullptr) return launch_colpass_mixed(a, frames, st);  // sizes not powers of two
+    // cfg2's 2048 -> 4096 column pass on register warp FFTs (colpass2048.cu); OFDMR_COL2048=0 keeps
+    // the generic Stockham kernel (cross-check)
+    const char* e2048 = getenv("OFDMR_COL2048");
+    if (!(e2048 && e2048[0] == '0') && colpass2048_applies(a, n, np)) return launch_colpass2048(a, frames, st);
     switch (n) {
         case 16: return launch_colpass_n<16>(a, np, frames, st);
         case 32: return launch_colpass_n<32>(a, np, frames, st);

@@ -619,6 +619,45 @@ def test_sft_estimate_noise_from_slice(cuda, n, m):
         assert got[f] == ref, (f, got[f], ref)
 
 
+@pytest.mark.parametrize("variant", ["dft_ce_L201", "ls_rect"])
+def test_pipeline_cfg2_column_variants(cuda, variant):
+    """cfg2's register-FFT column pass (colpass2048.cu) off its default: an odd tap count L = 201
+    (part of the last tap block masked) and the plain LS estimator with a rectangular window."""
+    if variant == "dft_ce_L201":
+        cfg = configs.CFG2.replace(n_cp=201)
+    else:
+        cfg = configs.CFG2.replace(estimator=configs.EST_LS, window=configs.WINDOW_RECT)
+    _pipeline_parity(cfg, 2)
+
+
+def test_colpass2048_matches_generic_column_pass(cuda, monkeypatch):
+    """The cfg2 column pass (warp FFT_1024 chain) against the generic shared-memory Stockham
+    column pass (OFDMR_COL2048=0) on the same 6 ZC-precoded frames: maps, sigma_h^2, detections."""
+    cfg = configs.CFG2
+    fb = gen.frames(cfg, 20, 6)
+    with Receiver.from_config(cfg) as rx:
+        d1, p1 = rx.pipeline(fb.y, fb.x, fb.sigma2, want_map=True)
+        monkeypatch.setenv("OFDMR_COL2048", "0")
+        d0, p0 = rx.pipeline(fb.y, fb.x, fb.sigma2, want_map=True)
+        torch.cuda.synchronize()
+    p0, p1 = p0.cpu().numpy(), p1.cpu().numpy()
+    for f in range(6):
+        assert np.abs(p1[f] - p0[f]).max() <= 2e-5 * p0[f].max(), f
+        assert [(a, b) for a, b, _ in d1.frame(f)] == [(a, b) for a, b, _ in d0.frame(f)], f
+    s1, s0 = d1.sigma2_h.cpu().numpy(), d0.sigma2_h.cpu().numpy()
+    assert np.abs(s1 - s0).max() <= 1e-12 * s0.max()  # same terms, 8- vs 2-column tile sums
+
+
+def test_pipeline_cfg2_zero_cell_raises(cuda):
+    cfg = configs.CFG2
+    fb = gen.frames(cfg, 0, 2)
+    x = fb.x.copy()
+    x[1, 1500, 300] = 0
+    with Receiver.from_config(cfg) as rx:
+        with pytest.raises(ConfigError):
+            rx.pipeline(fb.y, x, fb.sigma2)
+
+
 def test_rowpass_zp_matches_generic_rowpass(cuda):
     # cfg2's zero-padded row pass (rowpass_zp.cu: 4 x FFT_512 per row, K <= 8) against the generic
     # shared-memory row pass (taken for K > 8) on the same 12 ZC-precoded frames
