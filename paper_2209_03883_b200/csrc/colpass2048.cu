@@ -220,14 +220,11 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
 #pragma unroll 1
         for (int sx = 0; sx < 4; ++sx) {
             float2 v[32];
+            const float jc = sx == 0 ? 1.f : sx == 2 ? -1.f : 0.f, js = sx == 1 ? 1.f : sx == 3 ? -1.f : 0.f;  // j^s
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
                 const int q = lane + 32 * i;
-                const float2 h1 = hreg[i];
-                // j^s H'[q + 1024]
-                const float2 r = sx == 0 ? h1 : sx == 1 ? make_float2(-h1.y, h1.x)
-                               : sx == 2 ? make_float2(-h1.x, -h1.y) : make_float2(h1.y, -h1.x);
-                float2 y = cadd(col[lane + 33 * i], r);
+                float2 y = cfma_cs(jc, js, hreg[i], col[lane + 33 * i]);  // H'[q] + j^s H'[q + 1024]
                 if (sx) {
                     float2 wv = __ldg(tw4 + sx * q);  // W_4096^{sq}, conjugated: inverse
                     wv.y = -wv.y;

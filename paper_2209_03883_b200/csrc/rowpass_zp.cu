@@ -95,10 +95,9 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
             float2 v[32];
 #pragma unroll
             for (int n = 0; n < 32; ++n) v[n] = __ldg(grow + j + 16 * n);
-            if (m1 != 0) {
+            // m1 = 0 multiplies by pre[0] = 1 exactly: no divergent branch between the half-warps
 #pragma unroll
-                for (int n = 1; n < 32; ++n) v[n] = cmul(v[n], s.pre[(m1 * n) & 127]);
-            }
+            for (int n = 1; n < 32; ++n) v[n] = cmul(v[n], s.pre[(m1 * n) & 127]);
             dft32<false>(v);
             const float2* pw = s.post[m1] + j;
 #pragma unroll
@@ -115,9 +114,10 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
                 for (int jj = 0; jj < 16; ++jj) w[jj] = sc[k1 * 16 + (jj ^ j)];
                 dft16<false>(w);
                 // X[m1 + 4 (k1 + 32 k2)], fft-shifted by M'/2
-                const int base = m1 + 4 * k1 + kZMP / 2;
+                // zp_phys only flips bit 1 from bit 5, which the 128 k2 steps leave unchanged
+                const int base = zp_phys(m1 + 4 * k1 + kZMP / 2);
 #pragma unroll
-                for (int k2 = 0; k2 < 16; ++k2) prow[zp_phys((base + 128 * k2) & (kZMP - 1))] = cnorm(w[k2]) * a.scale;
+                for (int k2 = 0; k2 < 16; ++k2) prow[(base + 128 * k2) & (kZMP - 1)] = cnorm(w[k2]) * a.scale;
             }
             __syncwarp();  // the slot is rewritten by the next pass
         }
