@@ -49,22 +49,27 @@ __device__ __forceinline__ int zp_phys(int m) { return m ^ (((m >> 5) & 1) << 1)
 
 }  // namespace
 
-__global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
+__global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a, int frames) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ZpSmem& s = *reinterpret_cast<ZpSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int hw = tid >> 4, j = tid & 15, hsel = (tid >> 4) & 1;
-    const int f = blockIdx.y, rb = blockIdx.x, np = a.n_prime, r0 = rb * kZR;
-    const int nrows = min(kZR, np - r0), TR = nrows + 2;
+    const int np = a.n_prime;
+    const int nblk = (np + kZR - 1) / kZR;
 
-    // twiddle tables (host-built, zp_tw layout: post[4][512] then pre[128])
+    // twiddle tables (host-built, zp_tw layout: post[4][512] then pre[128]), once per CTA
     {
         const float4* src = reinterpret_cast<const float4*>(a.zp_tw);
         float4* dst = reinterpret_cast<float4*>(&s.post[0][0]);
         for (int i = tid; i < (4 * 512 + 128) / 2; i += kZThreads) dst[i] = __ldg(src + i);
     }
-    if (warp == 0 && a.detect) {
-        // threshold once per CTA (sigma_h^2 in the order the merge kernel reports it)
+    // persistent over (frame, row block) items; consecutive items of a CTA are usually of one frame
+    int cur_f = -1;
+    for (int it = blockIdx.x; it < frames * nblk; it += gridDim.x) {
+    const int f = it / nblk, rb = it - f * nblk, r0 = rb * kZR;
+    const int nrows = min(kZR, np - r0), TR = nrows + 2;
+    if (f != cur_f && warp == 0 && a.detect) {
+        // threshold once per frame (sigma_h^2 in the order the merge kernel reports it)
         double eta;
         if (a.eta_in != nullptr) {
             eta = a.eta_in[f];
@@ -76,7 +81,8 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
         if ((double)e < eta) e = nextafterf(e, INFINITY);
         if (lane == 0) s.eta_f = e;
     }
-    __syncthreads();
+    cur_f = f;
+    __syncthreads();  // tables / eta visible; the previous item's tile, slots and key list are free
 
     // ---- 1. P tile: rows (r0 - 1 + t) mod N', t < TR
     const float2* gf = a.g + (size_t)f * a.g_rows * kZM;
@@ -124,6 +130,19 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
     }
     __syncthreads();
 
+    // the next item's G rows (16 x 4 KiB) into L2 while this one stores / detects
+    {
+        const int nit = it + gridDim.x;
+        if (nit < frames * nblk) {
+            const int nf = nit / nblk, nr0 = (nit - nf * nblk) * kZR;
+            const char* gb = reinterpret_cast<const char*>(a.g + (size_t)nf * a.g_rows * kZM);
+            for (int i = tid; i < kZTR * 32; i += kZThreads) {  // 32 lines of 128 B per row
+                const int gr = (nr0 - 1 + i / 32 + np) % np;
+                if (gr < a.g_rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(gb + (size_t)gr * kZM * 8 + (i % 32) * 128));
+            }
+        }
+    }
+
     // ---- 2. map store (interior rows)
     if (a.p_out != nullptr) {
         float* po = a.p_out + (size_t)f * np * kZMP + (size_t)r0 * kZMP;
@@ -134,7 +153,7 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
             __stcs(reinterpret_cast<float4*>(po + (size_t)r * kZMP) + q, v);
         }
     }
-    if (!a.detect) return;
+    if (!a.detect) continue;
 
     // ---- 3. threshold + strict wrapped 3x3 local maxima, per-thread top-8 (periodogram.cpp:77-136)
     const float eta_f = s.eta_f;
@@ -174,8 +193,9 @@ __global__ void __launch_bounds__(kZThreads, 1) rowpass_zp_kernel(RowArgs a) {
     __syncthreads();
     block_topk<kZThreads>(list, kZThreads * kZK, a.kmax, s.top, s.best, s.idx);
     __syncthreads();
-    unsigned long long* out = a.cand + ((size_t)f * gridDim.x + rb) * a.kmax;
+    unsigned long long* out = a.cand + ((size_t)f * nblk + rb) * a.kmax;
     for (int i = tid; i < a.kmax; i += kZThreads) out[i] = s.top[i];
+    }
 }
 
 bool rowpass_zp_applies(const RowArgs& a, int mp) {
@@ -189,8 +209,11 @@ cudaError_t launch_rowpass_zp(const RowArgs& a, int frames, cudaStream_t st) {
     const size_t smem = sizeof(ZpSmem);
     cudaError_t e = cudaFuncSetAttribute(rowpass_zp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((a.n_prime + kZR - 1) / kZR, frames);
-    rowpass_zp_kernel<<<grid, kZThreads, smem, st>>>(a);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int items = frames * ((a.n_prime + kZR - 1) / kZR);
+    rowpass_zp_kernel<<<items < sms ? items : sms, kZThreads, smem, st>>>(a, frames);
     return cudaGetLastError();
 }
 
