@@ -673,6 +673,23 @@ def test_rowpass_zp_matches_generic_rowpass(cuda):
         assert all(abs(p - q) <= 1e-4 * q for (_, _, p), (_, _, q) in zip(a, b))
 
 
+def test_rowpass_zp_full_scan_fallback(cuda):
+    # a threshold far below the noise floor puts more cells above eta than the tile's candidate
+    # list holds: rowpass_zp falls back to its full scan; same frames through the generic row pass
+    cfg = configs.CFG2
+    fb = gen.frames(cfg, 0, 3)
+    s2 = fb.sigma2 * 1e-3
+    with Receiver.from_config(cfg) as rx:
+        d8, _ = rx.pipeline(fb.y, fb.x, s2)
+    with Receiver.from_config(cfg.replace(max_targets=9)) as rx:
+        d9, _ = rx.pipeline(fb.y, fb.x, s2)
+    for f in range(3):
+        a, b = d8.frame(f), d9.frame(f)[:8]
+        assert len(a) == 8
+        assert [(x, y) for x, y, _ in a] == [(x, y) for x, y, _ in b]
+        assert all(abs(p - q) <= 1e-4 * q for (_, _, p), (_, _, q) in zip(a, b))
+
+
 @pytest.mark.parametrize("window", [0, 1])
 def test_fused_periodogram_many_frames_on_device(cuda, window, monkeypatch):
     """1000 frames (~55 per 8-CTA frame group: each double-buffered G buffer reused ~27 times,
