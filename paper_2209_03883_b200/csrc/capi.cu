@@ -695,7 +695,7 @@ int ofdmr_create(const ofdmr_config* cfg, ofdmr_context** out) {
         c->fused_grid = 2 * sms;  // 2 resident CTAs per SM (128 regs x 256 threads, ~102 KB smem)
         // two frames in flight per 2-CTA cluster (pass A of frame i+1 overlaps pass C of frame i)
         if (e == cudaSuccess) e = cudaMalloc(&c->dscratch, sizeof(float2) * 128 * 256 * size_t(c->fused_grid));
-        if (e == cudaSuccess) e = cudaMalloc(&c->fedges, sizeof(float) * 16 * 2 * 1024 * size_t(c->fused_grid));
+        if (e == cudaSuccess) e = cudaMalloc(&c->fedges, sizeof(float) * kFusedEdgeStride * size_t(c->fused_grid));
         if (e == cudaSuccess) e = cudaMalloc(&c->fpend, sizeof(unsigned long long) * kFusedPend * size_t(c->fused_grid));
         if (e == cudaSuccess) e = cudaMalloc(&c->fpend_loc, sizeof(int) * kFusedPend * size_t(c->fused_grid));
         if (e == cudaSuccess) e = cudaMalloc(&c->ftlist, sizeof(unsigned long long) * 1024 * size_t(c->fused_grid));

@@ -22,7 +22,7 @@ struct FusedArgs {
     const float2* tw1024_t;
     const float2* tw256_t;
     float2* dscratch;          // per cluster [2][128 * 256] compressed D (double-buffered)
-    float* edges;              // per cluster [2 ranks][16 steps][2 edges][1024] P edge columns
+    float* edges;              // per CTA [16 steps][2 edges][1024] edge-column regions + [32] counts (kFusedEdgeStride)
     unsigned long long* pend;  // per cluster [2 ranks][kFusedPend] edge candidates
     int* pend_loc;
     unsigned long long* tlist; // per CTA [kTileList] frame candidate list             // per cluster [2 ranks][kFusedPend] partner edge-column locator
@@ -34,6 +34,7 @@ struct FusedArgs {
 };
 
 constexpr int kFusedPend = 2048;  // pending edge candidates per CTA per frame
+constexpr int kFusedEdgeStride = 16 * 2 * 1024 + 32;  // floats per CTA: 32 edge-column regions + their counts
 
 }  // namespace ofdmr
 

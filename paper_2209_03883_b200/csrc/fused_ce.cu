@@ -18,6 +18,8 @@
 //
 // Memory per frame: 4 MiB of HBM reads (Y, x_tx), 1 MiB of L2 traffic (D, D'), ~100 B out.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "radar_kernels.cuh"
 #include "warp_fft.cuh"
@@ -121,9 +123,19 @@ __device__ void warp_merge_topk(unsigned long long* run, unsigned long long* tl,
 
 // Pull the 128-B lines of one 8-column tile (1024 rows of Y and x_tx) into L2 so the next
 // tile's loads hit L2 while this tile computes (the pair covers both 64-B halves of a line).
+#ifndef CE_TMAPF
+#define CE_TMAPF 0  // 1: one TMA L2 prefetch per array of the CTA's next pass-A tile while this one computes
+#endif
+#ifndef CE_EVICT_FIRST
+#define CE_EVICT_FIRST 1  // 1: the streamed Y / x_tx lines are marked evict-first in L2 (the D / D' scratch stays)
+#endif
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_pol(void* smem, const void* gmem, unsigned long long pol) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "l"(pol) : "memory");
 }
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
@@ -138,8 +150,13 @@ __device__ __forceinline__ void prefetch_tile(const float2* y, const float2* x, 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const size_t off = fbase + (size_t)(threadIdx.x + 256 * j) * kM + c0;
+#ifdef CE_PF_NORMAL
+        asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(y + off));
+        asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(x + off));
+#else
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(y + off));
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(x + off));
+#endif
     }
 }
 
@@ -151,7 +168,7 @@ __device__ __forceinline__ float eta_float(double eta) {
 }
 
 template <bool HAMMING>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024_kernel(FusedArgs a) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024_kernel(FusedArgs a, const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -183,10 +200,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     int ifr = cid, iu = 0, ist = 0, islot = 0, cslot = 0;
     const size_t lane_off = (size_t)(tid >> 2) * kM + 8 * rank + (tid & 3) * 2;
     size_t ioff = (size_t)cid * kN * kM + lane_off;
+#if CE_EVICT_FIRST
+    unsigned long long pol_stream;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+#endif
     auto a_issue = [&]() {
         if (ifr < a.frames) {
+#if CE_EVICT_FIRST
+            cp_async16_pol(&s.stg[islot][0][tid], a.y + ioff, pol_stream);
+            cp_async16_pol(&s.stg[islot][1][tid], a.x + ioff, pol_stream);
+#else
             cp_async16(&s.stg[islot][0][tid], a.y + ioff);
             cp_async16(&s.stg[islot][1][tid], a.x + ioff);
+#endif
         }
         cp_async_commit();
         islot = islot + 1 == kRing ? 0 : islot + 1;
@@ -207,7 +233,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     // dC: pass-C D' of the step's C tile, loaded into dpre right after the FFT so the
     // L2 latency overlaps the tap store
     auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell, const float2* dC, float4 (&dpre)[2]) {
-        (void)f;
         const int c0 = 16 * u + 8 * rank;
         float inv_tile = 0.f, nmax = 0.f;
 #pragma unroll 4
@@ -242,6 +267,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         inv_acc += (double)inv_tile;  // fp32 within a tile (32 terms), fp64 across tiles
         __syncthreads();
         PH(0);
+#if CE_TMAPF
+        if (tid == 0) {
+            // this CTA's next tile (1024 rows x 8 symbols of Y and x_tx, 64 KiB each) into L2
+            int pu = u + 1, pf = f;
+            if (pu >= 16) {
+                pu = 0;
+                pf += ncl;
+            }
+            if (pf < a.frames) {
+                const int pc0 = 16 * pu + 8 * rank;
+                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                                 reinterpret_cast<unsigned long long>(&ymap)),
+                             "r"(pc0), "r"(0), "r"(4 * pf)
+                             : "memory");
+                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                                 reinterpret_cast<unsigned long long>(&xmap)),
+                             "r"(pc0), "r"(0), "r"(4 * pf)
+                             : "memory");
+            }
+        }
+#endif
         // stream the next tile into L2 while this one computes (one step ahead)
         // stream tile PF_AHEAD steps ahead into L2 while this one computes
         if (PF_AHEAD > 0) {
@@ -353,8 +399,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     // columns 0 and 7 are pre-tested against their own side here and finished at the end of
     // the frame against the partner's stored edge columns, so no cluster barrier is needed
     // inside the step loop.
-    float* my_edges = a.edges + ((size_t)cid * 2 + rank) * 16 * 2 * kN;
-    const float* partner_edges = a.edges + ((size_t)cid * 2 + (rank ^ 1)) * 16 * 2 * kN;
+    // per CTA: 16 steps x 2 edge columns; a column's region holds either a sparse list of its
+    // cells >= eta ((row << 32) | value bits, at most 64) or, when there are more, the whole column
+    // (1024 floats); the per-column counts follow the regions
+    float* my_edges = a.edges + ((size_t)cid * 2 + rank) * kFusedEdgeStride;
+    const float* partner_edges = a.edges + ((size_t)cid * 2 + (rank ^ 1)) * kFusedEdgeStride;
+    int* my_ecnt = reinterpret_cast<int*>(my_edges + 16 * 2 * kN);
+    const int* partner_ecnt = reinterpret_cast<const int*>(partner_edges + 16 * 2 * kN);
     unsigned long long* my_pend = a.pend + ((size_t)cid * 2 + rank) * kFusedPend;
     int* my_ploc = a.pend_loc + ((size_t)cid * 2 + rank) * kFusedPend;
     unsigned long long* tl = a.tlist + (size_t)blockIdx.x * kTileList;  // frame candidates (L2)
@@ -454,15 +505,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 }
             }
         }
-        // this step's edge columns for the partner's end-of-frame tests
-        {
-            const float* pb = reinterpret_cast<const float*>(s.cols);
-#pragma unroll
-            for (int i = tid; i < 2 * kN / 4; i += 256) {  // 16-B vectors (column bases are 16-B aligned)
-                const int e = i >> 8, r4 = (i & 255) * 4;
-                const float4 v4 = *reinterpret_cast<const float4*>(pb + (e ? 7 : 0) * (2 * kVS) + r4);
-                __stcg(reinterpret_cast<float4*>(my_edges + ((size_t)u * 2 + e) * kN + r4), v4);
+        // this step's edge columns for the partner's end-of-frame tests: only cells >= eta can
+        // beat a pending candidate, so the column goes out as its (short) candidate list
+        if (w == 0 || w == 7) {
+            const int e = w == 7;
+            const float* B = reinterpret_cast<const float*>(s.cols) + w * (2 * kVS);
+            const int cnt = s.ccnt[w];
+            float* reg = my_edges + ((size_t)u * 2 + e) * kN;
+            if (cnt <= 64) {
+                for (int i = lane; i < cnt; i += 32) {
+                    const unsigned r = s.clist[w][i];
+                    __stcg(reinterpret_cast<unsigned long long*>(reg) + i,
+                           ((unsigned long long)r << 32) | (unsigned long long)__float_as_uint(B[r]));
+                }
+            } else {
+                for (int i = lane; i < kN / 4; i += 32)
+                    __stcg(reinterpret_cast<float4*>(reg) + i, *reinterpret_cast<const float4*>(B + 4 * i));
             }
+            if (lane == 0) __stcg(my_ecnt + u * 2 + e, cnt);
         }
         __syncthreads();
         PH(8);
@@ -482,8 +542,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             const int r = (int)(idx >> 8);
             const float vv = __uint_as_float((uint32_t)(key >> 32));
             const float* col = partner_edges + (size_t)loc * kN;
-            const float n0 = __ldcg(col + ((r - 1) & (kN - 1))), n1 = __ldcg(col + r), n2 = __ldcg(col + ((r + 1) & (kN - 1)));
-            if (n0 >= vv || n1 >= vv || n2 >= vv) continue;
+            const int ru = (r - 1) & (kN - 1), rd = (r + 1) & (kN - 1);
+            const int pc = __ldcg(partner_ecnt + loc);
+            if (pc <= 64) {
+                bool beaten = false;
+                const unsigned long long* pl = reinterpret_cast<const unsigned long long*>(col);
+                for (int q = 0; q < pc; ++q) {
+                    const unsigned long long e = __ldcg(pl + q);
+                    const int pr = (int)(e >> 32);
+                    beaten |= (pr == ru || pr == r || pr == rd) && __uint_as_float((uint32_t)e) >= vv;
+                }
+                if (beaten) continue;
+            } else {
+                const float n0 = __ldcg(col + ru), n1 = __ldcg(col + r), n2 = __ldcg(col + rd);
+                if (n0 >= vv || n1 >= vv || n2 >= vv) continue;
+            }
             const int sl = atomicAdd(&s.tcnt, 1);
             if (sl < kTileList) tl[sl] = key;
         }
@@ -592,20 +665,54 @@ extern "C" int ofdmr_debug_phase_cycles(unsigned long long* out, int reset) {
 
 namespace ofdmr {
 
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn_ce() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// [frames][1024 k][256 l] c64 as a 3-D f64 tensor (l, k mod 256, 4 frame + k / 256); box = 8 symbols x
+// all 1024 subcarriers (one CTA's pass-A tile), used for L2 prefetches only
+bool tile_map(CUtensorMap* m, const float2* base, int frames) {
+    auto enc = encode_fn_ce();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {256, 256, 4ull * (cuuint64_t)frames};
+    const cuuint64_t strides[2] = {256 * 8, 256 * 256 * 8};
+    const cuuint32_t box[3] = {8, 256, 4};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float2*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
 cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st) {
     const size_t smem = sizeof(FusedSmem);
     grid &= ~1;  // whole clusters
     if (grid < 2) grid = 2;
+    CUtensorMap ymap{}, xmap{};
+#if CE_TMAPF
+    if (!tile_map(&ymap, a.y, a.frames) || !tile_map(&xmap, a.x, a.frames)) return cudaErrorInvalidValue;
+#endif
     if (hamming) {
         cudaError_t e = cudaFuncSetAttribute(fused_ce1024_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        fused_ce1024_kernel<true><<<grid, 256, smem, st>>>(a);
+        fused_ce1024_kernel<true><<<grid, 256, smem, st>>>(a, ymap, xmap);
     } else {
         cudaError_t e = cudaFuncSetAttribute(fused_ce1024_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        fused_ce1024_kernel<false><<<grid, 256, smem, st>>>(a);
+        fused_ce1024_kernel<false><<<grid, 256, smem, st>>>(a, ymap, xmap);
     }
     return cudaGetLastError();
 }

@@ -59,9 +59,15 @@ constexpr bool PG3_MATH_ON = true;
 #ifndef PG3_PSTORE
 #define PG3_PSTORE 0
 #endif
+#ifndef PG3_ROWPIPE
+#define PG3_ROWPIPE 0  // 1: the two FFT_256 rows of a row-warp round interleaved (more ILP, fewer warp syncs)
+#endif
 #ifndef PG3_HBUF
 #define PG3_HBUF (PG3_TMA_STORE ? 3 : 2)
 #endif
+// column twiddles through the read-only cache instead of a shared-memory table (frees 8 KiB:
+// needed for a third H tile buffer)
+#define PG3_TWG (PG3_TMA_STORE || PG3_HBUF > 2)
 constexpr int kGrp = 8;                      // CTAs per frame group
 constexpr int kTC = 4;                       // symbols per column tile = column warps
 constexpr int kHBuf = PG3_HBUF;              // H tiles in flight
@@ -78,7 +84,7 @@ constexpr unsigned kBlockBytes = kBlockElems * 8u;   // 64 KiB
 struct __align__(1024) Pg3Smem {
     float2 htile[kHBuf][kN * kTC];   // [k][4 symbols], 32-B swizzle (1024-B aligned)
     float2 gbuf[2][kBlockElems];     // m-block slab [l][j ^ (l & 31)], then rows [q][l]
-#if !PG3_TMA_STORE
+#if !PG3_TWG
     float2 tw[1024];                 // tw[m * 32 + j] = W_1024^{j m}
 #endif
     unsigned long long mbar_h[kHBuf];
@@ -171,9 +177,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool is_col = warp < kColWarps;
     const int ridx = is_col ? warp : warp - kColWarps;
     const int g = blockIdx.x / kGrp, rank = blockIdx.x % kGrp, ng = gridDim.x / kGrp;
-#if !PG3_TMA_STORE
+#if !PG3_TWG
     for (int i = tid; i < 1024; i += kThreads) s.tw[i] = a.tw1024_t[i];
-#else
+#endif
+#if !PG3_TMA_STORE
     (void)gmap;
 #endif
     if (tid == 0) {
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (kTwReg) {
 #pragma unroll
             for (int m = 0; m < 32; ++m) {
-#if PG3_TMA_STORE
+#if PG3_TWG
                 const float2 w = __ldg(a.tw1024_t + m * 32 + lane);
 #else
                 const float2 w = s.tw[m * 32 + lane];
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (kTwReg) {
                     w = twc[m];
                 } else {
-#if PG3_TMA_STORE
+#if PG3_TWG
                     w = __ldg(a.tw1024_t + m * 32 + lane);
 #else
                     w = s.tw[m * 32 + lane];
@@ -382,6 +389,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < 32; ++q) gb[q * kM + (l ^ (8 * (q & 1)))] = v[q];
             bar_row();
             P3(6);
+#if PG3_ROWPIPE
+            {
+                // FFT_256 over l for rows q = 2 wr + h and 16 + 2 wr + h, the two rows' chains interleaved
+                float2* sl0 = gb + (2 * wr + h) * kM;
+                float2* sl1 = gb + (16 + 2 * wr + h) * kM;
+                float2 xa[16], xb[16];
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    xa[r] = sl0[(j ^ hx) + 16 * r];
+                    xb[r] = sl1[(j ^ hx) + 16 * r];
+                    if (HAMMING) {
+                        xa[r] = cscale(xa[r], wlr[r]);
+                        xb[r] = cscale(xb[r], wlr[r]);
+                    }
+                }
+                dft16<false>(xa);
+                dft16<false>(xb);
+#pragma unroll
+                for (int t1 = 1; t1 < 16; ++t1) {
+                    xa[t1] = cmul(xa[t1], twr[t1]);
+                    xb[t1] = cmul(xb[t1], twr[t1]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int t1 = 0; t1 < 16; ++t1) {
+                    sl0[t1 * 16 + (j ^ t1 ^ hx)] = xa[t1];
+                    sl1[t1 * 16 + (j ^ t1 ^ hx)] = xb[t1];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    xa[jj] = sl0[j * 16 + (jj ^ j ^ hx)];
+                    xb[jj] = sl1[j * 16 + (jj ^ j ^ hx)];
+                }
+                dft16<false>(xa);
+                dft16<false>(xb);
+                float* prow0 = a.p + ((size_t)(g + i * ng) * kN + m + 32 * (2 * wr + h)) * kM;
+                float* prow1 = prow0 + (size_t)32 * 16 * kM;
+#pragma unroll
+                for (int t2 = 0; t2 < 16; ++t2) __stcs(prow0 + ((j + 16 * t2 + 128) & 255), cnorm(xa[t2]) * a.scale);
+#pragma unroll
+                for (int t2 = 0; t2 < 16; ++t2) __stcs(prow1 + ((j + 16 * t2 + 128) & 255), cnorm(xb[t2]) * a.scale);
+            }
+#else
             // FFT_256 over l for rows q = 16 p + 2 wr + h
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
@@ -459,6 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int t2 = 0; t2 < 16; ++t2) __stcs(prow + ((j + 16 * t2 + 128) & 255), cnorm(x[t2]) * a.scale);
 #endif
             }
+#endif
 #if PG3_PSTORE == 3
             if (j == 0) bulk_wait_read_all();  // this lane's P row copies have read their slots
 #endif
