@@ -18,8 +18,6 @@
 //
 // Memory per frame: 4 MiB of HBM reads (Y, x_tx), 1 MiB of L2 traffic (D, D'), ~100 B out.
 #include <cooperative_groups.h>
-#include <cuda.h>
-#include <cudaTypedefs.h>
 
 #include "radar_kernels.cuh"
 #include "warp_fft.cuh"
@@ -83,6 +81,7 @@ struct FusedSmem {
     int zc_part;
     int overflow;
     int zcs[2];
+    unsigned tmem_base;                // CE_TMEM: base address of this CTA's 128 tensor-memory columns
     double part;
     double etas[2];
     double s2hs[2];
@@ -123,8 +122,8 @@ __device__ void warp_merge_topk(unsigned long long* run, unsigned long long* tl,
 
 // Pull the 128-B lines of one 8-column tile (1024 rows of Y and x_tx) into L2 so the next
 // tile's loads hit L2 while this tile computes (the pair covers both 64-B halves of a line).
-#ifndef CE_TMAPF
-#define CE_TMAPF 0  // 1: one TMA L2 prefetch per array of the CTA's next pass-A tile while this one computes
+#ifndef CE_TMEM
+#define CE_TMEM 0  // 1: pass-A stages are consumed (LS) between the compute phases into tensor memory
 #endif
 #ifndef CE_EVICT_FIRST
 #define CE_EVICT_FIRST 1  // 1: the streamed Y / x_tx lines are marked evict-first in L2 (the D / D' scratch stays)
@@ -168,7 +167,7 @@ __device__ __forceinline__ float eta_float(double eta) {
 }
 
 template <bool HAMMING>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024_kernel(FusedArgs a, const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024_kernel(FusedArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -191,7 +190,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
 #endif
     s.tw256[tid] = a.tw256_t[tid];
     if (tid == 0) s.overflow = 0;
+#if CE_TMEM
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&s.tmem_base))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#endif
     __syncthreads();
+#if CE_TMEM
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this thread's 64 words: TMEM lane = 32 (w mod 4) + lane, columns [64 (w / 4), + 64)
+    const unsigned tm_thread = s.tmem_base + ((unsigned)(32 * (w & 3)) << 16) + (unsigned)(64 * (w >> 2));
+#endif
     PH_INIT();
 
     // pass-A input stream: cp.async ring over this CTA's linear sequence of tiles
@@ -227,6 +240,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         }
     };
     for (int st = 0; st < kRing; ++st) a_issue();
+#if CE_TMEM
+    // Pending pass-A tile: its 16 stages are consumed (LS divide) as they land, in groups of up to
+    // kRing between the compute phases of the step, into this thread's tensor-memory words; the
+    // next A_tile only copies them into the column tile.  The ring loads then have a whole compute
+    // phase to arrive instead of being waited for back to back.
+    const int my_tiles = cid < a.frames ? 16 * ((a.frames - cid + ncl - 1) / ncl) : 0;
+    int tiles_done = 0, pend_st = 0;
+    float p_inv = 0.f, p_nmax = 0.f;
+    auto drain = [&](int n) {
+        if (tiles_done >= my_tiles) return;
+#pragma unroll 1
+        for (int q = 0; q < n && pend_st < 16; ++q, ++pend_st) {
+            cp_async_wait<kRing - 1>();
+            const float4 y4 = s.stg[cslot][0][tid];
+            const float4 x4 = s.stg[cslot][1][tid];
+            cslot = cslot + 1 == kRing ? 0 : cslot + 1;
+            const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
+            const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
+            const float i0 = rcp_approx(n0);
+            const float i1 = rcp_approx(n1);
+            p_inv += i0 + i1;
+            p_nmax = fmaxf(p_nmax, fmaxf(n0, n1));
+            const float r0x = fmaf(y4.x, x4.x, y4.y * x4.y) * i0, r0y = fmaf(y4.y, x4.x, -y4.x * x4.y) * i0;
+            const float r1x = fmaf(y4.z, x4.z, y4.w * x4.w) * i1, r1y = fmaf(y4.w, x4.z, -y4.z * x4.w) * i1;
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tm_thread + 4 * pend_st),
+                         "r"(__float_as_uint(r0x)), "r"(__float_as_uint(r0y)), "r"(__float_as_uint(r1x)),
+                         "r"(__float_as_uint(r1y))
+                         : "memory");
+            a_issue();
+        }
+    };
+#define CE_DRAIN(n) drain(n)
+#else
+#define CE_DRAIN(n)
+#endif
 
     // ---------------------------------------------------------------- pass A, one tile
     // column tile u (8 symbols) of frame f: LS divide -> IFFT_N -> L taps x 1/N -> D
@@ -234,6 +282,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     // L2 latency overlaps the tap store
     auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell, const float2* dC, float4 (&dpre)[2]) {
         const int c0 = 16 * u + 8 * rank;
+#if CE_TMEM
+        (void)f;
+        // the stages not yet consumed, then tensor memory -> column tile
+        drain(16);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int g4 = 0; g4 < 4; ++g4) {
+            unsigned r[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+                "%15}, [%16];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+                  "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                : "r"(tm_thread + 16 * g4)
+                : "memory");
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int idx = tid + (4 * g4 + q) * 256;
+                const int k = idx >> 2, c = (idx & 3) * 2;
+                const int pk = k + (k >> 5);
+                s.cols[c * kVS + pk] = make_float2(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
+                s.cols[(c + 1) * kVS + pk] = make_float2(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+            }
+        }
+        const float inv_tile = p_inv, nmax = p_nmax;
+        p_inv = 0.f;
+        p_nmax = 0.f;
+        pend_st = 0;
+        ++tiles_done;
+#else
         float inv_tile = 0.f, nmax = 0.f;
 #pragma unroll 4
         for (int st = 0; st < 16; ++st) {
@@ -260,6 +339,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             // refill the slot (its values were consumed above) with the stage kRing ahead
             a_issue();
         }
+#endif
         // |x|^2 outside the fp32 normal range somewhere in the tile (an exactly zero x cell,
         // estimation.cpp:17, or a denormal / huge one the reference divides in fp64): the frame is
         // flagged for the exact general path (status bit 1), which decides the zero-cell error
@@ -267,27 +347,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         inv_acc += (double)inv_tile;  // fp32 within a tile (32 terms), fp64 across tiles
         __syncthreads();
         PH(0);
-#if CE_TMAPF
-        if (tid == 0) {
-            // this CTA's next tile (1024 rows x 8 symbols of Y and x_tx, 64 KiB each) into L2
-            int pu = u + 1, pf = f;
-            if (pu >= 16) {
-                pu = 0;
-                pf += ncl;
-            }
-            if (pf < a.frames) {
-                const int pc0 = 16 * pu + 8 * rank;
-                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                                 reinterpret_cast<unsigned long long>(&ymap)),
-                             "r"(pc0), "r"(0), "r"(4 * pf)
-                             : "memory");
-                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
-                                 reinterpret_cast<unsigned long long>(&xmap)),
-                             "r"(pc0), "r"(0), "r"(4 * pf)
-                             : "memory");
-            }
-        }
-#endif
         // stream the next tile into L2 while this one computes (one step ahead)
         // stream tile PF_AHEAD steps ahead into L2 while this one computes
         if (PF_AHEAD > 0) {
@@ -304,6 +363,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = col[lane + 33 * i];
             warp_fft1024<true, 32, TW_GLOBAL, 4>(v, col, twp);  // lane t1: taps t1 + 32 t2, t2 < 4
+            CE_DRAIN(kRing);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int idx = tid + j * 256;
@@ -434,6 +494,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             for (int i = 0; i < 4; ++i) v[i] = col[lane + 33 * i];
             if constexpr (HAMMING) {
                 warp_fft1024<false, 4, TW_GLOBAL>(v, col, twp);
+#if CE_TMEM >= 2
+                CE_DRAIN(kRing);
+#endif
 #pragma unroll
                 for (int t2 = 0; t2 < 32; ++t2) v[t2] = cscale(v[t2], __ldg(a.wk + lane + 32 * t2));
                 warp_fft1024<true, 32, TW_GLOBAL>(v, col, twp);
@@ -461,6 +524,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 }
             }
         }
+        CE_DRAIN(kRing);
         __syncthreads();
         PH(6);
         {
@@ -524,6 +588,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             }
             if (lane == 0) __stcg(my_ecnt + u * 2 + e, cnt);
         }
+        CE_DRAIN(kRing);
         __syncthreads();
         PH(8);
     };
@@ -641,6 +706,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         }
     }
     cluster.sync();  // no CTA leaves while its partner may still read its shared memory
+#if CE_TMEM
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s.tmem_base) : "memory");
+#endif
 }
 
 size_t fused_ce_smem() { return sizeof(FusedSmem); }
@@ -665,54 +733,20 @@ extern "C" int ofdmr_debug_phase_cycles(unsigned long long* out, int reset) {
 
 namespace ofdmr {
 
-namespace {
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn_ce() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-// [frames][1024 k][256 l] c64 as a 3-D f64 tensor (l, k mod 256, 4 frame + k / 256); box = 8 symbols x
-// all 1024 subcarriers (one CTA's pass-A tile), used for L2 prefetches only
-bool tile_map(CUtensorMap* m, const float2* base, int frames) {
-    auto enc = encode_fn_ce();
-    if (!enc) return false;
-    const cuuint64_t dims[3] = {256, 256, 4ull * (cuuint64_t)frames};
-    const cuuint64_t strides[2] = {256 * 8, 256 * 256 * 8};
-    const cuuint32_t box[3] = {8, 256, 4};
-    const cuuint32_t es[3] = {1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<float2*>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-}  // namespace
-
 cudaError_t launch_fused_ce(const FusedArgs& a, bool hamming, int grid, cudaStream_t st) {
     const size_t smem = sizeof(FusedSmem);
     grid &= ~1;  // whole clusters
     if (grid < 2) grid = 2;
-    CUtensorMap ymap{}, xmap{};
-#if CE_TMAPF
-    if (!tile_map(&ymap, a.y, a.frames) || !tile_map(&xmap, a.x, a.frames)) return cudaErrorInvalidValue;
-#endif
     if (hamming) {
         cudaError_t e = cudaFuncSetAttribute(fused_ce1024_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        fused_ce1024_kernel<true><<<grid, 256, smem, st>>>(a, ymap, xmap);
+        fused_ce1024_kernel<true><<<grid, 256, smem, st>>>(a);
     } else {
         cudaError_t e = cudaFuncSetAttribute(fused_ce1024_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        fused_ce1024_kernel<false><<<grid, 256, smem, st>>>(a, ymap, xmap);
+        fused_ce1024_kernel<false><<<grid, 256, smem, st>>>(a);
     }
     return cudaGetLastError();
 }
