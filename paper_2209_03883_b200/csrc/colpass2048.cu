@@ -59,6 +59,21 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+// LS cell with the fused kernels' arithmetic (fused_ce.cu pass A): rcp.approx (1 ulp) instead of
+// an IEEE division, 1/|x|^2 summed in fp32 over a short run; |x|^2 outside the fp32 normal range
+// (zero, denormal or huge x) takes the exact fp64 cell of radar_kernels.cuh
+__device__ __forceinline__ float2 ls_cell_fast(float yr, float yi, float xr, float xi, float& inv_run, double& inv_acc,
+                                               int& zero_cell) {
+    const float n = fmaf(xr, xr, xi * xi);
+    if (__builtin_expect(n >= 1.17549435e-38f && n <= 3.40282347e38f, 1)) {
+        float i;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(i) : "f"(n));
+        inv_run += i;
+        return make_float2(fmaf(yr, xr, yi * xi) * i, fmaf(yi, xr, -yr * xi) * i);
+    }
+    return ls_cell_fp64(yr, yi, xr, xi, inv_acc, zero_cell);
+}
+
 __device__ __forceinline__ double block_sum(double v, double* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -108,8 +123,9 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
 #pragma unroll
         for (int st = 0; st < kRing - 1; ++st) issue(st);
         double inv_acc = 0.0;
+        float inv_run = 0.f;
         int zero_cell = 0;
-#pragma unroll 2
+#pragma unroll 8
         for (int st = 0; st < kStages; ++st) {
             issue(st + kRing - 1);
             cp_async_wait<kRing - 1>();
@@ -118,8 +134,12 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
             float2 h0, h1;
             if (ls) {
                 const float4 x4 = slot[kT + tid];
-                h0 = ls_cell(y4.x, y4.y, x4.x, x4.y, inv_acc, zero_cell);
-                h1 = ls_cell(y4.z, y4.w, x4.z, x4.w, inv_acc, zero_cell);
+                h0 = ls_cell_fast(y4.x, y4.y, x4.x, x4.y, inv_run, inv_acc, zero_cell);
+                h1 = ls_cell_fast(y4.z, y4.w, x4.z, x4.w, inv_run, inv_acc, zero_cell);
+                if ((st & 7) == 7) {  // 16 terms in fp32, then fp64
+                    inv_acc += (double)inv_run;
+                    inv_run = 0.f;
+                }
             } else {
                 h0 = make_float2(y4.x, y4.y);
                 h1 = make_float2(y4.z, y4.w);

@@ -645,7 +645,9 @@ def test_colpass2048_matches_generic_column_pass(cuda, monkeypatch):
         assert np.abs(p1[f] - p0[f]).max() <= 2e-5 * p0[f].max(), f
         assert [(a, b) for a, b, _ in d1.frame(f)] == [(a, b) for a, b, _ in d0.frame(f)], f
     s1, s0 = d1.sigma2_h.cpu().numpy(), d0.sigma2_h.cpu().numpy()
-    assert np.abs(s1 - s0).max() <= 1e-12 * s0.max()  # same terms, 8- vs 2-column tile sums
+    # colpass2048 forms 1/|x|^2 with rcp.approx and sums runs of 16 terms in fp32 (as the fused
+    # kernels do); the generic pass divides in IEEE fp32 and sums in fp64
+    assert np.abs(s1 - s0).max() <= 1e-7 * s0.max()
 
 
 def test_pipeline_cfg2_zero_cell_raises(cuda):

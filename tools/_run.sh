@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-L=$PWD/paper_2209_03883_b200
-OFDMR_LIB=$L/libofdmr_b200_tt0.so python tools/phase_timing.py 4096 > gpurun_out/t12.log 2>&1
-OFDMR_LIB=$L/libofdmr_b200_tt2.so python tools/phase_timing.py 4096 >> gpurun_out/t12.log 2>&1
-cat gpurun_out/t12.log
+python -m pytest tests -m gpu -x -q -k "cfg2 or zp or colpass2048" > gpurun_out/t14.log 2>&1
+tail -3 gpurun_out/t14.log
