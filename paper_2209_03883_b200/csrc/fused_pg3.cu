@@ -60,7 +60,7 @@ constexpr bool PG3_MATH_ON = true;
 #define PG3_PSTORE 0
 #endif
 #ifndef PG3_ROWPIPE
-#define PG3_ROWPIPE 0  // 1: the two FFT_256 rows of a row-warp round interleaved (more ILP, fewer warp syncs)
+#define PG3_ROWPIPE 1  // 1: the two FFT_256 rows of a row-warp round interleaved (more ILP, fewer warp syncs)
 #endif
 #ifndef PG3_HBUF
 #define PG3_HBUF (PG3_TMA_STORE ? 3 : 2)
