@@ -81,7 +81,6 @@ struct FusedSmem {
     int zc_part;
     int overflow;
     int zcs[2];
-    unsigned tmem_base;                // CE_TMEM: base address of this CTA's 128 tensor-memory columns
     double part;
     double etas[2];
     double s2hs[2];
@@ -122,9 +121,6 @@ __device__ void warp_merge_topk(unsigned long long* run, unsigned long long* tl,
 
 // Pull the 128-B lines of one 8-column tile (1024 rows of Y and x_tx) into L2 so the next
 // tile's loads hit L2 while this tile computes (the pair covers both 64-B halves of a line).
-#ifndef CE_TMEM
-#define CE_TMEM 0  // 1: pass-A stages are consumed (LS) between the compute phases into tensor memory
-#endif
 #ifndef CE_EVICT_FIRST
 #define CE_EVICT_FIRST 1  // 1: the streamed Y / x_tx lines are marked evict-first in L2 (the D / D' scratch stays)
 #endif
@@ -190,21 +186,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
 #endif
     s.tw256[tid] = a.tw256_t[tid];
     if (tid == 0) s.overflow = 0;
-#if CE_TMEM
-    if (w == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
-                         (unsigned)__cvta_generic_to_shared(&s.tmem_base))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-#endif
     __syncthreads();
-#if CE_TMEM
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // this thread's 64 words: TMEM lane = 32 (w mod 4) + lane, columns [64 (w / 4), + 64)
-    const unsigned tm_thread = s.tmem_base + ((unsigned)(32 * (w & 3)) << 16) + (unsigned)(64 * (w >> 2));
-#endif
     PH_INIT();
 
     // pass-A input stream: cp.async ring over this CTA's linear sequence of tiles
@@ -240,41 +222,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         }
     };
     for (int st = 0; st < kRing; ++st) a_issue();
-#if CE_TMEM
-    // Pending pass-A tile: its 16 stages are consumed (LS divide) as they land, in groups of up to
-    // kRing between the compute phases of the step, into this thread's tensor-memory words; the
-    // next A_tile only copies them into the column tile.  The ring loads then have a whole compute
-    // phase to arrive instead of being waited for back to back.
-    const int my_tiles = cid < a.frames ? 16 * ((a.frames - cid + ncl - 1) / ncl) : 0;
-    int tiles_done = 0, pend_st = 0;
-    float p_inv = 0.f, p_nmax = 0.f;
-    auto drain = [&](int n) {
-        if (tiles_done >= my_tiles) return;
-#pragma unroll 1
-        for (int q = 0; q < n && pend_st < 16; ++q, ++pend_st) {
-            cp_async_wait<kRing - 1>();
-            const float4 y4 = s.stg[cslot][0][tid];
-            const float4 x4 = s.stg[cslot][1][tid];
-            cslot = cslot + 1 == kRing ? 0 : cslot + 1;
-            const float n0 = fmaf(x4.x, x4.x, x4.y * x4.y);
-            const float n1 = fmaf(x4.z, x4.z, x4.w * x4.w);
-            const float i0 = rcp_approx(n0);
-            const float i1 = rcp_approx(n1);
-            p_inv += i0 + i1;
-            p_nmax = fmaxf(p_nmax, fmaxf(n0, n1));
-            const float r0x = fmaf(y4.x, x4.x, y4.y * x4.y) * i0, r0y = fmaf(y4.y, x4.x, -y4.x * x4.y) * i0;
-            const float r1x = fmaf(y4.z, x4.z, y4.w * x4.w) * i1, r1y = fmaf(y4.w, x4.z, -y4.z * x4.w) * i1;
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tm_thread + 4 * pend_st),
-                         "r"(__float_as_uint(r0x)), "r"(__float_as_uint(r0y)), "r"(__float_as_uint(r1x)),
-                         "r"(__float_as_uint(r1y))
-                         : "memory");
-            a_issue();
-        }
-    };
-#define CE_DRAIN(n) drain(n)
-#else
-#define CE_DRAIN(n)
-#endif
 
     // ---------------------------------------------------------------- pass A, one tile
     // column tile u (8 symbols) of frame f: LS divide -> IFFT_N -> L taps x 1/N -> D
@@ -282,37 +229,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
     // L2 latency overlaps the tap store
     auto A_tile = [&](int f, int u, float2* dsc, double& inv_acc, int& zero_cell, const float2* dC, float4 (&dpre)[2]) {
         const int c0 = 16 * u + 8 * rank;
-#if CE_TMEM
-        (void)f;
-        // the stages not yet consumed, then tensor memory -> column tile
-        drain(16);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int g4 = 0; g4 < 4; ++g4) {
-            unsigned r[16];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-                "%15}, [%16];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-                  "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                : "r"(tm_thread + 16 * g4)
-                : "memory");
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int idx = tid + (4 * g4 + q) * 256;
-                const int k = idx >> 2, c = (idx & 3) * 2;
-                const int pk = k + (k >> 5);
-                s.cols[c * kVS + pk] = make_float2(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]));
-                s.cols[(c + 1) * kVS + pk] = make_float2(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-            }
-        }
-        const float inv_tile = p_inv, nmax = p_nmax;
-        p_inv = 0.f;
-        p_nmax = 0.f;
-        pend_st = 0;
-        ++tiles_done;
-#else
         float inv_tile = 0.f, nmax = 0.f;
 #pragma unroll 4
         for (int st = 0; st < 16; ++st) {
@@ -339,7 +255,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             // refill the slot (its values were consumed above) with the stage kRing ahead
             a_issue();
         }
-#endif
         // |x|^2 outside the fp32 normal range somewhere in the tile (an exactly zero x cell,
         // estimation.cpp:17, or a denormal / huge one the reference divides in fp64): the frame is
         // flagged for the exact general path (status bit 1), which decides the zero-cell error
@@ -363,7 +278,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = col[lane + 33 * i];
             warp_fft1024<true, 32, TW_GLOBAL, 4>(v, col, twp);  // lane t1: taps t1 + 32 t2, t2 < 4
-            CE_DRAIN(kRing);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int idx = tid + j * 256;
@@ -494,9 +408,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             for (int i = 0; i < 4; ++i) v[i] = col[lane + 33 * i];
             if constexpr (HAMMING) {
                 warp_fft1024<false, 4, TW_GLOBAL>(v, col, twp);
-#if CE_TMEM >= 2
-                CE_DRAIN(kRing);
-#endif
 #pragma unroll
                 for (int t2 = 0; t2 < 32; ++t2) v[t2] = cscale(v[t2], __ldg(a.wk + lane + 32 * t2));
                 warp_fft1024<true, 32, TW_GLOBAL>(v, col, twp);
@@ -524,7 +435,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
                 }
             }
         }
-        CE_DRAIN(kRing);
         __syncthreads();
         PH(6);
         {
@@ -588,7 +498,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
             }
             if (lane == 0) __stcg(my_ecnt + u * 2 + e, cnt);
         }
-        CE_DRAIN(kRing);
         __syncthreads();
         PH(8);
     };
@@ -706,9 +615,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) fused_ce1024
         }
     }
     cluster.sync();  // no CTA leaves while its partner may still read its shared memory
-#if CE_TMEM
-    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s.tmem_base) : "memory");
-#endif
 }
 
 size_t fused_ce_smem() { return sizeof(FusedSmem); }
