@@ -85,6 +85,22 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return s;
 }
 
+#ifdef OFDMR_PHASE_TIMING
+__device__ unsigned long long g_c2_phase[8];
+#define C2P_INIT() long long _ph_t = clock64();
+#define C2P(i)                                                          \
+    do {                                                                \
+        if (tid == 0) {                                                 \
+            const long long _n = clock64();                             \
+            atomicAdd(&g_c2_phase[i], (unsigned long long)(_n - _ph_t)); \
+            _ph_t = _n;                                                 \
+        }                                                               \
+    } while (0)
+#else
+#define C2P_INIT()
+#define C2P(i)
+#endif
+
 __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frames) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C2Smem& s = *reinterpret_cast<C2Smem*>(smem_raw);
@@ -104,6 +120,7 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
     float2* scr = col + kScr;
     const int q4 = tid & 3, r0 = tid >> 2;  // LS: column pair, row within a stage
 
+    C2P_INIT();
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int f = it / ntile, tile = it - f * ntile, c0 = tile * kC;
         const size_t fbase = (size_t)f * kN * m;
@@ -158,6 +175,7 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
             }
         }
         __syncthreads();  // tile complete; the ring (staging area) is free
+        C2P(0);
 
         // the next item's rows into L2 while this one computes
         {
@@ -235,6 +253,7 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
             }
         }
 
+        C2P(1);
         // ---- 4. IFFT_4096 as four IFFT_1024 (s = 0..3) -> G rows 4p + s, staged per 64-B segment
         float2* g = a.g_out + (size_t)f * a.g_rows * m + c0;
 #pragma unroll 1
@@ -253,6 +272,7 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
                 v[i] = y;
             }
             warp_fft1024<true, 32>(v, scr, s.tw);  // lane t1: X[4 (t1 + 32 t2) + sx]
+            C2P(2);
             __syncthreads();                       // staging free (previous segment stored)
 #pragma unroll
             for (int t2 = 0; t2 < 32; ++t2) s.stage[(lane + 32 * t2) * kSP + w] = v[t2];
@@ -264,6 +284,7 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
                 const float2 v0 = s.stage[p * kSP + 2 * qq], v1 = s.stage[p * kSP + 2 * qq + 1];
                 *reinterpret_cast<float4*>(g + (size_t)(4 * p + sx) * m + 2 * qq) = make_float4(v0.x, v0.y, v1.x, v1.y);
             }
+            C2P(3);
         }
         __syncthreads();  // staging and tile free for the next item
     }
@@ -273,6 +294,24 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
 
 // cfg2's column pass: N = 2048, N' = 4096, DFT-CE with L <= 256 (or plain LS / H input), G out,
 // no H output requested
+}  // namespace ofdmr
+extern "C" int ofdmr_debug_c2_phase_cycles(unsigned long long* out, int reset) {
+#ifdef OFDMR_PHASE_TIMING
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, ofdmr::g_c2_phase, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(ofdmr::g_c2_phase, z, sizeof(z));
+    }
+    return 8;
+#else
+    (void)out;
+    (void)reset;
+    return 0;
+#endif
+}
+namespace ofdmr {
+
 bool colpass2048_applies(const ColArgs& a, int n, int np) {
     return n == kN && np == kNP && a.tw_n == nullptr && a.g_out != nullptr && a.h_out == nullptr && !a.shortcut &&
            a.ce_taps >= 0 && a.ce_taps <= 256 && a.m % kC == 0 && a.g_rows == kNP && a.m >= kC &&
