@@ -675,6 +675,16 @@ def test_rowpass_zp_matches_generic_rowpass(cuda):
         assert all(abs(p - q) <= 1e-4 * q for (_, _, p), (_, _, q) in zip(a, b))
 
 
+@pytest.mark.parametrize("n,np_,window,L", [(64, 64, configs.WINDOW_RECT, 16), (128, 256, configs.WINDOW_HAMMING, 32)])
+def test_rowpass_zp_other_delay_sizes(cuda, n, np_, window, L):
+    # rowpass_zp (M = 512 -> M' = 2048, K <= 8) behind the generic column pass: the DFT-CE shortcut's
+    # all-zero rows (rect, N' = N), a last row block shorter than 14 rows, and a 1/(N M) that is not
+    # an even power of two (scale kept out of the twiddles)
+    cfg = configs.CFG1.replace(name="zp-small", n=n, m=512, n_prime=np_, m_prime=2048, n_cp=L, window=window,
+                               max_targets=4, snr_lo_db=5.0, snr_hi_db=5.0)
+    _pipeline_parity(cfg, 2)
+
+
 def test_rowpass_zp_full_scan_fallback(cuda):
     # a threshold far below the noise floor puts more cells above eta than the tile's candidate
     # list holds: rowpass_zp falls back to its full scan; same frames through the generic row pass
