@@ -25,8 +25,6 @@
 // (64 B, the tile's 8 columns) is staged through shared memory and stored coalesced.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
-
 #include "radar_kernels.cuh"
 #include "warp_fft.cuh"
 
@@ -292,273 +290,6 @@ __global__ void __launch_bounds__(kT, 1) colpass2048_kernel(ColArgs a, int frame
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// Two warps per column (16 warps, 128 registers per thread): warp w works on column w & 7 in
-// role w >> 3.  The independent transforms of a column are split across the pair -- role 0
-// takes a[k] (even taps), E and the delay IFFTs s = 0, 1; role 1 takes b[k] (odd taps), O and
-// s = 2, 3 -- so every FFT phase has twice the warps in flight.  H' (2048 values) then lives in
-// the column's two shared-memory regions instead of registers, and the delay IFFTs transpose in
-// two 16-row steps through a 528-entry slot per warp carved out of the staging area (which is
-// the cp.async ring during LS, the transpose scratch during an FFT and the G staging after it).
-constexpr int kPT = 512;             // threads per CTA
-constexpr int kPRows = kPT / 4;      // rows per ring stage (128)
-constexpr int kPStages = kN / kPRows;
-constexpr int kPRing = 4;
-constexpr int kScr2 = 16 * 33;       // half-transpose slot per warp (float2)
-static_assert(16 * kScr2 <= 1024 * kSP, "transpose slots must fit the staging area");
-static_assert(kPRing * 2 * kPT * 16 <= (int)sizeof(float2) * 1024 * kSP, "ring must fit the staging area");
-
-struct __align__(16) C2PSmem {
-    float2 cols[kC * kVS];
-    float2 stage[1024 * kSP];
-    float2 tw[1024];
-    double red[16];
-};
-
-__device__ __forceinline__ void pair_bar(int c) { asm volatile("bar.sync %0, 64;" ::"r"(c + 1) : "memory"); }
-
-// warp_fft1024 (warp_fft.cuh) with the 32 x 32 transpose done as two 16-row halves through a
-// 16 x 33 slot: lanes 0-15 collect their rows after the first half, lanes 16-31 after the second
-template <bool INV, int NZ, int NOUT = 32>
-__device__ __forceinline__ void warp_fft1024_2s(float2 (&v)[32], float2* scr, const float2* tw) {
-    const int lane = threadIdx.x & 31;
-    if constexpr (NZ == 4) dft32_in4<INV>(v);
-    else dft32<INV>(v);
-#pragma unroll
-    for (int t1 = 1; t1 < 32; ++t1) {
-        float2 w = tw[t1 * 32 + lane];
-        if (INV) w.y = -w.y;
-        v[t1] = cmul(v[t1], w);
-    }
-    float2 r[32];
-    __syncwarp();
-#pragma unroll
-    for (int t1 = 0; t1 < 16; ++t1) scr[t1 * 33 + lane] = v[t1];
-    __syncwarp();
-    if (lane < 16) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = scr[lane * 33 + j];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t1 = 0; t1 < 16; ++t1) scr[t1 * 33 + lane] = v[16 + t1];
-    __syncwarp();
-    if (lane >= 16) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = scr[(lane - 16) * 33 + j];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = r[j];
-    if constexpr (NOUT == 4) dft32_out4<INV>(v);
-    else dft32<INV>(v);
-}
-
-__global__ void __launch_bounds__(kPT, 1) colpass2048p_kernel(ColArgs a, int frames) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C2PSmem& s = *reinterpret_cast<C2PSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int c = w & 7, role = w >> 3;
-    const int m = a.m;
-    const int ntile = m / kC;
-    const int items = frames * ntile;
-    const int per = a.ntiles / ntile;
-    const bool ls = a.y != nullptr;
-    const bool ce = a.ce_taps > 0;
-    const int L = a.ce_taps;
-    const float2* __restrict__ tw4 = a.tw;  // e^{-j 2 pi t / 4096}
-
-    for (int i = tid; i < 1024; i += kPT) s.tw[i] = tw4[(4 * (i & 31) * (i >> 5)) & 4095];
-    float4* ring = reinterpret_cast<float4*>(s.stage);  // [kPRing][2][kPT]
-    float2* reg0 = s.cols + c * kVS;      // h low half -> role 0's scratch -> H'[q]
-    float2* reg1 = reg0 + kScr;           // h high half -> role 1's scratch -> H'[q + 1024]
-    float2* mine = role ? reg1 : reg0;
-    float2* scr2 = s.stage + w * kScr2;   // stage-3 transpose slot
-    const int q4 = tid & 3, r0 = tid >> 2;
-
-    C2P_INIT();
-    for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        const int f = it / ntile, tile = it - f * ntile, c0 = tile * kC;
-        const size_t fbase = (size_t)f * kN * m;
-
-        // ---- 1. LS into the column-major tile
-        const float2* src0 = (ls ? a.y : a.h) + fbase + (size_t)r0 * m + c0 + 2 * q4;
-        const float2* src1 = ls ? a.x + fbase + (size_t)r0 * m + c0 + 2 * q4 : nullptr;
-        auto issue = [&](int st) {
-            if (st < kPStages) {
-                const size_t off = (size_t)st * kPRows * m;
-                float4* slot = ring + (st % kPRing) * 2 * kPT;
-                cp_async16(slot + tid, src0 + off);
-                if (ls) cp_async16(slot + kPT + tid, src1 + off);
-            }
-            cp_async_commit();
-        };
-#pragma unroll
-        for (int st = 0; st < kPRing - 1; ++st) issue(st);
-        double inv_acc = 0.0;
-        float inv_run = 0.f;
-        int zero_cell = 0;
-#pragma unroll 4
-        for (int st = 0; st < kPStages; ++st) {
-            issue(st + kPRing - 1);
-            cp_async_wait<kPRing - 1>();
-            const float4* slot = ring + (st % kPRing) * 2 * kPT;
-            const float4 y4 = slot[tid];
-            float2 h0, h1;
-            if (ls) {
-                const float4 x4 = slot[kPT + tid];
-                h0 = ls_cell_fast(y4.x, y4.y, x4.x, x4.y, inv_run, inv_acc, zero_cell);
-                h1 = ls_cell_fast(y4.z, y4.w, x4.z, x4.w, inv_run, inv_acc, zero_cell);
-                if ((st & 3) == 3) {  // 8 terms in fp32, then fp64
-                    inv_acc += (double)inv_run;
-                    inv_run = 0.f;
-                }
-            } else {
-                h0 = make_float2(y4.x, y4.y);
-                h1 = make_float2(y4.z, y4.w);
-            }
-            const int k = st * kPRows + r0;
-            const int pk = k + (k >> 5);
-            s.cols[(2 * q4) * kVS + pk] = h0;
-            s.cols[(2 * q4 + 1) * kVS + pk] = h1;
-        }
-        cp_async_wait<0>();
-        if (ls) {
-            if (zero_cell) atomicOr(a.status + f, 1);
-            if (a.inv_partial != nullptr) {
-                double v = inv_acc;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) s.red[w] = v;
-                __syncthreads();
-                if (tid < per) {
-                    double sum = 0.0;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) sum += s.red[i];
-                    a.inv_partial[(size_t)f * a.ntiles + tile * per + tid] = tid == 0 ? sum : 0.0;
-                }
-            }
-        }
-        __syncthreads();  // tile complete; the ring (staging area) is free
-        C2P(0);
-
-        // the next item's rows into L2 while this one computes
-        {
-            const int nit = it + gridDim.x;
-            if (nit < items) {
-                const int nf = nit / ntile, nc0 = (nit - nf * ntile) * kC;
-                const float2* p0 = (ls ? a.y : a.h) + (size_t)nf * kN * m + nc0;
-#pragma unroll
-                for (int j = 0; j < kN / kPT; ++j) {
-                    const size_t off = (size_t)(tid + kPT * j) * m;
-                    prefetch_l2(p0 + off);
-                    if (ls) prefetch_l2(a.x + (size_t)nf * kN * m + nc0 + off);
-                }
-            }
-        }
-
-        // ---- 2./3. per column pair: [DFT-CE] and the window -> H'[q] in reg0, H'[q + 1024] in reg1
-        const float wl = a.wl != nullptr ? a.wl[c0 + c] : 1.0f;
-        if (ce) {
-            float2 v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int k = lane + 32 * i;
-                const float2 lo = reg0[k + i], hi = reg1[k + i];
-                if (role == 0) {
-                    v[i] = cadd(lo, hi);                       // a[k]
-                } else {
-                    float2 wv = __ldg(tw4 + 2 * k);            // W_2048^k
-                    wv.y = -wv.y;
-                    v[i] = cmul(csub(lo, hi), wv);             // b[k]
-                }
-            }
-            pair_bar(c);  // both halves are in registers: the regions are the two warps' scratch
-            warp_fft1024<true, 32, false, 4>(v, mine, s.tw);   // lane t1: x[2 (t1 + 32 t2) + role], t2 < 4
-            constexpr float inv_n = 1.0f / (float)kN;
-            float2 e[32];
-#pragma unroll
-            for (int t2 = 0; t2 < 4; ++t2) {
-                const int u = lane + 32 * t2;
-                e[t2] = 2 * u + role < L ? cscale(v[t2], inv_n) : make_float2(0.f, 0.f);
-            }
-            warp_fft1024<false, 4>(e, mine, s.tw);             // E[q] (role 0) or O[q] (role 1), q = lane + 32 i
-            if (role == 1) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) reg1[lane + 33 * i] = cmul(e[i], __ldg(tw4 + 2 * (lane + 32 * i)));  // W_2048^q O
-            }
-            pair_bar(c);
-            if (role == 0) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int q = lane + 32 * i;
-                    const float2 t = reg1[lane + 33 * i];
-                    float2 h0 = cadd(e[i], t), h1 = csub(e[i], t);
-                    if (a.wk != nullptr) {
-                        h0 = cscale(h0, __ldg(a.wk + q) * wl);
-                        h1 = cscale(h1, __ldg(a.wk + q + 1024) * wl);
-                    }
-                    reg0[lane + 33 * i] = h0;
-                    reg1[lane + 33 * i] = h1;
-                }
-            }
-            pair_bar(c);
-        } else {
-            if (a.wk != nullptr) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int q = lane + 32 * i;
-                    mine[q + i] = cscale(mine[q + i], __ldg(a.wk + q + 1024 * role) * wl);
-                }
-            }
-            pair_bar(c);
-        }
-
-        C2P(1);
-        // ---- 4. IFFT_4096 as four IFFT_1024: role 0 takes s = 0, 1, role 1 takes s = 2, 3
-        float2* g = a.g_out + (size_t)f * a.g_rows * m + c0;
-#pragma unroll 1
-        for (int rd = 0; rd < 2; ++rd) {
-            const int sx = 2 * role + rd;
-            float2 v[32];
-            const float jc = sx == 0 ? 1.f : sx == 2 ? -1.f : 0.f, js = sx == 1 ? 1.f : sx == 3 ? -1.f : 0.f;  // j^s
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int q = lane + 32 * i;
-                float2 y = cfma_cs(jc, js, reg1[lane + 33 * i], reg0[lane + 33 * i]);  // H'[q] + j^s H'[q + 1024]
-                if (sx) {
-                    float2 wv = __ldg(tw4 + sx * q);  // W_4096^{sq}, conjugated: inverse
-                    wv.y = -wv.y;
-                    y = cmul(y, wv);
-                }
-                v[i] = y;
-            }
-            if (rd) __syncthreads();  // the previous round's staged rows are stored: the area is scratch again
-            warp_fft1024_2s<true, 32>(v, scr2, s.tw);  // lane t1: X[4 (t1 + 32 t2) + sx]
-            C2P(2);
-#pragma unroll 1
-            for (int half = 0; half < 2; ++half) {
-                __syncthreads();  // transpose slots / previous staging done
-                if (role == half) {
-#pragma unroll
-                    for (int t2 = 0; t2 < 32; ++t2) s.stage[(lane + 32 * t2) * kSP + c] = v[t2];
-                }
-                __syncthreads();
-                const int sxs = 2 * half + rd;  // the delay phase staged by this half's warps
-#pragma unroll 4
-                for (int rr = 0; rr < 1024 * 4 / kPT; ++rr) {
-                    const int idx = tid + kPT * rr;  // 1024 rows x 4 quarters of 16 B
-                    const int p = idx >> 2, qq = idx & 3;
-                    const float2 v0 = s.stage[p * kSP + 2 * qq], v1 = s.stage[p * kSP + 2 * qq + 1];
-                    *reinterpret_cast<float4*>(g + (size_t)(4 * p + sxs) * m + 2 * qq) = make_float4(v0.x, v0.y, v1.x, v1.y);
-                }
-            }
-            C2P(3);
-        }
-        __syncthreads();  // staging and tile free for the next item
-    }
-}
-
 }  // namespace
 
 // cfg2's column pass: N = 2048, N' = 4096, DFT-CE with L <= 256 (or plain LS / H input), G out,
@@ -589,20 +320,6 @@ bool colpass2048_applies(const ColArgs& a, int n, int np) {
 }
 
 cudaError_t launch_colpass2048(const ColArgs& a, int frames, cudaStream_t st) {
-    {
-        const char* e = getenv("OFDMR_COL2048");
-        if (e && e[0] == '2') {  // two warps per column
-            const size_t psmem = sizeof(C2PSmem);
-            cudaError_t er = cudaFuncSetAttribute(colpass2048p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem);
-            if (er != cudaSuccess) return er;
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            const int items = frames * (a.m / kC);
-            colpass2048p_kernel<<<items < sms ? items : sms, kPT, psmem, st>>>(a, frames);
-            return cudaGetLastError();
-        }
-    }
     const size_t smem = sizeof(C2Smem);
     cudaError_t e = cudaFuncSetAttribute(colpass2048_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
